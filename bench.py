@@ -1,0 +1,378 @@
+#!/usr/bin/env python
+"""bench.py -- SSA events/s and verified trajectories/s of the B200 hot path
+(BASELINE.json metric) on one workload, with roofline, CPU-oracle baseline,
+end-to-end and clock records.  One JSON line on rank 0.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C2] [--impl smc|reference]
+
+A step is one pass of the whole hot path over one batch: for a Wilson workload
+(C2, C5) the full Fig. 2 estimate (all rounds: SSA + on-the-fly monitor + counts
++ allreduce + Wilson step); for a fixed-N workload (C1, C3, C4) one smc_run of
+its N replicas.  Default workload: C2 = BASELINE.json configs[1].
+Multi-GPU: one process per GPU (torchrun), NCCL allreduce of the counts per
+round, time = max over ranks.
+"""
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads  # noqa: E402
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+SM_COUNT_DEFAULT = 148
+
+
+def env_rank():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+
+
+# ------------------------------------------------------------- algorithmic work
+def algorithmic_inst_per_event(cfg, variant, dep_sizes, change_sizes, hill_per_event):
+    """Thread-instructions one SSA event must execute:
+    Philox 60, two u53 conversions 10, log 85, IEEE division 40, a0 sum
+    (M adds flat / G group adds two-level), selection (3 per compare: M flat,
+    2 sqrt(M) two-level), state update 2|v|, dependency updates 8|dep(j)|,
+    Hill divisions 80 per Hill law updated, atoms + monitor 15."""
+    M = len(cfg["reactions"])
+    mean_dep = sum(dep_sizes) / M
+    mean_v = sum(change_sizes) / M
+    if variant == 1:
+        a0, sel = M, 3 * M
+    else:
+        a0, sel = math.ceil(M / math.ceil(M / 32)), 3 * 2 * math.sqrt(M)
+    return 60 + 10 + 85 + 40 + a0 + sel + 2 * mean_v + 8 * mean_dep + 80 * hill_per_event + 15
+
+
+def model_stats(cfg):
+    """dep(j) sizes, |v_j| and Hill laws per event of the model (host-side bookkeeping only)."""
+    N, M = len(cfg["species"]), len(cfg["reactions"])
+    reads = []
+    changes = []
+    for r in cfg["reactions"]:
+        s = {a for a, _ in r["reactants"]}
+        if r.get("hill"):
+            s.add(r["hill"]["repressor"])
+        reads.append(s)
+        d = {}
+        for a, st in r["reactants"]:
+            d[a] = d.get(a, 0) - st
+        for a, st in r["products"]:
+            d[a] = d.get(a, 0) + st
+        changes.append({a for a, v in d.items() if v != 0})
+    deps = [[k for k in range(M) if reads[k] & changes[j]] for j in range(M)]
+    hill = [sum(1 for k in deps[j] if cfg["reactions"][k].get("hill")) for j in range(M)]
+    return [len(d) for d in deps], [len(c) for c in changes], sum(hill) / M
+
+
+# ------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampled every 100 ms from before the warm-up to after the timed region;
+    the record keeps the samples inside the timed window (all load samples if the window is
+    shorter than the sampling period)."""
+    FIELDS = ["timestamp", "clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = os.path.join("/tmp", "smc_clocks_%d_%d.csv" % (os.getpid(), gpu_index))
+        self.window = None
+
+    def start(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + ",".join(self.FIELDS),
+                                          "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.fh,
+                                         stderr=subprocess.DEVNULL)
+            time.sleep(0.5)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.fh.close()
+        import datetime
+        rows = []
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) != len(self.FIELDS):
+                continue
+            try:
+                ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                rows.append((ts, float(parts[1]), float(parts[2]), parts[3:]))
+            except ValueError:
+                continue
+        if not rows:
+            return None
+        inside = [r for r in rows if self.window and self.window[0] - 0.1 <= r[0] <= self.window[1] + 0.1]
+        use = inside if inside else [r for r in rows if r[1] > 300.0] or rows
+        sm = sorted(r[1] for r in use)
+        reasons = set()
+        for r in use:
+            for n, v in zip(self.NAMES, r[3]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(r[2] for r in use), "samples": len(use),
+                "in_timed_window": bool(inside), "reasons": sorted(reasons)}
+
+
+# -------------------------------------------------------------- CPU oracle
+def oracle_sample(cfg, budget_s, procs=None, first_chunk=None):
+    """Time the oracle (as it stands) on the workload over `procs` processes.
+    Wilson workloads whose full run fits the budget: the complete Fig. 2 estimate, repeated
+    until `budget_s`.  Otherwise: the first replicas of the workload, in growing chunks,
+    until `budget_s` seconds or the workload is exhausted."""
+    from oracle import oracle as O
+    from oracle import wilson_procedure
+    procs = procs or os.cpu_count() or 1
+    samp = cfg["sampling"]
+    if samp["mode"] == "wilson" and len(cfg["reactions"]) <= 32:
+        t0 = time.perf_counter()
+        ev = tr = runs = 0
+        last = None
+        while True:
+            acc = dict(events=0, n=0)
+
+            def batch(first, n):
+                c, _, _ = O.run_parallel(cfg, cfg["formula"], cfg["seed"], first, n, procs=procs,
+                                         t_max=cfg.get("t_max", 0.0))
+                acc["events"] += c["events"]
+                acc["n"] += n
+                return c["n_true"]
+            last = wilson_procedure(batch, samp["half_width"], samp["confidence"])
+            ev += acc["events"]
+            tr += acc["n"]
+            runs += 1
+            if time.perf_counter() - t0 >= budget_s:
+                break
+        el = time.perf_counter() - t0
+        return dict(events=ev, trajectories=tr, seconds=el, procs=procs, n=last["n_total"], runs=runs,
+                    what="%d complete Fig. 2 estimates (%d replicas each)" % (runs, last["n_total"]))
+    total_n = samp["n"] if samp["mode"] == "fixed" else None
+    chunk = first_chunk or procs * 8
+    first = 0
+    tot = dict(n_true=0, n_false=0, events=0, errors=0)
+    t0 = time.perf_counter()
+    while True:
+        n = chunk if total_n is None else min(chunk, total_n - first)
+        if n <= 0:
+            break
+        c, _, _ = O.run_parallel(cfg, cfg["formula"], cfg["seed"], first, n, procs=procs,
+                                 chunk=max(1, n // (procs * 2)), t_max=cfg.get("t_max", 0.0))
+        for k in tot:
+            tot[k] += c[k]
+        first += n
+        el = time.perf_counter() - t0
+        if el >= budget_s:
+            break
+        chunk = min(chunk * 2, max(procs, int(first / el * (budget_s - el)) + 1))
+    el = time.perf_counter() - t0
+    return dict(events=tot["events"], trajectories=tot["n_true"] + tot["n_false"], seconds=el, procs=procs,
+                n=first, n_true=tot["n_true"], what="the first %d replicas of the workload" % first)
+
+
+def run_reference(args, cfg):
+    rank, _, world = env_rank()
+    if rank != 0:
+        return
+    budget = args.cpu_seconds
+    for _ in range(args.warmup):
+        oracle_sample(cfg, min(2.0, budget))
+    ev = tr = secs = 0.0
+    last = None
+    for _ in range(args.steps):
+        s = oracle_sample(cfg, budget)
+        ev += s["events"]
+        tr += s["trajectories"]
+        secs += s["seconds"]
+        last = s
+    value = ev / secs
+    line = {"impl": "reference", "metric": "SSA events/s", "value": value, "unit": "events/s",
+            "trajectories_per_s": tr / secs, "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000 * secs / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg["name"], "formula": cfg["formula"], "sampling": cfg["sampling"],
+                       "sample_per_step": "%s (time-budgeted %.0f s)" % (last["what"], budget)},
+            "cpu_baseline": {"value": value, "unit": "events/s", "cores": last["procs"], "kind": "oracle",
+                             "sample": "%s per step, %d processes" % (last["what"], last["procs"])},
+            "e2e": {"value": value, "unit": "events/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="C2")
+    ap.add_argument("--impl", default="smc", choices=["smc", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--n", type=int, default=0, help="override fixed-N replica count (diagnostics)")
+    ap.add_argument("--variant", type=int, default=0)
+    args = ap.parse_args()
+    cfg = workloads.get(args.workload)
+    if args.n:
+        cfg = workloads.with_sampling(cfg, mode="fixed", n=args.n)
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_0912_2551_b200 as smc
+    rank, local_rank, world = env_rank()
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    smc.use_torch()
+    if world > 1:
+        smc.set_allreduce_torch(device=True)
+    dev_index = torch.cuda.current_device()
+
+    model = smc.Model.from_config(cfg)
+    if args.variant:
+        model.set_variant(args.variant)
+    prop = smc.Property(model, cfg["formula"], t_max=cfg.get("t_max", 0.0))
+    samp = cfg["sampling"]
+
+    def step():
+        if samp["mode"] == "wilson":
+            est = smc.estimate(model, prop, samp["confidence"], samp["half_width"], cfg["seed"])
+            return est["events"], est["n_total"], est
+        model.reset()
+        c = model.run(prop, samp["n"], cfg["seed"])
+        return c["events"], c["n_true"] + c["n_false"], c
+
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")   # > 126 MB L2
+    clocks = ClockSampler(dev_index)
+    clocks.start()
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    t_window0 = time.time()
+    tot_ms = 0.0
+    tot_kernel_ms = 0.0
+    launches = 0
+    events = trajectories = 0
+    last = None
+    for _ in range(args.steps):
+        flush.fill_(1.0)                       # evict L2 between timed steps (outside the step time)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        ev, tr, last = step()
+        e1.record()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        tot_ms += e0.elapsed_time(e1)
+        info = model.last_launch(prop)
+        tot_kernel_ms += info["kernel_ms"]
+        launches += info["launches"]
+        events += ev
+        trajectories += tr
+    clocks.window = (t_window0, time.time())
+    clk = clocks.stop()
+    if world > 1:
+        t = torch.tensor([tot_ms, tot_kernel_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms, tot_kernel_ms = float(t[0]), float(t[1])
+    # events / trajectories are GLOBAL (the counts are allreduced every round)
+    value = events / (tot_ms / 1e3)
+    traj_s = trajectories / (tot_ms / 1e3)
+
+    # roofline of the dominant kernel (the SSA kernel): SM-issue bound
+    info = model.last_launch(prop)
+    dep_sizes, change_sizes, hill_pe = model_stats(cfg)
+    ipe = algorithmic_inst_per_event(cfg, info["variant"], dep_sizes, change_sizes, hill_pe)
+    peaks = json.load(open(PEAKS_PATH)) if os.path.exists(PEAKS_PATH) else {}
+    sm_mhz = peaks.get("sm_max_mhz", 1965.0)
+    sms = torch.cuda.get_device_properties(dev_index).multi_processor_count
+    peak = sms * 4 * sm_mhz * 1e6 / 1e9           # G warp-instructions / s (1 per SMSP per clock)
+    per_gpu_events = events / world
+    achieved = per_gpu_events * ipe / 32.0 / (tot_kernel_ms / 1e3) / 1e9
+    roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Gwarp-inst/s", "frac": achieved / peak,
+                "traffic": None, "kernel": "smc_ssa_%s" % ("thread" if info["variant"] == 1 else "tile"),
+                "inst_per_event": ipe, "kernel_ms_per_step": tot_kernel_ms / args.steps,
+                "kernel_share_of_step": tot_kernel_ms / tot_ms,
+                "peak_source": "148 SM x 4 SMSP x 1 warp-inst/clk x sm_max_mhz (MEASURED_PEAKS.json)"}
+
+    # end to end through the C ABI with host buffers (model + property built from host arrays,
+    # copies inside the timed region, result read back to the host)
+    e2e_ms = 0.0
+    e2e_events = 0
+    h2d = d2h = 0
+    for _ in range(args.steps):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        m2 = smc.Model.from_config(cfg)
+        if args.variant:
+            m2.set_variant(args.variant)
+        p2 = smc.Property(m2, cfg["formula"], t_max=cfg.get("t_max", 0.0))
+        if samp["mode"] == "wilson":
+            r = smc.estimate(m2, p2, samp["confidence"], samp["half_width"], cfg["seed"])
+            e2e_events += r["events"]
+        else:
+            r = m2.run(p2, samp["n"], cfg["seed"])
+            e2e_events += r["events"]
+        torch.cuda.synchronize()
+        e2e_ms += (time.perf_counter() - t0) * 1e3
+        inf2 = m2.last_launch(p2)
+        h2d = int(inf2["table_bytes"]) + 72 * inf2["launches"]     # tables + kernel parameters
+        d2h = 32 * max(1, inf2["launches"])                        # int64[4] counts per round
+        del p2, m2
+    e2e = {"value": e2e_events / (e2e_ms / 1e3), "unit": "events/s", "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / args.steps}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        s = oracle_sample(cfg, args.cpu_seconds)
+        cpu = {"value": s["events"] / s["seconds"], "unit": "events/s", "cores": s["procs"], "kind": "oracle",
+               "trajectories_per_s": s["trajectories"] / s["seconds"],
+               "sample": "%s of %s (seed %d), %d processes, %.1f s"
+                         % (s["what"], cfg["name"], cfg["seed"], s["procs"], s["seconds"])}
+
+    if rank == 0:
+        line = {"metric": "SSA events/s", "value": value, "unit": "events/s", "trajectories_per_s": traj_s,
+                "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": tot_ms / args.steps,
+                "higher_is_better": True, "scaling": "strong" if samp["mode"] == "wilson" else "strong",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": cfg["name"], "formula": cfg["formula"], "sampling": samp,
+                           "species": len(cfg["species"]), "reactions": len(cfg["reactions"]),
+                           "parallelism": "dp%d" % world, "l2": "flushed (256 MB write) between timed steps",
+                           "variant": info["variant"], "block": info["block_threads"], "grid": info["grid_blocks"],
+                           "regs": info["regs_per_thread"]},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "clocks": clk,
+                "result": {k: last[k] for k in ("p_hat", "lower", "upper", "n_total", "rounds") if k in last}
+                if isinstance(last, dict) else None}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -214,7 +214,9 @@ def run_parallel(cfg, formula_text, seed, first, n, mode="stream", procs=None, c
         tasks.append((cfg, formula_text, cfg["species"], t_max, seed, s, m, mode))
         s += m
     build_oracle()
-    ctx = mp.get_context("fork")
+    # forkserver: workers are forked from a fresh single-threaded server, never from a
+    # process that already holds CUDA / torch threads
+    ctx = mp.get_context("forkserver")
     with cf.ProcessPoolExecutor(max_workers=procs, mp_context=ctx) as ex:
         res = list(ex.map(_worker, tasks))
     tot = dict(n_true=0, n_false=0, events=0, errors=0)

@@ -1,0 +1,361 @@
+// codegen.cpp -- specialise the SSA kernels to one (model, property) pair.
+//
+// Variant 1 (thread-owned): the model is emitted as straight-line code with
+// compile-time species/reaction indices, so x[N] and a[M] stay in registers;
+// the dependency graph becomes one bit-mask test per propensity.
+// Variant 2 (tile): sizes and table offsets become constants; the tables
+// themselves are packed here (pack_tables) and staged to smem by TMA.
+// Both variants get the same generated monitor (reading R16 templates).
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <sstream>
+
+#include "smc_internal.hpp"
+
+namespace smc {
+
+namespace {
+
+std::string dlit(double v) {          // exact double literal
+    if (std::isinf(v)) return v > 0 ? "(1.0/0.0)" : "(-1.0/0.0)";
+    char buf[64];
+    std::snprintf(buf, sizeof buf, "%a", v);
+    return buf;
+}
+std::string ilit(int64_t v) { return "(" + std::to_string(v) + "LL)"; }
+
+// ---------------------------------------------------------------- monitor ---
+struct MonGen {
+    const Property& P;
+    explicit MonGen(const Property& p) : P(p) {}
+
+    std::string atom(int i) const {
+        const Atom& a = P.atoms[(size_t)i];
+        std::string s = "(";
+        for (auto& kv : a.coef) s += "(smc_i64)x[" + std::to_string(kv.first) + "] * " + ilit(kv.second) + " + ";
+        s += ilit(a.cst) + ")";
+        static const char* ops[] = {" < ", " <= ", " >= ", " > ", " == ", " != "};
+        return "(" + s + ops[(int)a.op] + "0LL)";
+    }
+    std::string bexpr(int i) const {
+        if (i < 0) return "true";
+        const BExpr& e = P.bexprs[(size_t)i];
+        switch (e.k) {
+            case BExpr::ATOM: return atom(e.atom);
+            case BExpr::TRUE_: return "true";
+            case BExpr::FALSE_: return "false";
+            case BExpr::NOT: return "(!" + bexpr(e.a) + ")";
+            case BExpr::AND: return "(" + bexpr(e.a) + " && " + bexpr(e.b) + ")";
+            case BExpr::OR: return "(" + bexpr(e.a) + " || " + bexpr(e.b) + ")";
+        }
+        return "false";
+    }
+    static std::string contains(const Interval& I, const char* t) {
+        std::string s = std::string("(") + t + (I.lo_open ? " > " : " >= ") + dlit(I.lo);
+        if (I.finite()) s += std::string(" && ") + t + (I.hi_open ? " < " : " <= ") + dlit(I.hi);
+        return s + ")";
+    }
+    static std::string beyond(const Interval& I, const char* t) {
+        if (!I.finite()) return "false";
+        return std::string("(") + t + (I.hi_open ? " >= " : " > ") + dlit(I.hi) + ")";
+    }
+    std::string root(int i) const {
+        const RootExpr& r = P.root[(size_t)i];
+        switch (r.k) {
+            case RootExpr::LEAF: return "smc_tri(s" + std::to_string(r.leaf) + ")";
+            case RootExpr::NOT: return "smc_knot(" + root(r.a) + ")";
+            case RootExpr::AND: return "smc_kand(" + root(r.a) + ", " + root(r.b) + ")";
+            case RootExpr::OR: return "smc_kor(" + root(r.a) + ", " + root(r.b) + ")";
+        }
+        return "2";
+    }
+
+    std::string emit() const {
+        std::ostringstream o;
+        const size_t L = P.leaves.size();
+        o << "// monitor for: " << P.text << "\n";
+        o << "struct SmcMon {\n";
+        for (size_t i = 0; i < L; ++i) {
+            o << "    unsigned char s" << i << ";\n";
+            const Leaf& lf = P.leaves[i];
+            if (lf.kind == LeafKind::FG || lf.kind == LeafKind::GF) o << "    bool rs" << i << "_set; double rs" << i << ";\n";
+            if (lf.kind == LeafKind::GU) o << "    bool w" << i << "; double D" << i << ";\n";
+        }
+        // init
+        o << "    __device__ __forceinline__ void init() {\n";
+        for (size_t i = 0; i < L; ++i) {
+            o << "        s" << i << " = 0;\n";
+            const Leaf& lf = P.leaves[i];
+            if (lf.kind == LeafKind::FG || lf.kind == LeafKind::GF) o << "        rs" << i << "_set = false; rs" << i << " = 0.0;\n";
+            if (lf.kind == LeafKind::GU) o << "        w" << i << " = false; D" << i << " = 0.0;\n";
+        }
+        o << "    }\n";
+        // enter
+        o << "    template <class XA> __device__ __forceinline__ void enter(smc_u32 k, double t, double tp, const XA& x) {\n";
+        o << "        (void)k; (void)tp;\n";
+        for (size_t i = 0; i < L; ++i) {
+            const Leaf& lf = P.leaves[i];
+            std::string s = "s" + std::to_string(i), id = std::to_string(i);
+            std::string B1 = bexpr(lf.b1), B2 = bexpr(lf.b2);
+            o << "        if (" << s << " == 0) {\n";
+            switch (lf.kind) {
+                case LeafKind::ATOM0: o << "            " << s << " = " << B1 << " ? 1 : 2;\n"; break;
+                case LeafKind::F: o << "            if (" << contains(lf.I, "t") << " && " << B1 << ") " << s << " = 1;\n"; break;
+                case LeafKind::G: o << "            if (" << contains(lf.I, "t") << " && !" << B1 << ") " << s << " = 2;\n"; break;
+                case LeafKind::U:
+                    o << "            if (" << contains(lf.I, "t") << " && " << B2 << ") " << s << " = 1;\n";
+                    o << "            else if (!" << B1 << ") " << s << " = 2;\n";
+                    break;
+                case LeafKind::X:
+                    o << "            if (k == 1u) " << s << " = (" << contains(lf.I, "t") << " && " << B1 << ") ? 1 : 2;\n";
+                    break;
+                case LeafKind::FG:
+                case LeafKind::GF:
+                    o << "            const bool b = " << (lf.kind == LeafKind::GF ? "!" : "") << B1 << ";\n";
+                    o << "            if (!b) rs" << id << "_set = false;\n";
+                    o << "            else if (!rs" << id << "_set && t <= " << dlit(lf.I.hi) << ") { rs" << id
+                      << "_set = true; rs" << id << " = t; }\n";
+                    break;
+                case LeafKind::GU:
+                    o << "            const bool b1 = " << B1 << ";\n";
+                    o << "            if (w" << id << ") { if (!b1) " << s << " = 2; }\n";
+                    o << "            else if (" << B2 << ") {\n";
+                    o << "                if (k == 0u) " << s << " = 1;\n";
+                    o << "                else { w" << id << " = true; D" << id << " = __dadd_rn(tp, " << dlit(lf.J.hi) << ");\n";
+                    o << "                       if (t > D" << id << ") " << s << " = 1; else if (!b1) " << s << " = 2; }\n";
+                    o << "            } else if (!b1) " << s << " = 2;\n";
+                    break;
+            }
+            o << "        }\n";
+        }
+        o << "    }\n";
+        // advance
+        o << "    __device__ __forceinline__ void advance(smc_u32 k, double tn) {\n        (void)k;\n";
+        for (size_t i = 0; i < L; ++i) {
+            const Leaf& lf = P.leaves[i];
+            std::string s = "s" + std::to_string(i), id = std::to_string(i);
+            switch (lf.kind) {
+                case LeafKind::ATOM0: break;
+                case LeafKind::F: case LeafKind::U:
+                    o << "        if (" << s << " == 0 && " << beyond(lf.I, "tn") << ") " << s << " = 2;\n"; break;
+                case LeafKind::G:
+                    o << "        if (" << s << " == 0 && " << beyond(lf.I, "tn") << ") " << s << " = 1;\n"; break;
+                case LeafKind::X:
+                    o << "        if (" << s << " == 0 && k == 0u && !" << contains(lf.I, "tn") << ") " << s << " = 2;\n"; break;
+                case LeafKind::FG:
+                case LeafKind::GF: {
+                    const char* yes = lf.kind == LeafKind::FG ? "1" : "2";
+                    const char* no = lf.kind == LeafKind::FG ? "2" : "1";
+                    o << "        if (" << s << " == 0) {\n";
+                    o << "            if (rs" << id << "_set && tn > __dadd_rn(rs" << id << ", " << dlit(lf.J.hi) << ")) " << s << " = " << yes << ";\n";
+                    o << "            else if (!rs" << id << "_set && tn > " << dlit(lf.I.hi) << ") " << s << " = " << no << ";\n";
+                    o << "        }\n";
+                    break;
+                }
+                case LeafKind::GU:
+                    o << "        if (" << s << " == 0) {\n";
+                    o << "            if (w" << id << ") { if (tn > D" << id << ") " << s << " = 1; }\n";
+                    o << "            else if (tn > " << dlit(lf.I.hi) << ") " << s << " = 2;\n";
+                    o << "        }\n";
+                    break;
+            }
+        }
+        o << "    }\n";
+        // absorb
+        o << "    __device__ __forceinline__ void absorb() {\n";
+        for (size_t i = 0; i < L; ++i) {
+            const Leaf& lf = P.leaves[i];
+            std::string s = "s" + std::to_string(i), id = std::to_string(i);
+            std::string val;
+            switch (lf.kind) {
+                case LeafKind::ATOM0: continue;
+                case LeafKind::F: case LeafKind::U: case LeafKind::X: val = "2"; break;
+                case LeafKind::G: val = "1"; break;
+                case LeafKind::FG: val = "(rs" + id + "_set ? 1 : 2)"; break;
+                case LeafKind::GF: val = "(rs" + id + "_set ? 2 : 1)"; break;
+                case LeafKind::GU: val = "(w" + id + " ? 1 : 2)"; break;
+            }
+            o << "        if (" << s << " == 0) " << s << " = " << val << ";\n";
+        }
+        o << "    }\n";
+        // timeout
+        o << "    __device__ __forceinline__ void timeout() {\n";
+        for (size_t i = 0; i < L; ++i) o << "        if (s" << i << " == 0) s" << i << " = 3;\n";
+        o << "    }\n";
+        // verdict
+        o << "    __device__ __forceinline__ int verdict() const {\n";
+        o << "        const int r = " << root(P.root_idx) << ";\n";
+        o << "        if (r != 2) return r;\n";
+        o << "        if (";
+        for (size_t i = 0; i < L; ++i) o << (i ? " || " : "") << "s" << i << " == 0";
+        o << ") return -1;\n";
+        o << "        return 0;   // unknown at t_max -> false (P:314-317)\n";
+        o << "    }\n};\n";
+        return o.str();
+    }
+};
+
+// ------------------------------------------------- variant 1 model code ---
+std::string law_expr(const Reaction& r) {
+    // h exact in int64, a = c * (double)h, Hill: a / (1 + q^n)
+    std::vector<std::string> terms;
+    for (int q = 0; q < 2; ++q) {
+        if (r.s[q] < 0) continue;
+        std::string xs = "(smc_i64)x[" + std::to_string(r.s[q]) + "]";
+        terms.push_back(r.st[q] == 1 ? xs : "((" + xs + " * (" + xs + " - 1LL)) / 2LL)");
+    }
+    std::string h;
+    if (terms.empty()) h = "1LL";
+    else if (terms.size() == 1) h = terms[0];
+    else h = "(" + terms[0] + " * " + terms[1] + ")";
+    return "__dmul_rn(" + dlit(r.c) + ", (double)(" + h + "))";
+}
+
+std::string model_code_thread(const Model& m) {
+    std::ostringstream o;
+    const int N = m.N, M = m.M;
+    o << "__device__ __forceinline__ void smc_init_x(int (&x)[SMC_N]) {\n";
+    for (int s = 0; s < N; ++s) o << "    x[" << s << "] = " << m.x0[(size_t)s] << ";\n";
+    o << "}\n";
+    for (int k = 0; k < M; ++k) {
+        const Reaction& r = m.R[(size_t)k];
+        o << "__device__ __forceinline__ double smc_law" << k << "(const int (&x)[SMC_N]) {\n";
+        o << "    double a = " << law_expr(r) << ";\n";
+        if (r.hill) {
+            o << "    const double q = __ddiv_rn((double)x[" << r.rep << "], " << dlit(r.K) << ");\n";
+            o << "    double qn = q;\n";
+            for (int i = 1; i < r.n; ++i) o << "    qn = __dmul_rn(qn, q);\n";
+            o << "    a = __ddiv_rn(a, __dadd_rn(1.0, qn));\n";
+        }
+        o << "    return a;\n}\n";
+    }
+    o << "__device__ __forceinline__ void smc_laws_all(double (&a)[SMC_M], const int (&x)[SMC_N]) {\n";
+    for (int k = 0; k < M; ++k) o << "    a[" << k << "] = smc_law" << k << "(x);\n";
+    o << "}\n";
+    // x += v_j, per species; overflow guard only where some delta is positive
+    o << "__device__ __forceinline__ bool smc_apply(int j, int (&x)[SMC_N]) {\n    bool ok = true;\n";
+    for (int s = 0; s < N; ++s) {
+        std::vector<std::pair<int, int>> ds;
+        bool pos = false;
+        for (int j = 0; j < M; ++j)
+            for (auto& ch : m.R[(size_t)j].change)
+                if (ch.first == s) { ds.push_back({j, ch.second}); pos |= ch.second > 0; }
+        if (ds.empty()) continue;
+        std::string sel = "0";
+        for (auto it = ds.rbegin(); it != ds.rend(); ++it)
+            sel = "(j == " + std::to_string(it->first) + " ? " + std::to_string(it->second) + " : " + sel + ")";
+        o << "    { const int d = " << sel << ";\n";
+        if (pos)
+            o << "      const smc_i64 nv = (smc_i64)x[" << s << "] + d; if (nv > 2147483647LL) ok = false; x[" << s << "] = (int)nv; }\n";
+        else
+            o << "      x[" << s << "] += d; }\n";
+    }
+    o << "    return ok;\n}\n";
+    // dependency graph: a_k recomputed iff k in dep(j)
+    o << "__device__ __forceinline__ void smc_update(int j, double (&a)[SMC_M], const int (&x)[SMC_N]) {\n";
+    for (int k = 0; k < M; ++k) {
+        uint64_t mask = 0;
+        for (int j = 0; j < M; ++j)
+            for (int d : m.dep[(size_t)j])
+                if (d == k) mask |= 1ull << j;
+        uint64_t all = (M == 64) ? ~0ull : ((1ull << M) - 1ull);
+        if (mask == 0) continue;
+        if (mask == all) o << "    a[" << k << "] = smc_law" << k << "(x);\n";
+        else o << "    if ((0x" << std::hex << mask << std::dec << "ull >> j) & 1ull) a[" << k << "] = smc_law" << k << "(x);\n";
+    }
+    o << "}\n";
+    o << "__device__ __forceinline__ int smc_last_positive(const double (&a)[SMC_M]) {\n    return ";
+    for (int k = M - 1; k >= 1; --k) o << "a[" << k << "] > 0.0 ? " << k << " : ";
+    o << "0;\n}\n";
+    return o.str();
+}
+
+size_t align16(size_t v) { return (v + 15) & ~(size_t)15; }
+
+}  // namespace
+
+// --------------------------------------------------- variant 2 tables ---
+TileLayout pack_tables(const Model& m) {
+    TileLayout L;
+    const int N = m.N, M = m.M;
+    L.gs = (M + 31) / 32;
+    L.n_pad = (N + 3) & ~3;
+    for (auto& r : m.R) L.any_hill |= r.hill;
+    size_t nnz = 0;
+    for (auto& d : m.dep) { nnz += d.size(); L.max_dep = std::max<int>(L.max_dep, (int)d.size()); }
+    size_t o = 0;
+    L.off_x0 = o; o = align16(o + 4 * (size_t)L.n_pad);
+    L.off_sp = o; o = align16(o + 8 * (size_t)M);
+    L.off_c = o; o = align16(o + 8 * (size_t)M);
+    L.off_hill_rep = o; o = align16(o + (L.any_hill ? 4 * (size_t)M : 0));
+    L.off_hill_k = o; o = align16(o + (L.any_hill ? 8 * (size_t)M : 0));
+    L.off_hill_n = o; o = align16(o + (L.any_hill ? 4 * (size_t)M : 0));
+    L.off_chg = o; o = align16(o + 2 * 4 * (size_t)M);
+    L.off_dep_off = o; o = align16(o + 4 * ((size_t)M + 1));
+    L.off_dep_idx = o; o = align16(o + 2 * nnz);
+    L.bytes = o;
+    L.blob.assign(L.bytes, 0);
+    auto* x0 = (int32_t*)(L.blob.data() + L.off_x0);
+    for (int s = 0; s < N; ++s) x0[s] = m.x0[(size_t)s];
+    auto* sp = (int32_t*)(L.blob.data() + L.off_sp);
+    auto* c = (double*)(L.blob.data() + L.off_c);
+    auto* chg = (uint16_t*)(L.blob.data() + L.off_chg);
+    for (int j = 0; j < M; ++j) {
+        const Reaction& r = m.R[(size_t)j];
+        uint32_t w0 = 0xFFFF, w1 = 0xFFFF;
+        if (r.s[0] >= 0) w0 = (uint32_t)r.s[0] | ((uint32_t)r.st[0] << 16);
+        if (r.s[1] >= 0) w1 = (uint32_t)r.s[1] | ((uint32_t)r.st[1] << 16);
+        if (r.hill) w0 |= 0x80000000u;
+        sp[2 * j] = (int32_t)w0;
+        sp[2 * j + 1] = (int32_t)w1;
+        c[j] = r.c;
+        if (L.any_hill) {
+            ((int32_t*)(L.blob.data() + L.off_hill_rep))[j] = r.hill ? r.rep : 0;
+            ((double*)(L.blob.data() + L.off_hill_k))[j] = r.hill ? r.K : 1.0;
+            ((int32_t*)(L.blob.data() + L.off_hill_n))[j] = r.hill ? r.n : 1;
+        }
+        for (int q = 0; q < 4; ++q) {
+            uint16_t e = 0xFFFF;
+            if (q < (int)r.change.size()) e = (uint16_t)((r.change[(size_t)q].first << 4) | (r.change[(size_t)q].second + 8));
+            chg[4 * j + q] = e;
+        }
+    }
+    auto* doff = (uint32_t*)(L.blob.data() + L.off_dep_off);
+    auto* didx = (uint16_t*)(L.blob.data() + L.off_dep_idx);
+    size_t pos = 0;
+    for (int j = 0; j < M; ++j) {
+        doff[j] = (uint32_t)pos;
+        for (int k : m.dep[(size_t)j]) didx[pos++] = (uint16_t)k;
+    }
+    doff[M] = (uint32_t)pos;
+    return L;
+}
+
+std::string generate_source(const Model& m, const Property& p, int variant, const TileLayout* tl) {
+    std::ostringstream o;
+    o << "// generated by libsmc codegen: model N=" << m.N << " M=" << m.M << ", variant " << variant << "\n";
+    o << "#define SMC_N " << m.N << "\n#define SMC_M " << m.M << "\n";
+    o << "#define SMC_TMAX " << dlit(p.t_max) << "\n";
+    if (variant == 1) {
+        o << "#define SMC_BLOCK 128\n";
+    } else {
+        int gs2 = 1;
+        while (gs2 < tl->gs) gs2 <<= 1;
+        o << "#define SMC_GS " << tl->gs << "\n#define SMC_GS2 " << gs2 << "\n#define SMC_NPAD " << tl->n_pad << "\n";
+        o << "#define SMC_OFF_X0 " << tl->off_x0 << "\n#define SMC_OFF_SP " << tl->off_sp << "\n#define SMC_OFF_C " << tl->off_c
+          << "\n#define SMC_OFF_HREP " << tl->off_hill_rep << "\n#define SMC_OFF_HK " << tl->off_hill_k
+          << "\n#define SMC_OFF_HN " << tl->off_hill_n << "\n#define SMC_OFF_CHG " << tl->off_chg
+          << "\n#define SMC_OFF_DOFF " << tl->off_dep_off << "\n#define SMC_OFF_DIDX " << tl->off_dep_idx << "\n";
+        o << "#define SMC_TAB_BYTES " << tl->bytes << "\n";
+        o << "#define SMC_WARP_BYTES " << (size_t)tl->gs * 32 * 8 + 4 * (size_t)tl->n_pad << "\n";
+        o << "#define SMC_ANY_HILL " << (tl->any_hill ? 1 : 0) << "\n";
+    }
+    o << embedded_source("ssa_common.cuh") << "\n";
+    if (variant == 1) o << model_code_thread(m) << "\n";
+    o << MonGen(p).emit() << "\n";
+    o << embedded_source(variant == 1 ? "ssa_thread.cuh" : "ssa_tile.cuh") << "\n";
+    return o.str();
+}
+
+}  // namespace smc

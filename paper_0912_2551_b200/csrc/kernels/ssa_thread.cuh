@@ -1,0 +1,121 @@
+// ssa_thread.cuh -- variant 1: persistent THREAD-OWNED SSA + monitor kernel.
+//
+// Each lane owns one trajectory; species counts x[N] and propensities a[M]
+// live in registers (every index below is a compile-time constant after the
+// generated model code is inlined).  Lanes whose trajectory is decided are
+// refilled by warp ballot + one warp-aggregated 64-bit atomic on the work
+// cursor (compaction of the finished lanes onto new indices), so a warp keeps
+// all of its lanes busy while paths of different lengths end at different
+// times (P:291-294 on-the-fly halting makes them diverge).
+//
+// Generated hooks (codegen.cpp): SMC_N, SMC_M, SMC_BLOCK, SMC_TMAX,
+//   smc_init_x(x), smc_laws_all(a, x), smc_apply(j, x) -> ok,
+//   smc_update(j, a, x), smc_last_positive(a), struct SmcMon.
+//
+// One event (SSA template P:173-179 with the monitor of P:291-294):
+//   a0 = sum a (fixed order)          step 1
+//   a0 == 0 -> absorbed               step 5 "Terminate", reading R7
+//   tau = -log(u1)/a0, t' = t + tau   step 3, Eq. 2a
+//   monitor.advance(t')               close windows t' passes (may decide)
+//   j = min{j : sum_{i<=j} a_i > u2 a0}  step 2, Eq. 2b
+//   x += v_j; a_k = law_k(x), k in dep(j); t = t'   step 4
+//   monitor.enter(t, x)               (may decide)
+
+extern "C" __global__ void __launch_bounds__(SMC_BLOCK) smc_ssa_thread(SmcParams P) {
+    const smc_u32 lane = threadIdx.x & 31u;
+    int x[SMC_N];
+    double a[SMC_M];
+    double t = 0.0, tp = 0.0;
+    smc_u32 k = 0;
+    smc_u64 rel = 0;
+    SmcMon mon;
+    bool busy = false, exhausted = false;
+    smc_i64 c_true = 0, c_false = 0, c_ev = 0, c_err = 0;
+
+    for (;;) {
+        // ---- refill: compact the idle lanes onto fresh trajectory indices
+        for (;;) {
+            const bool want = !busy && !exhausted;
+            const smc_u32 wm = __ballot_sync(SMC_FULL, want);
+            if (wm == 0u) break;
+            const int leader = __ffs(wm) - 1;
+            smc_u64 base = 0;
+            if ((int)lane == leader) base = atomicAdd(P.cursor, (smc_u64)__popc(wm));
+            base = __shfl_sync(SMC_FULL, base, leader);
+            if (want) {
+                rel = base + (smc_u64)__popc(wm & ((1u << lane) - 1u));
+                if (rel >= P.count) {
+                    exhausted = true;
+                } else {
+                    smc_init_x(x);
+                    smc_laws_all(a, x);
+                    t = 0.0;
+                    tp = 0.0;
+                    k = 0;
+                    mon.init();
+                    mon.enter(0u, 0.0, 0.0, x);          // sigma_buff = {(s0, t0)}
+                    const int v = mon.verdict();
+                    if (v >= 0) {
+                        if (v == 1) ++c_true; else ++c_false;
+                        if (P.verdicts) { P.verdicts[rel] = (unsigned char)v; P.events_out[rel] = 0; }
+                    } else {
+                        busy = true;
+                    }
+                }
+            }
+        }
+        if (!__any_sync(SMC_FULL, busy)) break;
+        if (!busy) continue;
+
+        // ---- one SSA event of this lane's trajectory
+        double c[SMC_M];
+        c[0] = a[0];
+#pragma unroll
+        for (int m = 1; m < SMC_M; ++m) c[m] = __dadd_rn(c[m - 1], a[m]);
+        const double A = c[SMC_M - 1];
+        int v = -1;
+        if (!(A >= 0.0) || A > 1.7976931348623157e308) {
+            v = 2;                                        // bad propensity
+        } else if (A == 0.0) {
+            mon.absorb();
+            v = mon.verdict();
+        } else {
+            double e, u2;
+            smc_draw(P.seed, P.first + rel, (smc_u64)k, e, u2);
+            const double tn = __dadd_rn(t, __ddiv_rn(e, A));
+            mon.advance(k, tn);
+            v = mon.verdict();
+            if (v < 0 && SMC_TMAX > 0.0 && tn > SMC_TMAX) {
+                mon.timeout();
+                v = mon.verdict();
+            }
+            if (v < 0) {
+                const double target = __dmul_rn(u2, A);
+                int j = 0;
+#pragma unroll
+                for (int m = 0; m < SMC_M; ++m) j += (c[m] <= target) ? 1 : 0;   // c is non-decreasing
+                if (j == SMC_M) j = smc_last_positive(a);                      // rounding (reading R11)
+                if (!smc_apply(j, x)) {
+                    v = 2;                                                     // count overflow
+                } else {
+                    smc_update(j, a, x);
+                    tp = t;
+                    t = tn;
+                    ++k;
+                    mon.enter(k, t, tp, x);
+                    v = mon.verdict();
+                    if (v < 0 && (smc_u64)k >= P.event_cap) v = 2;
+                }
+            }
+        }
+        if (v >= 0) {
+            if (v == 1) ++c_true;
+            else if (v == 0) ++c_false;
+            else ++c_err;
+            c_ev += k;
+            if (P.verdicts) { P.verdicts[rel] = (unsigned char)v; P.events_out[rel] = (int)k; }
+            busy = false;
+        }
+    }
+    smc_flush_counts(c_true, c_false, c_ev, c_err, P.counters);
+}

@@ -1,0 +1,433 @@
+// runtime.cpp -- the round driver: device buffers (through the allocator
+// hook), launch configuration of the persistent kernels, shard slices,
+// counters, the allreduce hook, and the iterative Wilson loop of Fig. 2.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <functional>
+
+#include "smc_internal.hpp"
+
+// AOT kernel launcher (aot_kernels.cu)
+cudaError_t smc_launch_philox_debug(uint64_t seed, uint64_t traj, uint64_t step0, uint32_t n, uint32_t* dev_out,
+                                    cudaStream_t stream);
+
+namespace smc {
+
+Hooks& hooks() {
+    static Hooks h;
+    return h;
+}
+
+namespace {
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(SMC_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+cudaStream_t stream() { return (cudaStream_t)hooks().stream; }
+
+void* dalloc(size_t bytes) {
+    Hooks& h = hooks();
+    void* p = nullptr;
+    if (h.alloc) {
+        p = h.alloc(bytes, h.alloc_user);
+        if (!p) fail(SMC_E_CUDA, "allocator hook returned NULL");
+    } else {
+        ck(cudaMalloc(&p, bytes), "cudaMalloc");
+    }
+    return p;
+}
+void dfree(void* p) {
+    if (!p) return;
+    Hooks& h = hooks();
+    if (h.free_) h.free_(p, h.alloc_user);
+    else cudaFree(p);
+}
+
+}  // namespace
+
+struct PropKernel {
+    std::shared_ptr<Kernel> k;
+    std::string source;
+    int variant = 1;
+    int block = 128;
+    int grid_max = 0;
+    int smem = 0;
+    smc_launch_info info{};
+};
+
+struct DeviceState {
+    void* tables = nullptr;
+    TileLayout layout;
+    bool tables_ready = false;
+    void* ctl = nullptr;            // [0..8) cursor, [16..48) counters
+    int64_t* host_counts = nullptr; // pinned
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    int sm_count = 0, max_smem_optin = 0;
+    std::map<uint64_t, PropKernel> kernels;
+    ~DeviceState() {
+        if (e0) cudaEventDestroy(e0);
+        if (e1) cudaEventDestroy(e1);
+        if (host_counts) cudaFreeHost(host_counts);
+        dfree(ctl);
+        dfree(tables);
+    }
+    int64_t* counters() { return (int64_t*)((char*)ctl + 16); }
+};
+
+void DeviceStateDeleter::operator()(DeviceState* d) const { delete d; }
+
+namespace {
+
+DeviceState& device(Model& m) {
+    if (!m.dev) {
+        int n = 0;
+        ck(cudaGetDeviceCount(&n), "cudaGetDeviceCount");
+        if (n < 1) fail(SMC_E_CUDA, "no CUDA device");
+        auto d = std::make_unique<DeviceState>();
+        int dev = 0;
+        ck(cudaGetDevice(&dev), "cudaGetDevice");
+        ck(cudaDeviceGetAttribute(&d->sm_count, cudaDevAttrMultiProcessorCount, dev), "attr");
+        ck(cudaDeviceGetAttribute(&d->max_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev), "attr");
+        d->ctl = dalloc(64);
+        ck(cudaMallocHost((void**)&d->host_counts, 64), "cudaMallocHost");
+        ck(cudaEventCreate(&d->e0), "cudaEventCreate");
+        ck(cudaEventCreate(&d->e1), "cudaEventCreate");
+        m.dev.reset(d.release());
+    }
+    return *m.dev;
+}
+
+PropKernel& prepare(Model& m, const Property& p) {
+    DeviceState& d = device(m);
+    auto it = d.kernels.find(p.id);
+    if (it != d.kernels.end()) return it->second;
+    m.build_deps();
+    PropKernel pk;
+    pk.variant = m.variant();
+    const TileLayout* tl = nullptr;
+    if (pk.variant == 2) {
+        if (!d.tables_ready) {
+            d.layout = pack_tables(m);
+            d.tables = dalloc(d.layout.bytes);
+            ck(cudaMemcpyAsync(d.tables, d.layout.blob.data(), d.layout.bytes, cudaMemcpyHostToDevice, stream()),
+               "upload tables");
+            ck(cudaStreamSynchronize(stream()), "sync");
+            d.tables_ready = true;
+        }
+        tl = &d.layout;
+    }
+    pk.source = generate_source(m, p, pk.variant, tl);
+    pk.k = get_kernel(pk.source, pk.variant == 1 ? "smc_ssa_thread" : "smc_ssa_tile");
+    const void* fn = (const void*)pk.k->kernel;
+    if (pk.variant == 1) {
+        pk.block = 128;
+        int nb = 0;
+        ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, pk.block, 0), "occupancy");
+        pk.grid_max = std::max(1, nb) * d.sm_count;
+        pk.smem = 0;
+    } else {
+        const size_t wb = (size_t)tl->gs * 32 * 8 + 4 * (size_t)tl->n_pad;
+        cudaFuncAttributes fa;
+        ck(cudaFuncGetAttributes(&fa, fn), "cudaFuncGetAttributes");
+        const size_t max_dyn = (size_t)d.max_smem_optin - fa.sharedSizeBytes;
+        ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)max_dyn), "smem attr");
+        int best_total = 0, best_w = 0, best_nb = 0;
+        for (int W : {16, 12, 8, 6, 4, 2, 1}) {
+            size_t smem = tl->bytes + (size_t)W * wb;
+            if (smem > max_dyn) continue;
+            int nb = 0;
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, W * 32, smem) != cudaSuccess) continue;
+            if (nb * W > best_total) { best_total = nb * W; best_w = W; best_nb = nb; }
+        }
+        if (!best_total) fail(SMC_E_CUDA, "tile kernel: model tables do not fit in shared memory");
+        pk.block = best_w * 32;
+        pk.smem = (int)(tl->bytes + (size_t)best_w * wb);
+        pk.grid_max = best_nb * d.sm_count;
+    }
+    pk.info.variant = pk.variant;
+    pk.info.block_threads = pk.block;
+    pk.info.smem_bytes = pk.smem;
+    pk.info.regs_per_thread = pk.k->regs;
+    pk.info.compile_ms = pk.k->compile_ms;
+    pk.info.table_bytes = pk.variant == 2 ? (double)tl->bytes : 0.0;
+    return d.kernels.emplace(p.id, std::move(pk)).first->second;
+}
+
+// Launch one slice asynchronously on the stream; counters stay on the device.
+void launch_slice(Model& m, PropKernel& pk, uint64_t seed, uint64_t lo, uint64_t hi, uint8_t* dev_verdict,
+                  int32_t* dev_events) {
+    DeviceState& d = *m.dev;
+    ck(cudaMemsetAsync(d.ctl, 0, 64, stream()), "memset counters");
+    if (hi <= lo) return;
+    const uint64_t count = hi - lo;
+    struct Params {
+        unsigned long long seed, first, count;
+        unsigned long long* cursor;
+        long long* counters;
+        unsigned char* verdicts;
+        int* events_out;
+        unsigned long long event_cap;
+        const void* tables;
+    } P{seed, lo, count, (unsigned long long*)d.ctl, (long long*)d.counters(), dev_verdict, dev_events, m.event_cap,
+        d.tables};
+    const uint64_t per_block = pk.variant == 1 ? (uint64_t)pk.block : (uint64_t)(pk.block / 32);
+    const uint64_t need = (count + per_block - 1) / per_block;
+    const int grid = (int)std::min<uint64_t>((uint64_t)pk.grid_max, need);
+    void* args[] = {&P};
+    ck(cudaEventRecord(d.e0, stream()), "event");
+    ck(cudaLaunchKernel((const void*)pk.k->kernel, dim3((unsigned)grid), dim3((unsigned)pk.block), args,
+                        (size_t)pk.smem, stream()),
+       "cudaLaunchKernel");
+    ck(cudaEventRecord(d.e1, stream()), "event");
+    pk.info.grid_blocks = grid;
+    pk.info.launches += 1;
+}
+
+void finish_timing(Model& m, PropKernel& pk, bool launched) {
+    if (!launched) return;
+    float ms = 0.f;
+    ck(cudaEventElapsedTime(&ms, m.dev->e0, m.dev->e1), "cudaEventElapsedTime");
+    pk.info.kernel_ms += ms;
+}
+
+}  // namespace
+
+int run_round(Model& m, const Property& p, uint64_t seed, uint64_t base, uint64_t n, smc_counts* out) {
+    PropKernel& pk = prepare(m, p);
+    Hooks& h = hooks();
+    uint64_t lo = base, hi = base + n;
+    if (h.world > 1) smc_shard_range(base, n, h.rank, h.world, &lo, &hi);
+    launch_slice(m, pk, seed, lo, hi, nullptr, nullptr);
+    ck(cudaGetLastError(), "kernel launch");
+    if (h.allreduce) {
+        if (h.allreduce(m.dev->counters(), 4, h.allreduce_user) != 0) fail(SMC_E_COMM, "allreduce hook failed");
+    }
+    ck(cudaMemcpyAsync(m.dev->host_counts, m.dev->counters(), 32, cudaMemcpyDeviceToHost, stream()), "D2H counts");
+    ck(cudaStreamSynchronize(stream()), "cudaStreamSynchronize");
+    finish_timing(m, pk, hi > lo);
+    out->n_true = m.dev->host_counts[0];
+    out->n_false = m.dev->host_counts[1];
+    out->events = m.dev->host_counts[2];
+    out->errors = m.dev->host_counts[3];
+    return SMC_OK;
+}
+
+// ------------------------------------------------------------ Fig. 2 ---
+namespace {
+// The Fig. 2 loop over any round runner (global counts).
+template <class Runner>
+int wilson_loop(Runner&& run, double confidence, double eps, double start, smc_estimate_t* out) {
+    std::memset(out, 0, sizeof *out);
+    const double z = normal_quantile(confidence);
+    out->z = z;
+    int64_t N = wilson_sample_size(start, eps, z);       // "N = Wilson_Sample(1, epsilon, alpha)"
+    uint64_t cursor = 0;                                 // next trajectory index
+    int64_t n_tot = 0, yes = 0;
+    for (int round = 0; round < 100000; ++round) {
+        smc_counts c{};
+        int rc = run(cursor, (uint64_t)N, &c);           // "Perform N experiments"
+        if (rc != SMC_OK) return rc;
+        cursor += (uint64_t)N;
+        n_tot += c.n_true + c.n_false;                   // errors excluded from trials
+        yes += c.n_true;
+        out->events += c.events;
+        out->errors += c.errors;
+        out->rounds = round + 1;
+        out->n_total = n_tot;
+        out->n_true = yes;
+        if ((double)out->errors > 0.01 * (double)cursor) {
+            set_error("more than 1% of replicas ended in error (overflow / event cap / bad propensity)");
+            return SMC_E_ERRRATE;
+        }
+        if (n_tot == 0) { N = 1; continue; }
+        const double p_est = (double)yes / (double)n_tot;   // "pest = yess" (reading W2)
+        out->p_hat = p_est;
+        const double p_prime = round_estimate(p_est, eps);
+        const int64_t n_prime = wilson_sample_size(p_prime, eps, z);
+        const int64_t n_new = n_prime - n_tot;
+        if (n_new > 0) { N = n_new; continue; }
+        wilson_interval(p_est, (double)n_tot, z, &out->lower, &out->upper);
+        return SMC_OK;
+    }
+    set_error("Wilson loop did not terminate");
+    return SMC_E_ARG;
+}
+
+int guard(const std::function<int()>& f) {
+    try {
+        return f();
+    } catch (const Error& e) {
+        set_error(e.msg);
+        return e.code;
+    } catch (const std::exception& e) {
+        set_error(e.what());
+        return SMC_E_ARG;
+    }
+}
+}  // namespace
+
+}  // namespace smc
+
+using namespace smc;
+
+extern "C" {
+
+int smc_set_allocator(void* (*alloc)(size_t, void*), void (*free_)(void*, void*), void* user) {
+    if ((alloc == nullptr) != (free_ == nullptr)) { set_error("smc_set_allocator: set both or neither"); return SMC_E_ARG; }
+    hooks().alloc = alloc;
+    hooks().free_ = free_;
+    hooks().alloc_user = user;
+    return SMC_OK;
+}
+int smc_set_stream(void* s) { hooks().stream = s; return SMC_OK; }
+int smc_set_shard(int32_t rank, int32_t world) {
+    if (world < 1 || rank < 0 || rank >= world) { set_error("smc_set_shard: need 0 <= rank < world"); return SMC_E_ARG; }
+    hooks().rank = rank;
+    hooks().world = world;
+    return SMC_OK;
+}
+int smc_set_allreduce(int (*fn)(int64_t*, int32_t, void*), void* user) {
+    hooks().allreduce = fn;
+    hooks().allreduce_user = user;
+    return SMC_OK;
+}
+
+int smc_reset(smc_model* h) {
+    if (!h) { set_error("smc_reset: NULL"); return SMC_E_ARG; }
+    std::lock_guard<std::mutex> lk(h->m.mu);
+    h->m.cursor = 0;
+    return SMC_OK;
+}
+
+int smc_run(smc_model* h, const smc_property* ph, uint64_t n, uint64_t seed, smc_counts* out) {
+    if (!h || !ph || !out) { set_error("smc_run: NULL argument"); return SMC_E_ARG; }
+    return guard([&] {
+        Model& m = h->m;
+        std::lock_guard<std::mutex> lk(m.mu);
+        if (!m.has_seed || m.last_seed != seed) { m.cursor = 0; m.last_seed = seed; m.has_seed = true; }
+        PropKernel& pk = prepare(m, *ph->p);
+        pk.info.launches = 0;
+        pk.info.kernel_ms = 0.f;
+        int rc = run_round(m, *ph->p, seed, m.cursor, n, out);
+        if (rc == SMC_OK) m.cursor += n;
+        return rc;
+    });
+}
+
+int smc_estimate(smc_model* h, const smc_property* ph, double confidence, double half_width, uint64_t seed,
+                 smc_estimate_t* out) {
+    if (!h || !ph || !out || !(confidence > 0 && confidence < 1) || !(half_width > 0 && half_width < 0.5)) {
+        set_error("smc_estimate: need model, property, out, confidence in (0,1), half_width in (0,0.5)");
+        return SMC_E_ARG;
+    }
+    return guard([&] {
+        Model& m = h->m;
+        std::lock_guard<std::mutex> lk(m.mu);
+        PropKernel& pk = prepare(m, *ph->p);
+        pk.info.launches = 0;
+        pk.info.kernel_ms = 0.f;
+        return wilson_loop(
+            [&](uint64_t base, uint64_t n, smc_counts* c) { return run_round(m, *ph->p, seed, base, n, c); },
+            confidence, half_width, 1.0, out);
+    });
+}
+
+int smc_estimate_with_runner(smc_run_fn run, void* user, double confidence, double half_width, double start,
+                             smc_estimate_t* out) {
+    if (!run || !out || !(confidence > 0 && confidence < 1) || !(half_width > 0 && half_width < 0.5) ||
+        !(start >= 0 && start <= 1)) {
+        set_error("smc_estimate_with_runner: bad arguments");
+        return SMC_E_ARG;
+    }
+    return guard([&] {
+        return wilson_loop(
+            [&](uint64_t base, uint64_t n, smc_counts* c) -> int {
+                Hooks& hk = hooks();
+                uint64_t lo = base, hi = base + n;
+                if (hk.world > 1) smc_shard_range(base, n, hk.rank, hk.world, &lo, &hi);
+                smc_counts local{};
+                if (hi > lo) {
+                    int rc = run(lo, hi - lo, user, &local);
+                    if (rc != 0) { set_error("runner callback failed"); return SMC_E_ARG; }
+                }
+                int64_t buf[4] = {local.n_true, local.n_false, local.events, local.errors};
+                // with a runner the counts live in HOST memory; the hook sums them in place
+                if (hk.allreduce && hk.allreduce(buf, 4, hk.allreduce_user) != 0) {
+                    set_error("allreduce hook failed");
+                    return SMC_E_COMM;
+                }
+                c->n_true = buf[0];
+                c->n_false = buf[1];
+                c->events = buf[2];
+                c->errors = buf[3];
+                return SMC_OK;
+            },
+            confidence, half_width, start, out);
+    });
+}
+
+int smc_run_verdicts(smc_model* h, const smc_property* ph, uint64_t first, uint64_t n, uint64_t seed,
+                     uint8_t* dev_verdict, int32_t* dev_events) {
+    if (!h || !ph || !dev_verdict || !dev_events) { set_error("smc_run_verdicts: NULL argument"); return SMC_E_ARG; }
+    return guard([&] {
+        Model& m = h->m;
+        std::lock_guard<std::mutex> lk(m.mu);
+        PropKernel& pk = prepare(m, *ph->p);
+        pk.info.launches = 0;
+        pk.info.kernel_ms = 0.f;
+        launch_slice(m, pk, seed, first, first + n, dev_verdict, dev_events);
+        ck(cudaGetLastError(), "kernel launch");
+        ck(cudaStreamSynchronize(stream()), "cudaStreamSynchronize");
+        finish_timing(m, pk, n > 0);
+        return SMC_OK;
+    });
+}
+
+int smc_philox_blocks(uint64_t seed, uint64_t trajectory, uint64_t step0, uint32_t n, uint32_t* host_out) {
+    if (!host_out) { set_error("smc_philox_blocks: NULL"); return SMC_E_ARG; }
+    return guard([&] {
+        void* d = dalloc((size_t)n * 16 + 16);
+        try {
+            ck(smc_launch_philox_debug(seed, trajectory, step0, n, (uint32_t*)d, stream()), "philox kernel");
+            ck(cudaMemcpyAsync(host_out, d, (size_t)n * 16, cudaMemcpyDeviceToHost, stream()), "D2H");
+            ck(cudaStreamSynchronize(stream()), "sync");
+        } catch (...) {
+            dfree(d);
+            throw;
+        }
+        dfree(d);
+        return SMC_OK;
+    });
+}
+
+int smc_last_launch(const smc_model* h, const smc_property* ph, smc_launch_info* out) {
+    if (!h || !ph || !out) { set_error("smc_last_launch: NULL"); return SMC_E_ARG; }
+    const Model& m = h->m;
+    if (!m.dev) { set_error("smc_last_launch: no run yet"); return SMC_E_ARG; }
+    auto it = m.dev->kernels.find(ph->p->id);
+    if (it == m.dev->kernels.end()) { set_error("smc_last_launch: no run of this property"); return SMC_E_ARG; }
+    *out = it->second.info;
+    return SMC_OK;
+}
+
+int smc_kernel_source(smc_model* h, const smc_property* ph, char* buf, size_t* len) {
+    if (!h || !ph || !len) { set_error("smc_kernel_source: NULL"); return SMC_E_ARG; }
+    return guard([&] {
+        Model& m = h->m;
+        std::lock_guard<std::mutex> lk(m.mu);
+        m.build_deps();
+        const int v = m.variant();
+        TileLayout tl;
+        if (v == 2) tl = pack_tables(m);
+        std::string s = generate_source(m, *ph->p, v, v == 2 ? &tl : nullptr);
+        size_t need = s.size() + 1;
+        if (buf) std::memcpy(buf, s.c_str(), std::min(*len, need));
+        *len = need;
+        return SMC_OK;
+    });
+}
+
+}  // extern "C"

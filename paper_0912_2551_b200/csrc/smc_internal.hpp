@@ -1,0 +1,162 @@
+// smc_internal.hpp -- host-side data structures of libsmc (B200 path).
+// Independent of oracle/: nothing here is shared with the CPU oracle.
+#pragma once
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/smc.h"
+
+namespace smc {
+
+// ---------------------------------------------------------------- errors ---
+void set_error(const std::string& msg);
+struct Error {
+    int code;
+    std::string msg;
+};
+[[noreturn]] void fail(int code, const std::string& msg);
+
+// ----------------------------------------------------------------- model ---
+// One reaction channel R_j after normalisation.
+struct Reaction {
+    int s[2] = {-1, -1};     // reactant species (merged), -1 = none
+    int st[2] = {0, 0};      // stoichiometry 1..2
+    std::vector<std::pair<int, int>> change;   // (species, delta != 0), species ascending
+    double c = 0.0;
+    bool hill = false;
+    int rep = -1;
+    double K = 0.0;
+    int n = 0;
+};
+
+struct Kernel;        // compiled + loaded module (jit.cpp)
+struct DeviceState;   // device buffers (runtime.cpp)
+struct DeviceStateDeleter { void operator()(DeviceState* d) const; };
+
+struct Model {
+    int N = 0, M = 0;
+    std::vector<int32_t> x0;
+    std::vector<Reaction> R;
+    int variant_forced = 0;
+    uint64_t event_cap = 2147483647ull;
+    // dependency graph: dep[j] = { k : species(law_k) intersects changed(j) }
+    std::vector<std::vector<int>> dep;
+    bool deps_built = false;
+    // run state
+    uint64_t cursor = 0;
+    uint64_t last_seed = 0;
+    bool has_seed = false;
+    std::unique_ptr<DeviceState, DeviceStateDeleter> dev;
+    std::mutex mu;
+    void build_deps();
+    std::vector<int> law_species(int k) const;   // species read by a_k
+    int variant() const;                          // 1 thread-owned, 2 tile
+};
+
+// -------------------------------------------------------------- property ---
+enum class Cmp { LT, LE, GE, GT, EQ, NE };
+struct Atom {                       // sum_s coef[s] x_s + cst  (cmp)  0, exact int64
+    std::vector<std::pair<int, int64_t>> coef;
+    int64_t cst = 0;
+    Cmp op = Cmp::GT;
+};
+struct Interval {
+    double lo = 0.0, hi = 0.0;      // hi = +inf when unbounded
+    bool lo_open = false, hi_open = false;
+    bool finite() const;
+};
+// boolean expression over atoms: postfix-free tree
+struct BExpr {
+    enum K { ATOM, TRUE_, FALSE_, NOT, AND, OR } k;
+    int atom = -1;
+    int a = -1, b = -1;
+};
+enum class LeafKind { ATOM0, F, G, U, X, FG, GF, GU };
+struct Leaf {
+    LeafKind kind;
+    Interval I, J;       // outer / inner interval
+    int b1 = -1, b2 = -1;   // BExpr roots (-1 = tt)
+};
+struct RootExpr {        // Kleene combination of leaves
+    enum K { LEAF, NOT, AND, OR } k;
+    int leaf = -1;
+    int a = -1, b = -1;
+};
+struct Property {
+    uint64_t id = 0;
+    std::string text;
+    int N = 0;
+    double t_max = 0.0;
+    std::vector<Atom> atoms;
+    std::vector<BExpr> bexprs;
+    std::vector<Leaf> leaves;
+    std::vector<RootExpr> root;
+    int root_idx = -1;
+    double horizon = 0.0;
+};
+std::unique_ptr<Property> compile_property(const Model& m, const std::string& text,
+                                           const std::vector<std::string>& names, double t_max);
+
+// --------------------------------------------------------------- codegen ---
+struct TileLayout {               // packed model tables (variant 2), byte offsets
+    int gs = 0;                   // reactions per lane group
+    int n_pad = 0;
+    size_t off_x0 = 0, off_sp = 0, off_c = 0, off_hill_rep = 0, off_hill_k = 0, off_hill_n = 0;
+    size_t off_chg = 0, off_dep_off = 0, off_dep_idx = 0, bytes = 0;
+    bool any_hill = false;
+    int max_dep = 0;
+    std::vector<uint8_t> blob;    // host copy
+};
+TileLayout pack_tables(const Model& m);
+std::string generate_source(const Model& m, const Property& p, int variant, const TileLayout* tl);
+std::string embedded_source(const char* name);   // kernels/*.cuh embedded at build time
+
+// -------------------------------------------------------------------- jit ---
+struct Kernel {
+    void* library = nullptr;      // cudaLibrary_t
+    void* kernel = nullptr;       // cudaKernel_t
+    int regs = 0;
+    float compile_ms = 0.f;
+    std::string name;
+};
+std::shared_ptr<Kernel> get_kernel(const std::string& source, const char* entry);
+
+// --------------------------------------------------------------- runtime ---
+struct LaunchRecord {
+    smc_launch_info info{};
+};
+struct Hooks {
+    void* (*alloc)(size_t, void*) = nullptr;
+    void (*free_)(void*, void*) = nullptr;
+    void* alloc_user = nullptr;
+    void* stream = nullptr;
+    int rank = 0, world = 1;
+    int (*allreduce)(int64_t*, int32_t, void*) = nullptr;
+    void* allreduce_user = nullptr;
+};
+Hooks& hooks();
+
+// counts of one shard slice [lo, hi) (device kernel), no allreduce
+int run_slice(Model& m, const Property& p, uint64_t seed, uint64_t lo, uint64_t hi, smc_counts* local,
+              uint8_t* dev_verdict, int32_t* dev_events);
+// global counts of round range [base, base+n): shard + allreduce
+int run_round(Model& m, const Property& p, uint64_t seed, uint64_t base, uint64_t n, smc_counts* out);
+
+// ---------------------------------------------------------------- wilson ---
+double normal_quantile(double c);
+void wilson_interval(double p_hat, double n, double z, double* lo, double* hi);
+int64_t wilson_sample_size(double p, double eps, double z);
+double round_estimate(double p_hat, double eps);
+
+}  // namespace smc
+
+struct smc_model {
+    smc::Model m;
+};
+struct smc_property {
+    std::unique_ptr<smc::Property> p;
+};

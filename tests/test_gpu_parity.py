@@ -1,0 +1,254 @@
+"""GPU parity: the CUDA path through the C ABI against the oracle, element by
+element, on identical seeded inputs (north star bar: Philox and Wilson
+bit-exact; per-replica verdicts agree on >= 99.99 %; p-hat within 5e-4 at
+10^6 samples; estimates inside the 99 % Wilson interval of the closed form)."""
+import math
+
+import numpy as np
+import pytest
+
+import workloads
+from oracle import normal_quantile, wilson_interval, wilson_procedure
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+AGREE = 0.9999     # per-replica verdict agreement (log rounding may differ, north star)
+
+
+@pytest.fixture(scope="module")
+def smc():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("gpu test without a GPU")
+    import paper_0912_2551_b200 as smc
+    smc.use_torch()
+    return smc
+
+
+def _pair(smc, cfg, variant=0):
+    m = smc.Model.from_config(cfg)
+    if variant:
+        m.set_variant(variant)
+    p = smc.Property(m, cfg["formula"], t_max=cfg.get("t_max", 0.0))
+    return m, p
+
+
+def _oracle(cfg, seed, first, n, procs=None):
+    if n * 1 <= 4000 or procs == 1:
+        om = O.OracleModel(cfg)
+        of = O.OracleFormula(cfg["formula"], cfg["species"], cfg.get("t_max", 0.0))
+        return O.run(om, of, seed, first, n)
+    return O.run_parallel(cfg, cfg["formula"], seed, first, n, procs=procs, t_max=cfg.get("t_max", 0.0))
+
+
+def _compare(smc, cfg, seed, first, n, variant=0, oracle=None):
+    m, p = _pair(smc, cfg, variant)
+    v, e = m.run_verdicts(p, first, n, seed)
+    v, e = v.cpu().numpy(), e.cpu().numpy().astype(np.int64)
+    oc, ov, oe = oracle if oracle is not None else _oracle(cfg, seed, first, n)
+    agree_v = float((v == ov).mean())
+    agree_ve = float(((v == ov) & (e == oe)).mean())
+    return agree_v, agree_ve, v, e, ov, oe
+
+
+def test_philox_stream_bit_exact(smc):
+    for seed, traj, step0 in [(1, 0, 0), (2**64 - 1, 2**40 + 7, 2**33), (12345, 999_999, 17_000)]:
+        blocks = smc.smc_philox_blocks(seed, traj, step0, 64)
+        for q, b in enumerate(blocks):
+            assert b == O.philox(seed, traj, step0 + q)
+
+
+@pytest.mark.parametrize("variant", [1, 2])
+def test_c1_all_replicas(smc, variant):
+    cfg = workloads.c1()
+    a, ae, v, e, ov, oe = _compare(smc, cfg, cfg["seed"], 0, 10_000, variant)
+    assert a >= AGREE and ae >= AGREE
+    assert list(v[:3]) == [0, 0, 1] and list(e[:3]) == [9, 7, 10]     # worked example
+    exact = (1 - math.exp(-2.0)) ** 10
+    z = normal_quantile(0.99)
+    lo, hi = wilson_interval(v.sum() / 10_000, 10_000, z)
+    assert lo <= exact <= hi
+
+
+@pytest.mark.parametrize("variant", [1, 2])
+def test_c2_replicas(smc, variant):
+    cfg = workloads.c2()
+    a, ae, *_ = _compare(smc, cfg, cfg["seed"], 0, 3000, variant)
+    assert a >= AGREE and ae >= AGREE
+
+
+def test_c2_wilson_estimate(smc):
+    """C2 (configs[1]): Fig. 2 at 99 %, eps = 0.005; identical to the oracle's loop on the same
+    stream; both contain the exact P = 0.2146528874 (uniformisation)."""
+    cfg = workloads.c2()
+    m, p = _pair(smc, cfg)
+    est = smc.estimate(m, p, 0.99, 0.005, cfg["seed"])
+    om = O.OracleModel(cfg)
+    of = O.OracleFormula(cfg["formula"], cfg["species"])
+
+    def batch(first, n):
+        c, _, _ = O.run_parallel(cfg, cfg["formula"], cfg["seed"], first, n)
+        return c["n_true"]
+    ref = wilson_procedure(batch, 0.005, 0.99)
+    assert abs(est["p_hat"] - ref["p_hat"]) <= 5e-4
+    assert abs(est["n_total"] - ref["n_total"]) <= 0.01 * ref["n_total"]
+    exact = 0.2146528874
+    assert est["lower"] <= exact <= est["upper"]
+    assert ref["lower"] <= exact <= ref["upper"]
+    assert est["errors"] == 0
+    del om, of
+
+
+@pytest.mark.parametrize("variant", [1, 2])
+def test_c3_replicas(smc, variant):
+    cfg = workloads.c3()
+    a, ae, *_ = _compare(smc, cfg, cfg["seed"], 0, 400, variant)
+    assert a >= 0.995 and ae >= 0.995          # 400 replicas: one flip allowed at most
+    assert a == 1.0 or a * 400 >= 399
+
+
+def test_c3r_stress(smc):
+    cfg = workloads.c3r()
+    a, ae, *_ = _compare(smc, cfg, cfg["seed"], 0, 3000)
+    assert a >= AGREE
+
+
+def test_c3_full_size_sampled(smc):
+    """Full C3 size (10^6 replicas) in the bench launch configuration; the oracle checks a sample."""
+    cfg = workloads.c3()
+    m, p = _pair(smc, cfg)
+    n = cfg["sampling"]["n"]
+    v, e = m.run_verdicts(p, 0, n, cfg["seed"])
+    v, e = v.cpu().numpy(), e.cpu().numpy()
+    assert set(np.unique(v)) <= {0, 1}
+    g = np.random.default_rng(0)
+    idx = np.sort(g.choice(n, 64, replace=False))
+    om = O.OracleModel(cfg)
+    of = O.OracleFormula(cfg["formula"], cfg["species"])
+    bad = 0
+    for i in idx:
+        c, ov, oe = O.run(om, of, cfg["seed"], int(i), 1)
+        bad += int(ov[0] != v[i] or oe[0] != e[i])
+    assert bad <= 1
+    # counts path == per-replica path on the same indices
+    m.reset()
+    c = m.run(p, n, cfg["seed"])
+    assert c["n_true"] == int(v.sum()) and c["events"] == int(e.astype(np.int64).sum())
+    assert abs(c["n_true"] / n - 0.512) < 0.02          # survey pilot p ~ 0.512 (sanity, not a pin)
+
+
+def test_edge_cases(smc):
+    cfg = workloads.c1()
+    m, p = _pair(smc, cfg)
+    assert m.run(p, 0, 1) == dict(n_true=0, n_false=0, events=0, errors=0)
+    c1 = m.run(p, 1, 1)
+    assert c1["n_true"] + c1["n_false"] == 1
+    # absorbing start: A0 = 0 -> a0 = 0 at sigma[0]; F(A == 0) decided at entry 0 without events
+    z = dict(cfg, x0=[0])
+    m0, p0 = _pair(smc, z)
+    assert m0.run(p0, 1000, 3) == dict(n_true=1000, n_false=0, events=0, errors=0)
+    m1 = smc.Model.from_config(z)
+    p1 = smc.Property(m1, "G[0,5](A == 1)")
+    assert m1.run(p1, 10, 3) == dict(n_true=0, n_false=10, events=0, errors=0)
+    p2 = smc.Property(m1, "F[0,5](A == 1)")            # absorbed immediately -> F false
+    assert m1.run(p2, 10, 3)["n_false"] == 10
+    # event cap -> counted as errors
+    m2, p2 = _pair(smc, workloads.c2())
+    m2.set_event_cap(5)
+    c = m2.run(p2, 100, 2)
+    assert c["errors"] == 100 and c["events"] == 500
+    # count overflow -> error: birth from near INT32_MAX
+    big = dict(species=["A"], x0=[2147483640], reactions=[dict(reactants=[], products=[[0, 2]], rate=1.0, hill=None)],
+               formula="F[0,100](A < 0)")
+    m3, p3 = _pair(smc, big)
+    c = m3.run(p3, 50, 1)
+    assert c["errors"] == 50 and c["events"] == 50 * 3
+    # unbounded formula with t_max (pessimistic), oracle parity
+    cfgu = dict(cfg, formula="F(A == 0)", t_max=1.5)
+    a, ae, *_ = _compare(smc, cfgu, 9, 0, 5000)
+    assert a >= AGREE and ae >= AGREE
+
+
+@pytest.mark.parametrize("formula", [
+    "G[0,1](A >= 8)", "(A >= 7) U[0.2,1.5] (A <= 5)", "X[0,0.3](A == 9)", "F[0,1] G[0,0.5](A <= 6)",
+    "G[0,1.5] F[0,0.3](A >= 5)", "(G[0,0.5](A > 3)) U[0,2] (A <= 6)", "F(0.5,2](A == 7) & !G[0,0.2](A == 10)",
+    "(A == 10) | F[0,0.1](A < 9)"])
+def test_templates_vs_oracle(smc, formula):
+    cfg = dict(workloads.c1(), formula=formula)
+    for variant in (1, 2):
+        a, ae, *_ = _compare(smc, cfg, 4, 0, 5000, variant)
+        assert a >= AGREE and ae >= AGREE, (formula, variant, a, ae)
+
+
+def test_shard_invariance(smc):
+    """Same (seed, n) split over G emulated ranks (no allreduce) sums to the unsharded counts."""
+    cfg = workloads.c2()
+    m, p = _pair(smc, cfg)
+    whole = m.run(p, 20_000, 11)
+    for G in (2, 4, 8):
+        tot = dict(n_true=0, n_false=0, events=0, errors=0)
+        for r in range(G):
+            smc.smc_set_shard(r, G)
+            m.reset()
+            c = m.run(p, 20_000, 11)
+            for k in tot:
+                tot[k] += c[k]
+        smc.smc_set_shard(0, 1)
+        assert tot == whole
+
+
+@pytest.mark.parametrize("name", ["C4", "C5"])
+def test_large_networks_vs_oracle_fixture(smc, name):
+    """Tile variant (smem/TMA-staged tables) vs the oracle's per-replica verdicts and event
+    counts (tests/golden/<cfg>_oracle.json, written by scripts/make_fixtures.py from oracle/ only)."""
+    import json
+    import os
+    fx = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "%s_oracle.json" % name.lower())))
+    cfg = workloads.get(name)
+    assert fx["formula"] == cfg["formula"] and fx["seed"] == cfg["seed"]
+    m, p = _pair(smc, cfg)
+    v, e = m.run_verdicts(p, fx["first"], fx["n"], fx["seed"])
+    v, e = v.cpu().numpy(), e.cpu().numpy()
+    ov, oe = np.array(fx["verdicts"]), np.array(fx["events"])
+    mism = int(((v != ov) | (e != oe)).sum())
+    assert mism <= 1, (name, mism)           # ulp-level flips only (readings R12/S11)
+    assert m.last_launch(p)["variant"] == 2
+
+
+def test_c4_full_size_shard_sampled(smc):
+    """C4 (configs[3]: 10^7 replicas over 8 GPUs): rank 0's shard of 1.25e6 replicas in the bench
+    launch configuration; the oracle checks sampled replicas one by one."""
+    cfg = workloads.c4()
+    lo, hi = smc.smc_shard_range(0, cfg["sampling"]["n"], 0, 8)
+    m, p = _pair(smc, cfg)
+    v, e = m.run_verdicts(p, lo, hi - lo, cfg["seed"])
+    v, e = v.cpu().numpy(), e.cpu().numpy()
+    assert set(np.unique(v)) <= {0, 1}
+    idx = np.sort(np.random.default_rng(1).choice(hi - lo, 16, replace=False))
+    om = O.OracleModel(cfg)
+    of = O.OracleFormula(cfg["formula"], cfg["species"])
+    bad = 0
+    for i in idx:
+        c, ov, oe = O.run(om, of, cfg["seed"], int(lo + i), 1)
+        bad += int(ov[0] != v[i] or oe[0] != e[i])
+    assert bad == 0
+    assert abs(v.mean() - 0.54) < 0.03          # fixture estimate 0.5415 (2000 oracle replicas)
+
+
+def test_c5_first_round_sampled(smc):
+    """C5 (configs[4]): the first Fig. 2 round at 99.9 %, eps = 1e-4 (54,128 replicas), sampled."""
+    cfg = workloads.c5()
+    n = smc.smc_wilson_sample_size(1.0, 1e-4, 0.999)
+    assert n == 54128
+    m, p = _pair(smc, cfg)
+    v, e = m.run_verdicts(p, 0, n, cfg["seed"])
+    v, e = v.cpu().numpy(), e.cpu().numpy()
+    idx = np.sort(np.random.default_rng(2).choice(n, 6, replace=False))
+    om = O.OracleModel(cfg)
+    of = O.OracleFormula(cfg["formula"], cfg["species"])
+    bad = 0
+    for i in idx:
+        c, ov, oe = O.run(om, of, cfg["seed"], int(i), 1)
+        bad += int(ov[0] != v[i] or oe[0] != e[i])
+    assert bad == 0

@@ -1,0 +1,138 @@
+"""libsmc.so on a machine without a GPU: it loads, exports every symbol of
+include/smc.h, and its HOST logic is right (Wilson bit-exact with the oracle,
+property compiler, codegen, shard ranges, the Fig. 2 driver).  No kernel runs."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+import workloads
+import paper_0912_2551_b200 as smc
+from paper_0912_2551_b200 import _native
+from oracle import normal_quantile, wilson_interval, wilson_procedure, wilson_sample_size
+from oracle import oracle as O
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    text = open(os.path.join(ROOT, "include", "smc.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(smc_[a-z_]+)\s*\(", text)) - {"smc_run_fn"})
+
+
+def test_exports_every_declared_symbol():
+    L = smc.lib()
+    syms = header_symbols()
+    assert len(syms) == 24
+    for s in syms:
+        assert hasattr(L, s), s
+    assert sorted(n for n, _, _ in _native.SIGNATURES) == syms
+
+
+CONF = [0.8, 0.9, 0.95, 0.99, 0.995, 0.999, 0.9999, 0.99999]
+
+
+@pytest.mark.parametrize("c", CONF)
+def test_z_bit_exact(c):
+    assert smc.smc_normal_quantile(c) == normal_quantile(c)
+
+
+def test_wilson_interval_bit_exact():
+    g = np.random.default_rng(1)
+    for _ in range(3000):
+        n = int(g.integers(1, 10**8))
+        k = int(g.integers(0, n + 1)) if g.random() < 0.8 else int(g.choice([0, n]))
+        c = float(g.choice(CONF))
+        lo, hi = smc.smc_wilson_interval(k, n, c)
+        olo, ohi = wilson_interval(k / n, n, normal_quantile(c))
+        assert (lo, hi) == (olo, ohi)
+
+
+def test_wilson_sample_size_bit_exact():
+    g = np.random.default_rng(2)
+    for _ in range(3000):
+        p = float(g.random()) if g.random() < 0.9 else float(g.choice([0.0, 0.5, 1.0]))
+        eps = float(g.choice([0.1, 0.05, 0.025, 0.01, 0.005, 1e-3, 1e-4]))
+        c = float(g.choice(CONF))
+        assert smc.smc_wilson_sample_size(p, eps, c) == wilson_sample_size(p, eps, normal_quantile(c))
+    assert smc.smc_wilson_sample_size(0.5, 0.025, 0.99) == 2648
+
+
+def test_shard_ranges_partition():
+    for n in [0, 1, 7, 1000, 10**7 + 3]:
+        for world in [1, 2, 3, 4, 8]:
+            parts = [smc.smc_shard_range(100, n, r, world) for r in range(world)]
+            assert parts[0][0] == 100 and parts[-1][1] == 100 + n
+            for (a, b), (c, d) in zip(parts, parts[1:]):
+                assert b == c and a <= b
+            sizes = [b - a for a, b in parts]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def test_model_validation_lists_all_violations():
+    bad = dict(species=["A", "B"], x0=[-1, 3],
+               reactions=[dict(reactants=[[5, 1]], products=[], rate=1.0),
+                          dict(reactants=[[0, 1]], products=[[1, 1]], rate=-2.0)])
+    with pytest.raises(smc.SmcError) as e:
+        smc.Model.from_config(bad)
+    assert e.value.name == "SMC_E_MODEL"
+    msg = str(e.value)
+    assert "init_counts[0]" in msg and "reaction 0" in msg and "reaction 1" in msg
+
+
+def test_property_compiler_errors():
+    m = smc.Model.from_config(workloads.c2())
+    with pytest.raises(smc.SmcError) as e:
+        smc.Property(m, "F[0,50](Q > 500)")
+    assert e.value.name == "SMC_E_PARSE" and "unknown species" in str(e.value)
+    with pytest.raises(smc.SmcError) as e:
+        smc.Property(m, "F[0,50](P > )")
+    assert e.value.name == "SMC_E_PARSE"
+    with pytest.raises(smc.SmcError) as e:
+        smc.Property(m, "F[0,50](P * S > 5)")
+    assert e.value.name == "SMC_E_UNSUPPORTED"
+    with pytest.raises(smc.SmcError) as e:
+        smc.Property(m, "F[0,5](G[1,2](P > 5))")
+    assert e.value.name == "SMC_E_UNSUPPORTED"
+    with pytest.raises(smc.SmcError) as e:
+        smc.Property(m, "F(P > 5)")                 # unbounded needs t_max
+    assert e.value.name == "SMC_E_UNSUPPORTED"
+    for ok in ["F(P > 5)", "(E <= 4) U (P >= 5)", "G[0,1](2*ES - P + 3 != 0) & !X[0,1](S == 1000)",
+               "F[0,10] G[0,1](E > S)", "(G[0,100](E < 400)) U[0,200] (P > 300)", "F(0,1.5](P >= 2) | true"]:
+        smc.Property(m, ok, t_max=100.0)
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4"])
+def test_codegen_source(name):
+    cfg = workloads.get(name)
+    m = smc.Model.from_config(cfg)
+    p = smc.Property(m, cfg["formula"])
+    src = m.kernel_source(p)
+    assert "struct SmcMon" in src
+    assert ("smc_ssa_thread" in src) == (len(cfg["reactions"]) <= 32)
+
+
+def _oracle_runner(cfg, seed, stats):
+    om = O.OracleModel(cfg)
+    of = O.OracleFormula(cfg["formula"], cfg["species"])
+
+    def run(first, n):
+        c, _, _ = O.run(om, of, seed, first, n, per_traj=False)
+        stats.append((first, n))
+        return c
+    return run
+
+
+def test_fig2_driver_matches_oracle_loop():
+    """The library's Fig. 2 loop (host C++) == the oracle's (Python) on the same replica stream."""
+    cfg = workloads.c1()
+    calls = []
+    lib_est = smc.estimate_with_runner(_oracle_runner(cfg, 7, calls), 0.99, 0.01)
+    om = O.OracleModel(cfg)
+    of = O.OracleFormula(cfg["formula"], cfg["species"])
+    ref = wilson_procedure(lambda f, n: O.run(om, of, 7, f, n, per_traj=False)[0]["n_true"], 0.01, 0.99)
+    assert lib_est["n_total"] == ref["n_total"] and lib_est["n_true"] == ref["n_true"]
+    assert (lib_est["p_hat"], lib_est["lower"], lib_est["upper"]) == (ref["p_hat"], ref["lower"], ref["upper"])
+    assert lib_est["rounds"] == ref["rounds"] == len(calls)
