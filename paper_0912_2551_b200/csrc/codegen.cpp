@@ -218,9 +218,13 @@ std::string model_code_thread(const Model& m) {
     o << "__device__ __forceinline__ void smc_init_x(int (&x)[SMC_N]) {\n";
     for (int s = 0; s < N; ++s) o << "    x[" << s << "] = " << m.x0[(size_t)s] << ";\n";
     o << "}\n";
+    const HillTables ht = pack_hill_tables(m);
     for (int k = 0; k < M; ++k) {
         const Reaction& r = m.R[(size_t)k];
-        o << "__device__ __forceinline__ double smc_law" << k << "(const int (&x)[SMC_N]) {\n";
+        o << "__device__ __forceinline__ double smc_law" << k << "(const int (&x)[SMC_N], const double* __restrict__ H) {\n";
+        if (ht.offset[(size_t)k] >= 0)   // zero-order Hill law: a_k(x_r) tabulated (same IEEE ops, host side)
+            o << "    if (x[" << r.rep << "] < " << ht.size << ") return __ldg(H + " << ht.offset[(size_t)k] << " + x["
+              << r.rep << "]);\n";
         o << "    double a = " << law_expr(r) << ";\n";
         if (r.hill) {
             o << "    const double q = __ddiv_rn((double)x[" << r.rep << "], " << dlit(r.K) << ");\n";
@@ -230,8 +234,8 @@ std::string model_code_thread(const Model& m) {
         }
         o << "    return a;\n}\n";
     }
-    o << "__device__ __forceinline__ void smc_laws_all(double (&a)[SMC_M], const int (&x)[SMC_N]) {\n";
-    for (int k = 0; k < M; ++k) o << "    a[" << k << "] = smc_law" << k << "(x);\n";
+    o << "__device__ __forceinline__ void smc_laws_all(double (&a)[SMC_M], const int (&x)[SMC_N], const double* __restrict__ H) {\n";
+    for (int k = 0; k < M; ++k) o << "    a[" << k << "] = smc_law" << k << "(x, H);\n";
     o << "}\n";
     // x += v_j, per species; overflow guard only where some delta is positive
     o << "__device__ __forceinline__ bool smc_apply(int j, int (&x)[SMC_N]) {\n    bool ok = true;\n";
@@ -253,7 +257,7 @@ std::string model_code_thread(const Model& m) {
     }
     o << "    return ok;\n}\n";
     // dependency graph: a_k recomputed iff k in dep(j)
-    o << "__device__ __forceinline__ void smc_update(int j, double (&a)[SMC_M], const int (&x)[SMC_N]) {\n";
+    o << "__device__ __forceinline__ void smc_update(int j, double (&a)[SMC_M], const int (&x)[SMC_N], const double* __restrict__ H) {\n";
     for (int k = 0; k < M; ++k) {
         uint64_t mask = 0;
         for (int j = 0; j < M; ++j)
@@ -261,8 +265,8 @@ std::string model_code_thread(const Model& m) {
                 if (d == k) mask |= 1ull << j;
         uint64_t all = (M == 64) ? ~0ull : ((1ull << M) - 1ull);
         if (mask == 0) continue;
-        if (mask == all) o << "    a[" << k << "] = smc_law" << k << "(x);\n";
-        else o << "    if ((0x" << std::hex << mask << std::dec << "ull >> j) & 1ull) a[" << k << "] = smc_law" << k << "(x);\n";
+        if (mask == all) o << "    a[" << k << "] = smc_law" << k << "(x, H);\n";
+        else o << "    if ((0x" << std::hex << mask << std::dec << "ull >> j) & 1ull) a[" << k << "] = smc_law" << k << "(x, H);\n";
     }
     o << "}\n";
     o << "__device__ __forceinline__ int smc_last_positive(const double (&a)[SMC_M]) {\n    return ";
@@ -274,6 +278,25 @@ std::string model_code_thread(const Model& m) {
 size_t align16(size_t v) { return (v + 15) & ~(size_t)15; }
 
 }  // namespace
+
+// --------------------------------------------------- variant 1 tables ---
+HillTables pack_hill_tables(const Model& m) {
+    HillTables h;
+    h.offset.assign((size_t)m.M, -1);
+    for (int k = 0; k < m.M; ++k) {
+        const Reaction& r = m.R[(size_t)k];
+        if (!r.hill || r.s[0] >= 0 || r.s[1] >= 0) continue;
+        h.offset[(size_t)k] = (long long)h.values.size();
+        for (int x = 0; x < h.size; ++x) {
+            double a = r.c * (double)1LL;          // c * h with h = 1
+            const double q = (double)x / r.K;
+            double qn = q;
+            for (int i = 1; i < r.n; ++i) qn = qn * q;
+            h.values.push_back(a / (1.0 + qn));
+        }
+    }
+    return h;
+}
 
 // --------------------------------------------------- variant 2 tables ---
 TileLayout pack_tables(const Model& m) {

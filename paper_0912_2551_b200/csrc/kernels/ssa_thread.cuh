@@ -8,9 +8,14 @@
 // all of its lanes busy while paths of different lengths end at different
 // times (P:291-294 on-the-fly halting makes them diverge).
 //
+// The random draw of step k+1 (Philox + log, ~150 instructions) does not
+// depend on the state, so it is issued at the top of step k and overlaps the
+// state-dependent chain of step k (a0 -> tau -> monitor -> select -> update).
+//
 // Generated hooks (codegen.cpp): SMC_N, SMC_M, SMC_BLOCK, SMC_TMAX,
-//   smc_init_x(x), smc_laws_all(a, x), smc_apply(j, x) -> ok,
-//   smc_update(j, a, x), smc_last_positive(a), struct SmcMon.
+//   smc_init_x(x), smc_laws_all(a, x, H), smc_apply(j, x) -> ok,
+//   smc_update(j, a, x, H), smc_last_positive(a), struct SmcMon.
+//   H = P.tables: tabulated Hill propensities (zero-order Hill laws, x_r < table size).
 //
 // One event (SSA template P:173-179 with the monitor of P:291-294):
 //   a0 = sum a (fixed order)          step 1
@@ -23,11 +28,13 @@
 
 extern "C" __global__ void __launch_bounds__(SMC_BLOCK) smc_ssa_thread(SmcParams P) {
     const smc_u32 lane = threadIdx.x & 31u;
+    const double* __restrict__ H = (const double*)P.tables;
     int x[SMC_N];
     double a[SMC_M];
     double t = 0.0, tp = 0.0;
+    double e_cur = 0.0, u_cur = 0.0;      // draw of the current step k
     smc_u32 k = 0;
-    smc_u64 rel = 0;
+    smc_u64 rel = 0, traj = 0;
     SmcMon mon;
     bool busy = false, exhausted = false;
     smc_i64 c_true = 0, c_false = 0, c_ev = 0, c_err = 0;
@@ -47,8 +54,9 @@ extern "C" __global__ void __launch_bounds__(SMC_BLOCK) smc_ssa_thread(SmcParams
                 if (rel >= P.count) {
                     exhausted = true;
                 } else {
+                    traj = P.first + rel;
                     smc_init_x(x);
-                    smc_laws_all(a, x);
+                    smc_laws_all(a, x, H);
                     t = 0.0;
                     tp = 0.0;
                     k = 0;
@@ -60,6 +68,7 @@ extern "C" __global__ void __launch_bounds__(SMC_BLOCK) smc_ssa_thread(SmcParams
                         if (P.verdicts) { P.verdicts[rel] = (unsigned char)v; P.events_out[rel] = 0; }
                     } else {
                         busy = true;
+                        smc_draw(P.seed, traj, 0ull, e_cur, u_cur);
                     }
                 }
             }
@@ -80,9 +89,9 @@ extern "C" __global__ void __launch_bounds__(SMC_BLOCK) smc_ssa_thread(SmcParams
             mon.absorb();
             v = mon.verdict();
         } else {
-            double e, u2;
-            smc_draw(P.seed, P.first + rel, (smc_u64)k, e, u2);
-            const double tn = __dadd_rn(t, __ddiv_rn(e, A));
+            double e_nx, u_nx;                            // step k+1's draw, off the critical path
+            smc_draw(P.seed, traj, (smc_u64)k + 1ull, e_nx, u_nx);
+            const double tn = __dadd_rn(t, __ddiv_rn(e_cur, A));
             mon.advance(k, tn);
             v = mon.verdict();
             if (v < 0 && SMC_TMAX > 0.0 && tn > SMC_TMAX) {
@@ -90,7 +99,7 @@ extern "C" __global__ void __launch_bounds__(SMC_BLOCK) smc_ssa_thread(SmcParams
                 v = mon.verdict();
             }
             if (v < 0) {
-                const double target = __dmul_rn(u2, A);
+                const double target = __dmul_rn(u_cur, A);
                 int j = 0;
 #pragma unroll
                 for (int m = 0; m < SMC_M; ++m) j += (c[m] <= target) ? 1 : 0;   // c is non-decreasing
@@ -98,10 +107,12 @@ extern "C" __global__ void __launch_bounds__(SMC_BLOCK) smc_ssa_thread(SmcParams
                 if (!smc_apply(j, x)) {
                     v = 2;                                                     // count overflow
                 } else {
-                    smc_update(j, a, x);
+                    smc_update(j, a, x, H);
                     tp = t;
                     t = tn;
                     ++k;
+                    e_cur = e_nx;
+                    u_cur = u_nx;
                     mon.enter(k, t, tp, x);
                     v = mon.verdict();
                     if (v < 0 && (smc_u64)k >= P.event_cap) v = 2;

@@ -89,7 +89,7 @@ __device__ __forceinline__ int smc_aidx(int j) {     // swizzled slot of reactio
     return m * 32 + (l ^ m);
 }
 
-extern "C" __global__ void __launch_bounds__(512) smc_ssa_tile(SmcParams P) {
+extern "C" __global__ void __launch_bounds__(512, 1) smc_ssa_tile(SmcParams P) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ __align__(8) unsigned long long bar;
     const smc_u32 lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;

@@ -55,13 +55,15 @@ struct PropKernel {
     int block = 128;
     int grid_max = 0;
     int smem = 0;
+    const void* tables = nullptr;
     smc_launch_info info{};
 };
 
 struct DeviceState {
-    void* tables = nullptr;
+    void* tables[3] = {nullptr, nullptr, nullptr};   // per variant: [1] Hill tables, [2] tile tables
+    size_t table_bytes[3] = {0, 0, 0};
+    bool tables_ready[3] = {false, false, false};
     TileLayout layout;
-    bool tables_ready = false;
     void* ctl = nullptr;            // [0..8) cursor, [16..48) counters
     int64_t* host_counts = nullptr; // pinned
     cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -72,7 +74,7 @@ struct DeviceState {
         if (e1) cudaEventDestroy(e1);
         if (host_counts) cudaFreeHost(host_counts);
         dfree(ctl);
-        dfree(tables);
+        for (void* t : tables) dfree(t);
     }
     int64_t* counters() { return (int64_t*)((char*)ctl + 16); }
 };
@@ -108,17 +110,30 @@ PropKernel& prepare(Model& m, const Property& p) {
     PropKernel pk;
     pk.variant = m.variant();
     const TileLayout* tl = nullptr;
-    if (pk.variant == 2) {
-        if (!d.tables_ready) {
+    const int v = pk.variant;
+    if (!d.tables_ready[v]) {
+        const void* src = nullptr;
+        size_t bytes = 0;
+        HillTables ht;
+        if (v == 2) {
             d.layout = pack_tables(m);
-            d.tables = dalloc(d.layout.bytes);
-            ck(cudaMemcpyAsync(d.tables, d.layout.blob.data(), d.layout.bytes, cudaMemcpyHostToDevice, stream()),
-               "upload tables");
-            ck(cudaStreamSynchronize(stream()), "sync");
-            d.tables_ready = true;
+            src = d.layout.blob.data();
+            bytes = d.layout.bytes;
+        } else {
+            ht = pack_hill_tables(m);
+            src = ht.values.data();
+            bytes = ht.values.size() * sizeof(double);
         }
-        tl = &d.layout;
+        if (bytes) {
+            d.tables[v] = dalloc(bytes);
+            ck(cudaMemcpyAsync(d.tables[v], src, bytes, cudaMemcpyHostToDevice, stream()), "upload tables");
+            ck(cudaStreamSynchronize(stream()), "sync");
+        }
+        d.table_bytes[v] = bytes;
+        d.tables_ready[v] = true;
     }
+    if (v == 2) tl = &d.layout;
+    pk.tables = d.tables[v];
     pk.source = generate_source(m, p, pk.variant, tl);
     pk.k = get_kernel(pk.source, pk.variant == 1 ? "smc_ssa_thread" : "smc_ssa_tile");
     const void* fn = (const void*)pk.k->kernel;
@@ -152,7 +167,7 @@ PropKernel& prepare(Model& m, const Property& p) {
     pk.info.smem_bytes = pk.smem;
     pk.info.regs_per_thread = pk.k->regs;
     pk.info.compile_ms = pk.k->compile_ms;
-    pk.info.table_bytes = pk.variant == 2 ? (double)tl->bytes : 0.0;
+    pk.info.table_bytes = (double)d.table_bytes[v];
     return d.kernels.emplace(p.id, std::move(pk)).first->second;
 }
 
@@ -172,7 +187,7 @@ void launch_slice(Model& m, PropKernel& pk, uint64_t seed, uint64_t lo, uint64_t
         unsigned long long event_cap;
         const void* tables;
     } P{seed, lo, count, (unsigned long long*)d.ctl, (long long*)d.counters(), dev_verdict, dev_events, m.event_cap,
-        d.tables};
+        pk.tables};
     const uint64_t per_block = pk.variant == 1 ? (uint64_t)pk.block : (uint64_t)(pk.block / 32);
     const uint64_t need = (count + per_block - 1) / per_block;
     const int grid = (int)std::min<uint64_t>((uint64_t)pk.grid_max, need);

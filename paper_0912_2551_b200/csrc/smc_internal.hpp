@@ -112,6 +112,14 @@ struct TileLayout {               // packed model tables (variant 2), byte offse
     std::vector<uint8_t> blob;    // host copy
 };
 TileLayout pack_tables(const Model& m);
+// variant 1: zero-order Hill propensities a_k(x_r), x_r < size, tabulated on the host with
+// the same IEEE operations as the law (one __ldg instead of two divisions per update)
+struct HillTables {
+    int size = 2048;
+    std::vector<long long> offset;   // per reaction, -1 = not tabulated
+    std::vector<double> values;
+};
+HillTables pack_hill_tables(const Model& m);
 std::string generate_source(const Model& m, const Property& p, int variant, const TileLayout* tl);
 std::string embedded_source(const char* name);   // kernels/*.cuh embedded at build time
 
