@@ -91,6 +91,14 @@ int smc_model_set_variant(smc_model* m, int32_t variant);
  * counted as an error.  cap >= 1. */
 int smc_model_set_event_cap(smc_model* m, uint64_t cap);
 
+/* smc_estimate runs each Fig. 2 round prefix-exactly from a speculative batch
+ * (default on = 1): a round range not yet simulated starts a batch of
+ * max(needed, min(resident capacity of all GPUs, Eq. 4(0.5) - start)) replicas
+ * whose per-replica results later rounds consume by index.  Fig. 2 reads only
+ * prefixes of the index stream, so the estimate is identical with 0 (off:
+ * exactly the round's replicas per launch); only the time changes.  SMC_E_ARG on NULL. */
+int smc_model_set_speculation(smc_model* m, int32_t on);
+
 void smc_model_destroy(smc_model* m);
 
 /* ------------------------------------------------------------------------ */

@@ -39,6 +39,7 @@ SIGNATURES = [
     ("smc_model_set_hill", c_i32, [c_vp, c_i32, c_i32, c_dbl, c_i32]),
     ("smc_model_set_variant", c_i32, [c_vp, c_i32]),
     ("smc_model_set_event_cap", c_i32, [c_vp, c_u64]),
+    ("smc_model_set_speculation", c_i32, [c_vp, c_i32]),
     ("smc_model_destroy", None, [c_vp]),
     ("smc_property_compile", c_i32, [c_vp, ctypes.c_char_p, c_vp, c_dbl, ctypes.POINTER(c_vp)]),
     ("smc_property_destroy", None, [c_vp]),

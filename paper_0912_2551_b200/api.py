@@ -64,6 +64,9 @@ class Model:
     def set_event_cap(self, cap):
         check(lib().smc_model_set_event_cap(self.h, cap))
 
+    def set_speculation(self, on):
+        check(lib().smc_model_set_speculation(self.h, 1 if on else 0))
+
     def reset(self):
         check(lib().smc_reset(self.h))
 

@@ -19,6 +19,30 @@ __global__ void smc_philox_debug(smc_u64 seed, smc_u64 traj, smc_u64 step0, smc_
     out[4 * q + 3] = r[3];
 }
 
+// Counts of the replicas [i0, i1) of a speculative batch whose per-replica
+// verdicts / event counts sit at v[i - base], e[i - base] (prefix-exact Wilson
+// rounds).  Adds into counters {n_true, n_false, events, errors}.
+__global__ void smc_count_range(const unsigned char* __restrict__ v, const int* __restrict__ e, smc_u64 n,
+                                smc_i64* counters) {
+    smc_i64 ct = 0, cf = 0, ce = 0, cr = 0;
+    for (smc_u64 i = (smc_u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (smc_u64)gridDim.x * blockDim.x) {
+        const unsigned char vv = v[i];
+        ct += vv == 1;
+        cf += vv == 0;
+        cr += vv == 2;
+        ce += e[i];
+    }
+    smc_flush_counts(ct, cf, ce, cr, counters);
+}
+
+cudaError_t smc_launch_count_range(const unsigned char* v, const int* e, uint64_t n, long long* counters,
+                                   cudaStream_t stream) {
+    if (n == 0) return cudaSuccess;
+    const uint64_t blocks = (n + 255) / 256;
+    smc_count_range<<<(unsigned)(blocks < 592 ? blocks : 592), 256, 0, stream>>>(v, e, n, counters);
+    return cudaGetLastError();
+}
+
 cudaError_t smc_launch_philox_debug(uint64_t seed, uint64_t traj, uint64_t step0, uint32_t n, uint32_t* dev_out,
                                     cudaStream_t stream) {
     if (n == 0) return cudaSuccess;

@@ -8,6 +8,7 @@
 // Both variants get the same generated monitor (reading R16 templates).
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <sstream>
 
@@ -185,6 +186,10 @@ struct MonGen {
         o << "    }\n";
         // verdict
         o << "    __device__ __forceinline__ int verdict() const {\n";
+        if (L == 1 && P.root[(size_t)P.root_idx].k == RootExpr::LEAF) {   // root is the leaf itself
+            o << "        return s0 == 0 ? -1 : (s0 == 1 ? 1 : 0);   // unknown -> false (P:314-317)\n    }\n};\n";
+            return o.str();
+        }
         o << "        const int r = " << root(P.root_idx) << ";\n";
         o << "        if (r != 2) return r;\n";
         o << "        if (";
@@ -237,8 +242,10 @@ std::string model_code_thread(const Model& m) {
     o << "__device__ __forceinline__ void smc_laws_all(double (&a)[SMC_M], const int (&x)[SMC_N], const double* __restrict__ H) {\n";
     for (int k = 0; k < M; ++k) o << "    a[" << k << "] = smc_law" << k << "(x, H);\n";
     o << "}\n";
-    // x += v_j, per species; overflow guard only where some delta is positive
-    o << "__device__ __forceinline__ bool smc_apply(int j, int (&x)[SMC_N]) {\n    bool ok = true;\n";
+    // x += v_j, per species, in wrapping 32-bit arithmetic.  Counts are >= 0 and
+    // |delta| <= 4, so x + delta exceeds 2^31-1 exactly when the wrapped result is
+    // negative (reading R17): one sign test over the OR of the grown species.
+    o << "__device__ __forceinline__ bool smc_apply(int j, int (&x)[SMC_N]) {\n    int grown = 0;\n";
     for (int s = 0; s < N; ++s) {
         std::vector<std::pair<int, int>> ds;
         bool pos = false;
@@ -249,13 +256,10 @@ std::string model_code_thread(const Model& m) {
         std::string sel = "0";
         for (auto it = ds.rbegin(); it != ds.rend(); ++it)
             sel = "(j == " + std::to_string(it->first) + " ? " + std::to_string(it->second) + " : " + sel + ")";
-        o << "    { const int d = " << sel << ";\n";
-        if (pos)
-            o << "      const smc_i64 nv = (smc_i64)x[" << s << "] + d; if (nv > 2147483647LL) ok = false; x[" << s << "] = (int)nv; }\n";
-        else
-            o << "      x[" << s << "] += d; }\n";
+        o << "    x[" << s << "] = (int)((unsigned)x[" << s << "] + (unsigned)" << sel << ");\n";
+        if (pos) o << "    grown |= x[" << s << "];\n";
     }
-    o << "    return ok;\n}\n";
+    o << "    return grown >= 0;\n}\n";
     // dependency graph: a_k recomputed iff k in dep(j)
     o << "__device__ __forceinline__ void smc_update(int j, double (&a)[SMC_M], const int (&x)[SMC_N], const double* __restrict__ H) {\n";
     for (int k = 0; k < M; ++k) {
@@ -299,30 +303,40 @@ HillTables pack_hill_tables(const Model& m) {
 }
 
 // --------------------------------------------------- variant 2 tables ---
+// Tile width: 8 lanes per trajectory for small networks (4 trajectories per warp),
+// 16 / 32 when the per-lane groups would get long.  SMC_TILE_WIDTH overrides.
+int tile_width(const Model& m) {
+    if (const char* e = std::getenv("SMC_TILE_WIDTH")) {
+        int w = std::atoi(e);
+        if (w == 8 || w == 16 || w == 32) return w;
+    }
+    return m.M <= 256 ? 8 : (m.M <= 512 ? 16 : 32);
+}
+
 TileLayout pack_tables(const Model& m) {
     TileLayout L;
     const int N = m.N, M = m.M;
-    L.gs = (M + 31) / 32;
+    L.tw = tile_width(m);
+    L.gs = (M + L.tw - 1) / L.tw;
+    L.ch = (L.gs + L.tw - 1) / L.tw;
     L.n_pad = (N + 3) & ~3;
+    L.tile_bytes = (size_t)L.gs * L.tw * 8 + 4 * (size_t)L.n_pad;
     for (auto& r : m.R) L.any_hill |= r.hill;
     size_t nnz = 0;
     for (auto& d : m.dep) { nnz += d.size(); L.max_dep = std::max<int>(L.max_dep, (int)d.size()); }
     size_t o = 0;
     L.off_x0 = o; o = align16(o + 4 * (size_t)L.n_pad);
-    L.off_sp = o; o = align16(o + 8 * (size_t)M);
-    L.off_c = o; o = align16(o + 8 * (size_t)M);
+    L.off_law = o; o = align16(o + 16 * (size_t)M);
     L.off_hill_rep = o; o = align16(o + (L.any_hill ? 4 * (size_t)M : 0));
     L.off_hill_k = o; o = align16(o + (L.any_hill ? 8 * (size_t)M : 0));
     L.off_hill_n = o; o = align16(o + (L.any_hill ? 4 * (size_t)M : 0));
     L.off_chg = o; o = align16(o + 2 * 4 * (size_t)M);
     L.off_dep_off = o; o = align16(o + 4 * ((size_t)M + 1));
-    L.off_dep_idx = o; o = align16(o + 2 * nnz);
+    L.off_dep = o; o = align16(o + 4 * nnz);
     L.bytes = o;
     L.blob.assign(L.bytes, 0);
     auto* x0 = (int32_t*)(L.blob.data() + L.off_x0);
     for (int s = 0; s < N; ++s) x0[s] = m.x0[(size_t)s];
-    auto* sp = (int32_t*)(L.blob.data() + L.off_sp);
-    auto* c = (double*)(L.blob.data() + L.off_c);
     auto* chg = (uint16_t*)(L.blob.data() + L.off_chg);
     for (int j = 0; j < M; ++j) {
         const Reaction& r = m.R[(size_t)j];
@@ -330,14 +344,16 @@ TileLayout pack_tables(const Model& m) {
         if (r.s[0] >= 0) w0 = (uint32_t)r.s[0] | ((uint32_t)r.st[0] << 16);
         if (r.s[1] >= 0) w1 = (uint32_t)r.s[1] | ((uint32_t)r.st[1] << 16);
         if (r.hill) w0 |= 0x80000000u;
-        sp[2 * j] = (int32_t)w0;
-        sp[2 * j + 1] = (int32_t)w1;
-        c[j] = r.c;
+        unsigned char* law = L.blob.data() + L.off_law + 16 * (size_t)j;   // {int s0, int s1, double c}
+        std::memcpy(law, &w0, 4);
+        std::memcpy(law + 4, &w1, 4);
+        std::memcpy(law + 8, &r.c, 8);
         if (L.any_hill) {
             ((int32_t*)(L.blob.data() + L.off_hill_rep))[j] = r.hill ? r.rep : 0;
             ((double*)(L.blob.data() + L.off_hill_k))[j] = r.hill ? r.K : 1.0;
             ((int32_t*)(L.blob.data() + L.off_hill_n))[j] = r.hill ? r.n : 1;
         }
+        if (r.change.size() > 4) fail(SMC_E_MODEL, "internal: more than 4 changed species");
         for (int q = 0; q < 4; ++q) {
             uint16_t e = 0xFFFF;
             if (q < (int)r.change.size()) e = (uint16_t)((r.change[(size_t)q].first << 4) | (r.change[(size_t)q].second + 8));
@@ -345,11 +361,15 @@ TileLayout pack_tables(const Model& m) {
         }
     }
     auto* doff = (uint32_t*)(L.blob.data() + L.off_dep_off);
-    auto* didx = (uint16_t*)(L.blob.data() + L.off_dep_idx);
+    auto* dep = (uint32_t*)(L.blob.data() + L.off_dep);
     size_t pos = 0;
     for (int j = 0; j < M; ++j) {
         doff[j] = (uint32_t)pos;
-        for (int k : m.dep[(size_t)j]) didx[pos++] = (uint16_t)k;
+        for (int k : m.dep[(size_t)j]) {
+            const int l = k / L.gs, mm = k % L.gs;
+            const uint32_t slot = (uint32_t)(mm * L.tw + (l ^ (mm % L.tw)));   // swizzled smem slot of a_k
+            dep[pos++] = (uint32_t)k | (slot << 16);
+        }
     }
     doff[M] = (uint32_t)pos;
     return L;
@@ -361,17 +381,17 @@ std::string generate_source(const Model& m, const Property& p, int variant, cons
     o << "#define SMC_N " << m.N << "\n#define SMC_M " << m.M << "\n";
     o << "#define SMC_TMAX " << dlit(p.t_max) << "\n";
     if (variant == 1) {
-        o << "#define SMC_BLOCK 128\n";
+        // >= 4 resident CTAs of 128 threads: at most 128 registers per thread
+        o << "#define SMC_BLOCK 128\n#define SMC_MINB 4\n";
     } else {
-        int gs2 = 1;
-        while (gs2 < tl->gs) gs2 <<= 1;
-        o << "#define SMC_GS " << tl->gs << "\n#define SMC_GS2 " << gs2 << "\n#define SMC_NPAD " << tl->n_pad << "\n";
-        o << "#define SMC_OFF_X0 " << tl->off_x0 << "\n#define SMC_OFF_SP " << tl->off_sp << "\n#define SMC_OFF_C " << tl->off_c
+        o << "#define SMC_TW " << tl->tw << "\n#define SMC_GS " << tl->gs << "\n#define SMC_CH " << tl->ch
+          << "\n#define SMC_NPAD " << tl->n_pad << "\n";
+        o << "#define SMC_OFF_X0 " << tl->off_x0 << "\n#define SMC_OFF_LAW " << tl->off_law
           << "\n#define SMC_OFF_HREP " << tl->off_hill_rep << "\n#define SMC_OFF_HK " << tl->off_hill_k
           << "\n#define SMC_OFF_HN " << tl->off_hill_n << "\n#define SMC_OFF_CHG " << tl->off_chg
-          << "\n#define SMC_OFF_DOFF " << tl->off_dep_off << "\n#define SMC_OFF_DIDX " << tl->off_dep_idx << "\n";
+          << "\n#define SMC_OFF_DOFF " << tl->off_dep_off << "\n#define SMC_OFF_DEP " << tl->off_dep << "\n";
         o << "#define SMC_TAB_BYTES " << tl->bytes << "\n";
-        o << "#define SMC_WARP_BYTES " << (size_t)tl->gs * 32 * 8 + 4 * (size_t)tl->n_pad << "\n";
+        o << "#define SMC_TILE_BYTES " << tl->tile_bytes << "\n";
         o << "#define SMC_ANY_HILL " << (tl->any_hill ? 1 : 0) << "\n";
     }
     o << embedded_source("ssa_common.cuh") << "\n";

@@ -6,16 +6,18 @@
 // refilled by warp ballot + one warp-aggregated 64-bit atomic on the work
 // cursor (compaction of the finished lanes onto new indices), so a warp keeps
 // all of its lanes busy while paths of different lengths end at different
-// times (P:291-294 on-the-fly halting makes them diverge).
+// times (P:291-294 on-the-fly halting makes them diverge).  The refill runs
+// once per SMC_BURST events; a lane that finishes inside a burst idles for the
+// rest of it (at most SMC_BURST-1 event slots per trajectory).
 //
-// The random draw of step k+1 (Philox + log, ~150 instructions) does not
-// depend on the state, so it is issued at the top of step k and overlaps the
-// state-dependent chain of step k (a0 -> tau -> monitor -> select -> update).
+// The random draw of step k+1 (Philox + log) does not depend on the state, so
+// it is issued at the top of step k, in the same basic block as the a0 sum,
+// and overlaps the state-dependent chain of step k.
 //
 // Generated hooks (codegen.cpp): SMC_N, SMC_M, SMC_BLOCK, SMC_TMAX,
 //   smc_init_x(x), smc_laws_all(a, x, H), smc_apply(j, x) -> ok,
 //   smc_update(j, a, x, H), smc_last_positive(a), struct SmcMon.
-//   H = P.tables: tabulated Hill propensities (zero-order Hill laws, x_r < table size).
+//   H = P.tables: tabulated Hill propensities (zero-order Hill laws).
 //
 // One event (SSA template P:173-179 with the monitor of P:291-294):
 //   a0 = sum a (fixed order)          step 1
@@ -26,9 +28,14 @@
 //   x += v_j; a_k = law_k(x), k in dep(j); t = t'   step 4
 //   monitor.enter(t, x)               (may decide)
 
-extern "C" __global__ void __launch_bounds__(SMC_BLOCK) smc_ssa_thread(SmcParams P) {
+#ifndef SMC_BURST
+#define SMC_BURST 8
+#endif
+
+extern "C" __global__ void __launch_bounds__(SMC_BLOCK, SMC_MINB) smc_ssa_thread(SmcParams P) {
     const smc_u32 lane = threadIdx.x & 31u;
     const double* __restrict__ H = (const double*)P.tables;
+    const smc_u32 cap = (smc_u32)(P.event_cap < 0xFFFFFFFFull ? P.event_cap : 0xFFFFFFFFull);
     int x[SMC_N];
     double a[SMC_M];
     double t = 0.0, tp = 0.0;
@@ -37,7 +44,8 @@ extern "C" __global__ void __launch_bounds__(SMC_BLOCK) smc_ssa_thread(SmcParams
     smc_u64 rel = 0, traj = 0;
     SmcMon mon;
     bool busy = false, exhausted = false;
-    smc_i64 c_true = 0, c_false = 0, c_ev = 0, c_err = 0;
+    smc_u32 c_true = 0, c_false = 0, c_err = 0;
+    smc_i64 c_ev = 0;
 
     for (;;) {
         // ---- refill: compact the idle lanes onto fresh trajectory indices
@@ -74,58 +82,63 @@ extern "C" __global__ void __launch_bounds__(SMC_BLOCK) smc_ssa_thread(SmcParams
             }
         }
         if (!__any_sync(SMC_FULL, busy)) break;
-        if (!busy) continue;
 
-        // ---- one SSA event of this lane's trajectory
-        double c[SMC_M];
-        c[0] = a[0];
-#pragma unroll
-        for (int m = 1; m < SMC_M; ++m) c[m] = __dadd_rn(c[m - 1], a[m]);
-        const double A = c[SMC_M - 1];
-        int v = -1;
-        if (!(A >= 0.0) || A > 1.7976931348623157e308) {
-            v = 2;                                        // bad propensity
-        } else if (A == 0.0) {
-            mon.absorb();
-            v = mon.verdict();
-        } else {
+#pragma unroll 1
+        for (int burst = 0; burst < SMC_BURST; ++burst) {
+            if (!busy) continue;
+            // ---- one SSA event of this lane's trajectory
             double e_nx, u_nx;                            // step k+1's draw, off the critical path
             smc_draw(P.seed, traj, (smc_u64)k + 1ull, e_nx, u_nx);
-            const double tn = __dadd_rn(t, __ddiv_rn(e_cur, A));
-            mon.advance(k, tn);
-            v = mon.verdict();
-            if (v < 0 && SMC_TMAX > 0.0 && tn > SMC_TMAX) {
-                mon.timeout();
-                v = mon.verdict();
-            }
-            if (v < 0) {
-                const double target = __dmul_rn(u_cur, A);
-                int j = 0;
+            double c[SMC_M];
+            c[0] = a[0];
 #pragma unroll
-                for (int m = 0; m < SMC_M; ++m) j += (c[m] <= target) ? 1 : 0;   // c is non-decreasing
-                if (j == SMC_M) j = smc_last_positive(a);                      // rounding (reading R11)
-                if (!smc_apply(j, x)) {
-                    v = 2;                                                     // count overflow
-                } else {
-                    smc_update(j, a, x, H);
-                    tp = t;
-                    t = tn;
-                    ++k;
-                    e_cur = e_nx;
-                    u_cur = u_nx;
-                    mon.enter(k, t, tp, x);
+            for (int m = 1; m < SMC_M; ++m) c[m] = __dadd_rn(c[m - 1], a[m]);
+            const double A = c[SMC_M - 1];
+            const double tn = __dadd_rn(t, __ddiv_rn(e_cur, A));
+            int v = -1;
+            if (!(A > 0.0) || A > 1.7976931348623157e308) {
+                if (A == 0.0) {                           // absorbed (reading R7)
+                    mon.absorb();
                     v = mon.verdict();
-                    if (v < 0 && (smc_u64)k >= P.event_cap) v = 2;
+                } else {
+                    v = 2;                                // bad propensity
+                }
+            } else {
+                mon.advance(k, tn);
+                v = mon.verdict();
+                if (v < 0 && SMC_TMAX > 0.0 && tn > SMC_TMAX) {
+                    mon.timeout();
+                    v = mon.verdict();
+                }
+                if (v < 0) {
+                    const double target = __dmul_rn(u_cur, A);
+                    int j = 0;
+#pragma unroll
+                    for (int m = 0; m < SMC_M; ++m) j += (c[m] <= target) ? 1 : 0;   // c is non-decreasing
+                    if (j == SMC_M) j = smc_last_positive(a);                      // rounding (reading R11)
+                    if (!smc_apply(j, x)) {
+                        v = 2;                                                     // count overflow
+                    } else {
+                        smc_update(j, a, x, H);
+                        tp = t;
+                        t = tn;
+                        ++k;
+                        e_cur = e_nx;
+                        u_cur = u_nx;
+                        mon.enter(k, t, tp, x);
+                        v = mon.verdict();
+                        if (v < 0 && k >= cap) v = 2;
+                    }
                 }
             }
-        }
-        if (v >= 0) {
-            if (v == 1) ++c_true;
-            else if (v == 0) ++c_false;
-            else ++c_err;
-            c_ev += k;
-            if (P.verdicts) { P.verdicts[rel] = (unsigned char)v; P.events_out[rel] = (int)k; }
-            busy = false;
+            if (v >= 0) {
+                if (v == 1) ++c_true;
+                else if (v == 0) ++c_false;
+                else ++c_err;
+                c_ev += k;
+                if (P.verdicts) { P.verdicts[rel] = (unsigned char)v; P.events_out[rel] = (int)k; }
+                busy = false;
+            }
         }
     }
     smc_flush_counts(c_true, c_false, c_ev, c_err, P.counters);

@@ -1,26 +1,26 @@
-// ssa_tile.cuh -- variant 2: persistent WARP-OWNED (tile) SSA + monitor kernel
-// for networks whose state does not fit in registers (C4: 50 x 200, C5:
-// 200 x 1000).
+// ssa_tile.cuh -- variant 2: persistent TILE-OWNED SSA + monitor kernel for
+// networks whose state does not fit in registers (C4: 50 x 200, C5: 200 x 1000).
 //
-// * Model tables (reactant/law table, change lists, dependency CSR) are staged
-//   ONCE per CTA from HBM into shared memory by a TMA bulk copy
-//   (cp.async.bulk ... mbarrier::complete_tx), then read from smem only.
-// * One warp owns one trajectory: species counts x[N] and propensities a[M]
-//   live in the warp's shared-memory slice; lane l owns the contiguous
-//   reaction group [l*GS, (l+1)*GS) and keeps its group sum S_l in a register.
-//   a is stored XOR-swizzled, a(l, m) at m*32 + (l ^ m), so both the per-lane
-//   group walk (fixed m, all l) and the level-2 scan (fixed l, all m) are
-//   bank-conflict free.
-// * Per event: a0 = inclusive warp scan of S (fixed order), reaction selection
-//   in two levels (group by ballot on the scan, member by a scan inside the
-//   group), x += v_j by <= 4 lanes, the dependency list dep(j) evaluated one
-//   reaction per lane, and only the touched groups re-summed (fixed order,
-//   never incremental deltas: reading R12).
-// * Philox + log for 32 future steps are computed by the 32 lanes at once and
-//   handed out by shuffle (state-independent, so batching them is exact).
+// * Model tables (law table, change lists, dependency CSR) are staged ONCE per
+//   CTA from HBM into shared memory by a TMA bulk copy (cp.async.bulk ...
+//   mbarrier::complete_tx) and then read from smem only.
+// * A tile of SMC_TW lanes (8, 16 or 32) owns one trajectory; a warp runs
+//   32/SMC_TW trajectories in lock step.  x[N] and a[M] live in the tile's
+//   shared-memory slice; lane l of a tile owns the contiguous reaction group
+//   [l*GS, (l+1)*GS) and keeps its group sum S_l in a register.  a is stored
+//   XOR-swizzled, a(l, m) at m*TW + (l ^ (m % TW)), so both the per-lane
+//   group walk and the in-group selection are bank-conflict free.
+// * Per event: a0 = inclusive tile scan of the TW group sums (fixed order),
+//   two-level selection (group by ballot on the scan, member by chunked scan
+//   inside the group), x += v_j by <= 4 lanes, dep(j) evaluated one law per
+//   lane, and only the touched groups re-summed left to right (reading R12:
+//   never incremental deltas).
+// * The Philox + log draws of the next SMC_TW steps of every tile are computed
+//   together at the start of each burst of SMC_TW events, one draw per lane
+//   (state-independent, so batching them is exact).
 //
-// Generated hooks (codegen.cpp): SMC_N, SMC_M, SMC_GS, SMC_GS2, SMC_NPAD,
-//   SMC_OFF_*, SMC_TAB_BYTES, SMC_WARP_BYTES, SMC_ANY_HILL, SMC_TMAX, SmcMon.
+// Generated hooks (codegen.cpp): SMC_N, SMC_M, SMC_TW, SMC_GS, SMC_CH, SMC_NPAD,
+//   SMC_OFF_*, SMC_TAB_BYTES, SMC_TILE_BYTES, SMC_ANY_HILL, SMC_TMAX, SmcMon.
 
 __device__ __forceinline__ void smc_mbar_init(unsigned long long* bar, unsigned count) {
     const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
@@ -46,35 +46,41 @@ __device__ __forceinline__ void smc_mbar_wait(unsigned long long* bar, unsigned 
     }
 }
 
+// Law table entry: reactant species/stoichiometry and the rate, one 16-byte load.
+struct __align__(16) SmcLaw {
+    int s0;      // s | st << 16 | hill << 31, 0xFFFF = none
+    int s1;
+    double c;
+};
+
 struct SmcTabs {
     const int* x0;
-    const int2* sp;       // .x = s0 | st0 << 16 | hill << 31, .y = s1 | st1 << 16 (0xFFFF = none)
-    const double* c;
+    const SmcLaw* law;
     const int* hill_rep;
     const double* hill_k;
     const int* hill_n;
     const unsigned short* chg;       // [M][4]: species << 4 | (delta + 8), 0xFFFF = none
     const unsigned* dep_off;         // [M+1]
-    const unsigned short* dep_idx;   // [nnz]
+    const unsigned* dep;             // [nnz]: k | slot << 16 (slot = swizzled smem index of a_k)
 };
 
 // a_j(x) from the shared-memory law table (readings R8/R9);
 // h_j is exact in int64, then one conversion and one multiply.
 __device__ __forceinline__ double smc_law_tab(int j, const int* xs, const SmcTabs& T) {
-    const int2 sp = T.sp[j];
+    const SmcLaw L = T.law[j];
     smc_i64 h = 1;
-    const int s0 = sp.x & 0xFFFF, s1 = sp.y & 0xFFFF;
+    const int s0 = L.s0 & 0xFFFF, s1 = L.s1 & 0xFFFF;
     if (s0 != 0xFFFF) {
         const smc_i64 v = xs[s0];
-        h = (((sp.x >> 16) & 3) == 1) ? v : (v * (v - 1)) / 2;
+        h = (((L.s0 >> 16) & 3) == 1) ? v : (v * (v - 1)) / 2;
     }
     if (s1 != 0xFFFF) {
         const smc_i64 v = xs[s1];
-        h = h * ((((sp.y >> 16) & 3) == 1) ? v : (v * (v - 1)) / 2);
+        h = h * ((((L.s1 >> 16) & 3) == 1) ? v : (v * (v - 1)) / 2);
     }
-    double a = __dmul_rn(T.c[j], (double)h);
+    double a = __dmul_rn(L.c, (double)h);
 #if SMC_ANY_HILL
-    if (sp.x < 0) {
+    if (L.s0 < 0) {
         const double q = __ddiv_rn((double)xs[T.hill_rep[j]], T.hill_k[j]);
         double qn = q;
         for (int i = 1; i < T.hill_n[j]; ++i) qn = __dmul_rn(qn, q);
@@ -84,15 +90,15 @@ __device__ __forceinline__ double smc_law_tab(int j, const int* xs, const SmcTab
     return a;
 }
 
-__device__ __forceinline__ int smc_aidx(int j) {     // swizzled slot of reaction j
-    const int l = j / SMC_GS, m = j - l * SMC_GS;
-    return m * 32 + (l ^ m);
-}
+__device__ __forceinline__ int smc_slot(int l, int m) { return m * SMC_TW + (l ^ (m % SMC_TW)); }
 
 extern "C" __global__ void __launch_bounds__(512, 1) smc_ssa_tile(SmcParams P) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ __align__(8) unsigned long long bar;
-    const smc_u32 lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const int lane = (int)(threadIdx.x & 31u), warp = (int)(threadIdx.x >> 5);
+    constexpr int TW = SMC_TW, TPW = 32 / SMC_TW;
+    const int tl = lane % TW, tile = lane / TW;
+    const smc_u32 tbits = (TW == 32) ? SMC_FULL : (((1u << TW) - 1u) << (tile * TW));
 
     // ---- stage the model tables: one TMA bulk copy per 32 KB chunk
     if (threadIdx.x == 0) smc_mbar_init(&bar, 1);
@@ -108,147 +114,203 @@ extern "C" __global__ void __launch_bounds__(512, 1) smc_ssa_tile(SmcParams P) {
 
     SmcTabs T;
     T.x0 = (const int*)(smem + SMC_OFF_X0);
-    T.sp = (const int2*)(smem + SMC_OFF_SP);
-    T.c = (const double*)(smem + SMC_OFF_C);
+    T.law = (const SmcLaw*)(smem + SMC_OFF_LAW);
     T.hill_rep = (const int*)(smem + SMC_OFF_HREP);
     T.hill_k = (const double*)(smem + SMC_OFF_HK);
     T.hill_n = (const int*)(smem + SMC_OFF_HN);
     T.chg = (const unsigned short*)(smem + SMC_OFF_CHG);
     T.dep_off = (const unsigned*)(smem + SMC_OFF_DOFF);
-    T.dep_idx = (const unsigned short*)(smem + SMC_OFF_DIDX);
-    double* at = (double*)(smem + SMC_TAB_BYTES + (size_t)warp * SMC_WARP_BYTES);
-    int* xs = (int*)(at + SMC_GS * 32);
+    T.dep = (const unsigned*)(smem + SMC_OFF_DEP);
+    double* at = (double*)(smem + SMC_TAB_BYTES + (size_t)(warp * TPW + tile) * SMC_TILE_BYTES);
+    int* xs = (int*)(at + SMC_GS * TW);
 
-    smc_i64 c_true = 0, c_false = 0, c_ev = 0, c_err = 0;   // lane 0 of each warp
+    // ---- per-tile trajectory state (replicated in the tile's lanes)
+    bool act = false, exhausted = false;
+    smc_u64 rel = 0, traj = 0;
+    double t = 0.0, tp = 0.0, S = 0.0;
+    smc_u32 k = 0, kb = 0;
+    double Eb = 0.0, Ub = 0.0;          // draw of step kb + tl
+    SmcMon mon;
+    smc_u32 c_true = 0, c_false = 0, c_err = 0;   // tile leader
+    smc_i64 c_ev = 0;
+
     for (;;) {
-        smc_u64 rel = 0;
-        if (lane == 0) rel = atomicAdd(P.cursor, 1ull);
-        rel = __shfl_sync(SMC_FULL, rel, 0);
-        if (rel >= P.count) break;
-        const smc_u64 traj = P.first + rel;
-
-        // ---- init: x = x0, all a_j, group sums, monitor at sigma[0]
-        for (int s = lane; s < SMC_N; s += 32) xs[s] = T.x0[s];
-        __syncwarp();
-        double S = 0.0;
-#pragma unroll 4
-        for (int m = 0; m < SMC_GS; ++m) {
-            const int j = (int)lane * SMC_GS + m;
-            const double val = (j < SMC_M) ? smc_law_tab(j, xs, T) : 0.0;
-            at[m * 32 + ((int)lane ^ m)] = val;
-            S = (m == 0) ? val : __dadd_rn(S, val);
+        // ---- refill: tiles without a trajectory claim fresh indices (one atomic per warp)
+        for (;;) {
+            const bool want = !act && !exhausted;
+            const smc_u32 wm = __ballot_sync(SMC_FULL, want && tl == 0);
+            if (wm == 0u) break;
+            const int leader = __ffs(wm) - 1;
+            smc_u64 base = 0;
+            if (lane == leader) base = atomicAdd(P.cursor, (smc_u64)__popc(wm));
+            base = __shfl_sync(SMC_FULL, base, leader);
+            if (want) {
+                rel = base + (smc_u64)__popc(wm & ((1u << (tile * TW)) - 1u));
+                if (rel >= P.count) exhausted = true;
+            }
+            const bool init = want && !exhausted;
+            if (init) {
+                traj = P.first + rel;
+                for (int s = tl; s < SMC_N; s += TW) xs[s] = T.x0[s];
+            }
+            __syncwarp();
+            if (init) {
+                double s2 = 0.0;
+                for (int m = 0; m < SMC_GS; ++m) {
+                    const int j = tl * SMC_GS + m;
+                    const double val = (j < SMC_M) ? smc_law_tab(j, xs, T) : 0.0;
+                    at[smc_slot(tl, m)] = val;
+                    s2 = (m == 0) ? val : __dadd_rn(s2, val);
+                }
+                S = s2;
+                t = 0.0;
+                tp = 0.0;
+                k = 0;
+                mon.init();
+                mon.enter(0u, 0.0, 0.0, xs);        // sigma_buff = {(s0, t0)}
+                const int v = mon.verdict();
+                if (v >= 0) {
+                    if (tl == 0) {
+                        if (v == 1) ++c_true; else ++c_false;
+                        if (P.verdicts) { P.verdicts[rel] = (unsigned char)v; P.events_out[rel] = 0; }
+                    }
+                } else {
+                    act = true;
+                }
+            }
+            __syncwarp();
         }
-        __syncwarp();
-        SmcMon mon;
-        mon.init();
-        double t = 0.0, tp = 0.0;
-        smc_u32 k = 0, k0 = 0, kend = 0;
-        double Eb = 0.0, Ub = 0.0;
-        mon.enter(0u, 0.0, 0.0, xs);
-        int v = mon.verdict();
-        while (v < 0) {
-            // a0 = inclusive scan of the group sums (fixed association per lane)
+        if (!__any_sync(SMC_FULL, act)) break;
+
+        // ---- burst of TW events: draws of steps k .. k+TW-1, one per lane
+        if (act) smc_draw(P.seed, traj, (smc_u64)(k + (smc_u32)tl), Eb, Ub);
+        kb = k;
+#pragma unroll 1
+        for (int s = 0; s < TW; ++s) {
+            if (!__any_sync(SMC_FULL, act)) break;
+            // a0 = inclusive scan of the group sums, fixed association per lane
             double Pp = S;
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const double y = __shfl_up_sync(SMC_FULL, Pp, o);
-                if ((int)lane >= o) Pp = __dadd_rn(y, Pp);
+            for (int o = 1; o < TW; o <<= 1) {
+                const double y = __shfl_up_sync(SMC_FULL, Pp, o, TW);
+                if (tl >= o) Pp = __dadd_rn(y, Pp);
             }
-            const double A = __shfl_sync(SMC_FULL, Pp, 31);
-            if (!(A >= 0.0) || A > 1.7976931348623157e308) { v = 2; break; }
-            if (A == 0.0) { mon.absorb(); v = mon.verdict(); break; }
-            if (k >= kend) {                       // 32 future draws, one per lane
-                k0 = k;
-                kend = k + 32u;
-                smc_draw(P.seed, traj, (smc_u64)(k0 + lane), Eb, Ub);
-            }
-            const double E = __shfl_sync(SMC_FULL, Eb, (int)(k - k0));
-            const double U = __shfl_sync(SMC_FULL, Ub, (int)(k - k0));
+            const double A = __shfl_sync(SMC_FULL, Pp, TW - 1, TW);
+            const int q = (int)(k - kb) & (TW - 1);
+            const double E = __shfl_sync(SMC_FULL, Eb, q, TW);
+            const double U = __shfl_sync(SMC_FULL, Ub, q, TW);
             const double tn = __dadd_rn(t, __ddiv_rn(E, A));
-            mon.advance(k, tn);
-            v = mon.verdict();
-            if (v >= 0) break;
-            if (SMC_TMAX > 0.0 && tn > SMC_TMAX) { mon.timeout(); v = mon.verdict(); break; }
-
-            // ---- two-level selection: group g, then member m  (Eq. 2b)
+            int v = -1;
+            if (act) {
+                if (!(A > 0.0) || A > 1.7976931348623157e308) {
+                    if (A == 0.0) { mon.absorb(); v = mon.verdict(); }     // absorbed (reading R7)
+                    else v = 2;                                            // bad propensity
+                } else {
+                    mon.advance(k, tn);
+                    v = mon.verdict();
+                    if (v < 0 && SMC_TMAX > 0.0 && tn > SMC_TMAX) { mon.timeout(); v = mon.verdict(); }
+                }
+            }
+            const bool go = act && v < 0;              // this tile applies a reaction
+            // ---- two-level selection (Eq. 2b): group g by ballot on the scan ...
             const double target = __dmul_rn(U, A);
-            const smc_u32 bg = __ballot_sync(SMC_FULL, Pp > target);
-            int j;
-            if (bg) {
-                const int g = __ffs(bg) - 1;
-                double base = __shfl_sync(SMC_FULL, Pp, (g + 31) & 31);
-                if (g == 0) base = 0.0;
-                const double val = ((int)lane < SMC_GS) ? at[lane * 32 + (g ^ (int)lane)] : 0.0;
-                double q = (lane == 0) ? __dadd_rn(base, val) : val;
+            const smc_u32 bg = (__ballot_sync(SMC_FULL, Pp > target) & tbits) >> (tile * TW);
+            const smc_u32 bp = (__ballot_sync(SMC_FULL, S > 0.0) & tbits) >> (tile * TW);
+            const int g = bg ? (__ffs(bg) - 1) : (bp ? 31 - __clz(bp) : 0);
+            double base = __shfl_sync(SMC_FULL, Pp, (g + TW - 1) & (TW - 1), TW);
+            if (g == 0) base = 0.0;
+            // ... then the member inside group g: lane tl scans its chunk of SMC_CH elements
+            double cs = 0.0;
+            double av[SMC_CH];
 #pragma unroll
-                for (int o = 1; o < SMC_GS2; o <<= 1) {
-                    const double y = __shfl_up_sync(SMC_FULL, q, o);
-                    if ((int)lane >= o) q = __dadd_rn(y, q);
-                }
-                const smc_u32 bm = __ballot_sync(SMC_FULL, (int)lane < SMC_GS && q > target);
-                if (bm) {
-                    j = g * SMC_GS + __ffs(bm) - 1;
-                } else {                               // ulp tie: last positive member
-                    const smc_u32 bp = __ballot_sync(SMC_FULL, (int)lane < SMC_GS && val > 0.0);
-                    j = g * SMC_GS + 31 - __clz(bp);
-                }
-            } else {                                   // rounding: last a_j > 0 (reading R11)
-                const smc_u32 bs = __ballot_sync(SMC_FULL, S > 0.0);
-                const int g = 31 - __clz(bs);
-                const double val = ((int)lane < SMC_GS) ? at[lane * 32 + (g ^ (int)lane)] : 0.0;
-                const smc_u32 bp = __ballot_sync(SMC_FULL, (int)lane < SMC_GS && val > 0.0);
-                j = g * SMC_GS + 31 - __clz(bp);
+            for (int c = 0; c < SMC_CH; ++c) {
+                const int m = tl * SMC_CH + c;
+                av[c] = (m < SMC_GS) ? at[smc_slot(g, m)] : 0.0;
+                cs = (c == 0) ? av[c] : __dadd_rn(cs, av[c]);
             }
+            double ps = cs;                              // inclusive scan of the chunk sums
+#pragma unroll
+            for (int o = 1; o < TW; o <<= 1) {
+                const double y = __shfl_up_sync(SMC_FULL, ps, o, TW);
+                if (tl >= o) ps = __dadd_rn(y, ps);
+            }
+            double acc = __shfl_up_sync(SMC_FULL, ps, 1, TW);
+            acc = (tl == 0) ? base : __dadd_rn(base, acc);
+            int hit = -1, lastpos = -1;
+#pragma unroll
+            for (int c = 0; c < SMC_CH; ++c) {
+                acc = __dadd_rn(acc, av[c]);
+                if (hit < 0 && acc > target) hit = c;
+                if (av[c] > 0.0) lastpos = c;
+            }
+            const smc_u32 bh = (__ballot_sync(SMC_FULL, bg != 0 && hit >= 0) & tbits) >> (tile * TW);
+            const smc_u32 bl = (__ballot_sync(SMC_FULL, lastpos >= 0) & tbits) >> (tile * TW);
+            int jm;
+            if (bh) {
+                const int src = __ffs(bh) - 1;
+                jm = __shfl_sync(SMC_FULL, src * SMC_CH + hit, src, TW);
+            } else {                                     // rounding: last a_j > 0 (reading R11)
+                const int src = bl ? 31 - __clz(bl) : 0;
+                jm = __shfl_sync(SMC_FULL, src * SMC_CH + lastpos, src, TW);
+            }
+            const int j = go ? g * SMC_GS + jm : 0;
 
-            // ---- x += v_j  (<= 4 distinct species, one lane each)
+            // ---- x += v_j (<= 4 distinct species, one lane each; wrapping add, sign = overflow)
             bool ovf = false;
-            if (lane < 4u) {
-                const unsigned e = T.chg[j * 4 + (int)lane];
+            if (go && tl < 4) {
+                const unsigned e = T.chg[j * 4 + tl];
                 if (e != 0xFFFFu) {
-                    const int s = (int)(e >> 4);
-                    const smc_i64 nv = (smc_i64)xs[s] + (smc_i64)((int)(e & 15u) - 8);
-                    if (nv > 2147483647ll) ovf = true;
-                    else xs[s] = (int)nv;
+                    const int sp = (int)(e >> 4);
+                    const int nv = (int)((unsigned)xs[sp] + (unsigned)((int)(e & 15u) - 8));
+                    ovf = nv < 0;
+                    xs[sp] = nv;
                 }
             }
-            if (__any_sync(SMC_FULL, ovf)) { v = 2; break; }
+            const bool tile_ovf = ((__ballot_sync(SMC_FULL, ovf) & tbits) != 0u);
             __syncwarp();
-
             // ---- a_k = law_k(x) for k in dep(j), one reaction per lane
-            const unsigned d0 = T.dep_off[j], d1 = T.dep_off[j + 1];
+            const unsigned d0 = go ? T.dep_off[j] : 0u, d1 = go ? T.dep_off[j + 1] : 0u;
             smc_u32 touched = 0;
-            for (unsigned b = d0; b < d1; b += 32u) {
-                if (b + lane < d1) {
-                    const int kk = T.dep_idx[b + lane];
-                    const double an = smc_law_tab(kk, xs, T);
-                    at[smc_aidx(kk)] = an;
-                    touched |= 1u << (kk / SMC_GS);
+            for (unsigned b = d0; __any_sync(SMC_FULL, b < d1); b += TW) {
+                if (b + (unsigned)tl < d1) {
+                    const unsigned e = T.dep[b + tl];
+                    const int kk = (int)(e & 0xFFFFu), slot = (int)(e >> 16);
+                    at[slot] = smc_law_tab(kk, xs, T);
+                    touched |= 1u << ((slot ^ (slot / TW)) & (TW - 1));
                 }
             }
-            touched = __reduce_or_sync(SMC_FULL, touched);
+#pragma unroll
+            for (int o = TW / 2; o > 0; o >>= 1) touched |= __shfl_xor_sync(SMC_FULL, touched, o, TW);
             __syncwarp();
             // ---- re-sum only the touched groups, left to right
-            if ((touched >> lane) & 1u) {
-                double s2 = at[lane];
-#pragma unroll 8
-                for (int m = 1; m < SMC_GS; ++m) s2 = __dadd_rn(s2, at[m * 32 + ((int)lane ^ m)]);
+            if ((touched >> tl) & 1u) {
+                double s2 = at[smc_slot(tl, 0)];
+                for (int m = 1; m < SMC_GS; ++m) s2 = __dadd_rn(s2, at[smc_slot(tl, m)]);
                 S = s2;
             }
-            tp = t;
-            t = tn;
-            ++k;
-            mon.enter(k, t, tp, xs);
-            v = mon.verdict();
-            if (v < 0 && (smc_u64)k >= P.event_cap) v = 2;
+            if (go) {
+                if (tile_ovf) {
+                    v = 2;                                // count overflow
+                } else {
+                    tp = t;
+                    t = tn;
+                    ++k;
+                    mon.enter(k, t, tp, xs);
+                    v = mon.verdict();
+                    if (v < 0 && (smc_u64)k >= P.event_cap) v = 2;
+                }
+            }
+            if (act && v >= 0) {
+                if (tl == 0) {
+                    if (v == 1) ++c_true;
+                    else if (v == 0) ++c_false;
+                    else ++c_err;
+                    c_ev += k;
+                    if (P.verdicts) { P.verdicts[rel] = (unsigned char)v; P.events_out[rel] = (int)k; }
+                }
+                act = false;
+            }
         }
-        if (lane == 0) {
-            if (v == 1) ++c_true;
-            else if (v == 0) ++c_false;
-            else ++c_err;
-            c_ev += k;
-            if (P.verdicts) { P.verdicts[rel] = (unsigned char)v; P.events_out[rel] = (int)k; }
-        }
-        __syncwarp();
     }
     smc_flush_counts(c_true, c_false, c_ev, c_err, P.counters);
 }

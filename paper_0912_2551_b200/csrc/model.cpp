@@ -159,6 +159,12 @@ int smc_model_set_event_cap(smc_model* h, uint64_t cap) {
     return SMC_OK;
 }
 
+int smc_model_set_speculation(smc_model* h, int32_t on) {
+    if (!h) { set_error("smc_model_set_speculation: NULL model"); return SMC_E_ARG; }
+    h->m.speculate = on != 0;
+    return SMC_OK;
+}
+
 void smc_model_destroy(smc_model* h) { delete h; }
 
 }  // extern "C"

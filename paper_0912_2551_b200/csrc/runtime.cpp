@@ -13,6 +13,8 @@
 // AOT kernel launcher (aot_kernels.cu)
 cudaError_t smc_launch_philox_debug(uint64_t seed, uint64_t traj, uint64_t step0, uint32_t n, uint32_t* dev_out,
                                     cudaStream_t stream);
+cudaError_t smc_launch_count_range(const unsigned char* v, const int* e, uint64_t n, long long* counters,
+                                   cudaStream_t stream);
 
 namespace smc {
 
@@ -56,7 +58,12 @@ struct PropKernel {
     int grid_max = 0;
     int smem = 0;
     const void* tables = nullptr;
+    bool timing_pending = false;
+    int per_warp = 1;                      // trajectories per warp (variant 2)
     smc_launch_info info{};
+    uint64_t capacity() const {            // trajectories resident at once on this GPU
+        return (uint64_t)grid_max * (uint64_t)(variant == 1 ? block : (block / 32) * per_warp);
+    }
 };
 
 struct DeviceState {
@@ -64,8 +71,14 @@ struct DeviceState {
     size_t table_bytes[3] = {0, 0, 0};
     bool tables_ready[3] = {false, false, false};
     TileLayout layout;
-    void* ctl = nullptr;            // [0..8) cursor, [16..48) counters
+    void* ctl = nullptr;            // [0..8) cursor, [16..48) counters, [64..72) spec cursor, [80..112) spec scratch
     int64_t* host_counts = nullptr; // pinned
+    // speculative batch of smc_estimate (prefix-exact rounds): this rank's slice [lo, hi)
+    // of the batch [begin, end), per-replica verdicts/events at [i - lo]
+    unsigned char* spec_v = nullptr;
+    int* spec_e = nullptr;
+    uint64_t spec_cap = 0, spec_begin = 0, spec_end = 0, spec_lo = 0, spec_hi = 0;
+    bool spec_valid = false;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     int sm_count = 0, max_smem_optin = 0;
     std::map<uint64_t, PropKernel> kernels;
@@ -74,9 +87,13 @@ struct DeviceState {
         if (e1) cudaEventDestroy(e1);
         if (host_counts) cudaFreeHost(host_counts);
         dfree(ctl);
+        dfree(spec_v);
+        dfree(spec_e);
         for (void* t : tables) dfree(t);
     }
     int64_t* counters() { return (int64_t*)((char*)ctl + 16); }
+    unsigned long long* spec_cursor() { return (unsigned long long*)((char*)ctl + 64); }
+    int64_t* spec_scratch() { return (int64_t*)((char*)ctl + 80); }
 };
 
 void DeviceStateDeleter::operator()(DeviceState* d) const { delete d; }
@@ -93,7 +110,7 @@ DeviceState& device(Model& m) {
         ck(cudaGetDevice(&dev), "cudaGetDevice");
         ck(cudaDeviceGetAttribute(&d->sm_count, cudaDevAttrMultiProcessorCount, dev), "attr");
         ck(cudaDeviceGetAttribute(&d->max_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev), "attr");
-        d->ctl = dalloc(64);
+        d->ctl = dalloc(128);
         ck(cudaMallocHost((void**)&d->host_counts, 64), "cudaMallocHost");
         ck(cudaEventCreate(&d->e0), "cudaEventCreate");
         ck(cudaEventCreate(&d->e1), "cudaEventCreate");
@@ -144,7 +161,7 @@ PropKernel& prepare(Model& m, const Property& p) {
         pk.grid_max = std::max(1, nb) * d.sm_count;
         pk.smem = 0;
     } else {
-        const size_t wb = (size_t)tl->gs * 32 * 8 + 4 * (size_t)tl->n_pad;
+        const size_t wb = tl->tile_bytes * (size_t)(32 / tl->tw);   // smem per warp
         cudaFuncAttributes fa;
         ck(cudaFuncGetAttributes(&fa, fn), "cudaFuncGetAttributes");
         const size_t max_dyn = (size_t)d.max_smem_optin - fa.sharedSizeBytes;
@@ -161,6 +178,7 @@ PropKernel& prepare(Model& m, const Property& p) {
         pk.block = best_w * 32;
         pk.smem = (int)(tl->bytes + (size_t)best_w * wb);
         pk.grid_max = best_nb * d.sm_count;
+        pk.per_warp = 32 / tl->tw;
     }
     pk.info.variant = pk.variant;
     pk.info.block_threads = pk.block;
@@ -172,10 +190,13 @@ PropKernel& prepare(Model& m, const Property& p) {
 }
 
 // Launch one slice asynchronously on the stream; counters stay on the device.
+// spec: cursor / counters of the speculative control block (the round counters are
+// then filled by smc_count_range), else the main block (zeroed here).
 void launch_slice(Model& m, PropKernel& pk, uint64_t seed, uint64_t lo, uint64_t hi, uint8_t* dev_verdict,
-                  int32_t* dev_events) {
+                  int32_t* dev_events, bool spec = false) {
     DeviceState& d = *m.dev;
-    ck(cudaMemsetAsync(d.ctl, 0, 64, stream()), "memset counters");
+    if (spec) ck(cudaMemsetAsync((char*)d.ctl + 64, 0, 64, stream()), "memset spec block");
+    else ck(cudaMemsetAsync(d.ctl, 0, 64, stream()), "memset counters");
     if (hi <= lo) return;
     const uint64_t count = hi - lo;
     struct Params {
@@ -186,9 +207,9 @@ void launch_slice(Model& m, PropKernel& pk, uint64_t seed, uint64_t lo, uint64_t
         int* events_out;
         unsigned long long event_cap;
         const void* tables;
-    } P{seed, lo, count, (unsigned long long*)d.ctl, (long long*)d.counters(), dev_verdict, dev_events, m.event_cap,
-        pk.tables};
-    const uint64_t per_block = pk.variant == 1 ? (uint64_t)pk.block : (uint64_t)(pk.block / 32);
+    } P{seed, lo, count, spec ? d.spec_cursor() : (unsigned long long*)d.ctl,
+        (long long*)(spec ? d.spec_scratch() : d.counters()), dev_verdict, dev_events, m.event_cap, pk.tables};
+    const uint64_t per_block = pk.variant == 1 ? (uint64_t)pk.block : (uint64_t)(pk.block / 32 * pk.per_warp);
     const uint64_t need = (count + per_block - 1) / per_block;
     const int grid = (int)std::min<uint64_t>((uint64_t)pk.grid_max, need);
     void* args[] = {&P};
@@ -199,13 +220,85 @@ void launch_slice(Model& m, PropKernel& pk, uint64_t seed, uint64_t lo, uint64_t
     ck(cudaEventRecord(d.e1, stream()), "event");
     pk.info.grid_blocks = grid;
     pk.info.launches += 1;
+    pk.timing_pending = true;
 }
 
-void finish_timing(Model& m, PropKernel& pk, bool launched) {
-    if (!launched) return;
+void finish_timing(Model& m, PropKernel& pk, bool = true) {
+    if (!pk.timing_pending) return;
     float ms = 0.f;
     ck(cudaEventElapsedTime(&ms, m.dev->e0, m.dev->e1), "cudaEventElapsedTime");
     pk.info.kernel_ms += ms;
+    pk.timing_pending = false;
+}
+
+void read_counts(Model& m, PropKernel& pk, smc_counts* out) {
+    Hooks& h = hooks();
+    if (h.allreduce) {
+        if (h.allreduce(m.dev->counters(), 4, h.allreduce_user) != 0) fail(SMC_E_COMM, "allreduce hook failed");
+    }
+    ck(cudaMemcpyAsync(m.dev->host_counts, m.dev->counters(), 32, cudaMemcpyDeviceToHost, stream()), "D2H counts");
+    ck(cudaStreamSynchronize(stream()), "cudaStreamSynchronize");
+    finish_timing(m, pk);
+    out->n_true = m.dev->host_counts[0];
+    out->n_false = m.dev->host_counts[1];
+    out->events = m.dev->host_counts[2];
+    out->errors = m.dev->host_counts[3];
+}
+
+// Prefix-exact speculative round.  The counts of the round
+// range [base, base+n) are summed from per-replica results; when the range is not
+// covered by the current batch, a new batch starting at the first uncovered index
+// is launched with S = max(need, min(capacity of all GPUs, limit - start))
+// replicas.  Fig. 2 only ever consumes prefixes of the index stream and every
+// index is simulated exactly once by exactly one rank, so the counts -- and the
+// estimate -- are identical to the non-speculative rounds; replicas past the
+// final N_tot are simulated but never counted.
+void spec_round(Model& m, PropKernel& pk, uint64_t seed, uint64_t base, uint64_t n, uint64_t limit, smc_counts* out) {
+    DeviceState& d = *m.dev;
+    Hooks& h = hooks();
+    const uint64_t end = base + n;
+    ck(cudaMemsetAsync(d.ctl, 0, 64, stream()), "memset counters");
+    auto count = [&](uint64_t a, uint64_t b) {       // [a, b) within this rank's slice of the batch
+        a = std::max(a, d.spec_lo);
+        b = std::min(b, d.spec_hi);
+        if (b > a)
+            ck(smc_launch_count_range(d.spec_v + (a - d.spec_lo), d.spec_e + (a - d.spec_lo), b - a,
+                                      (long long*)d.counters(), stream()),
+               "count kernel");
+    };
+    uint64_t covered = base;
+    if (d.spec_valid && base >= d.spec_begin && base < d.spec_end) {
+        count(base, std::min(end, d.spec_end));
+        covered = std::min(end, d.spec_end);
+    }
+    if (covered < end) {
+        const uint64_t need = end - covered;
+        const uint64_t cap_all = pk.capacity() * (uint64_t)h.world;
+        const uint64_t room = limit > covered ? limit - covered : 0;
+        const uint64_t S = std::max(need, std::min(cap_all, room));
+        uint64_t lo = covered, hi = covered + S;
+        if (h.world > 1) smc_shard_range(covered, S, h.rank, h.world, &lo, &hi);
+        if (hi - lo > d.spec_cap) {
+            dfree(d.spec_v);
+            dfree(d.spec_e);
+            d.spec_v = nullptr;
+            d.spec_e = nullptr;
+            d.spec_cap = 0;
+            const uint64_t c = hi - lo;
+            d.spec_v = (unsigned char*)dalloc(c);
+            d.spec_e = (int*)dalloc(4 * c);
+            d.spec_cap = c;
+        }
+        launch_slice(m, pk, seed, lo, hi, d.spec_v, d.spec_e, true);
+        ck(cudaGetLastError(), "kernel launch");
+        d.spec_begin = covered;
+        d.spec_end = covered + S;
+        d.spec_lo = lo;
+        d.spec_hi = hi;
+        d.spec_valid = true;
+        count(covered, end);
+    }
+    read_counts(m, pk, out);
 }
 
 }  // namespace
@@ -217,16 +310,7 @@ int run_round(Model& m, const Property& p, uint64_t seed, uint64_t base, uint64_
     if (h.world > 1) smc_shard_range(base, n, h.rank, h.world, &lo, &hi);
     launch_slice(m, pk, seed, lo, hi, nullptr, nullptr);
     ck(cudaGetLastError(), "kernel launch");
-    if (h.allreduce) {
-        if (h.allreduce(m.dev->counters(), 4, h.allreduce_user) != 0) fail(SMC_E_COMM, "allreduce hook failed");
-    }
-    ck(cudaMemcpyAsync(m.dev->host_counts, m.dev->counters(), 32, cudaMemcpyDeviceToHost, stream()), "D2H counts");
-    ck(cudaStreamSynchronize(stream()), "cudaStreamSynchronize");
-    finish_timing(m, pk, hi > lo);
-    out->n_true = m.dev->host_counts[0];
-    out->n_false = m.dev->host_counts[1];
-    out->events = m.dev->host_counts[2];
-    out->errors = m.dev->host_counts[3];
+    read_counts(m, pk, out);
     return SMC_OK;
 }
 
@@ -344,9 +428,21 @@ int smc_estimate(smc_model* h, const smc_property* ph, double confidence, double
         PropKernel& pk = prepare(m, *ph->p);
         pk.info.launches = 0;
         pk.info.kernel_ms = 0.f;
-        return wilson_loop(
-            [&](uint64_t base, uint64_t n, smc_counts* c) { return run_round(m, *ph->p, seed, base, n, c); },
+        m.dev->spec_valid = false;
+        // no Fig. 2 round can reach past the conservative size Eq. 4(0.5) (N' <= Eq. 4(0.5))
+        const uint64_t limit = (uint64_t)wilson_sample_size(0.5, half_width, normal_quantile(confidence));
+        const bool speculate = m.speculate;
+        int rc = wilson_loop(
+            [&](uint64_t base, uint64_t n, smc_counts* c) {
+                if (speculate) {
+                    spec_round(m, pk, seed, base, n, limit, c);
+                    return (int)SMC_OK;
+                }
+                return run_round(m, *ph->p, seed, base, n, c);
+            },
             confidence, half_width, 1.0, out);
+        m.dev->spec_valid = false;
+        return rc;
     });
 }
 

@@ -43,6 +43,7 @@ struct Model {
     std::vector<Reaction> R;
     int variant_forced = 0;
     uint64_t event_cap = 2147483647ull;
+    bool speculate = true;           // prefix-exact speculative rounds in smc_estimate
     // dependency graph: dep[j] = { k : species(law_k) intersects changed(j) }
     std::vector<std::vector<int>> dep;
     bool deps_built = false;
@@ -103,10 +104,13 @@ std::unique_ptr<Property> compile_property(const Model& m, const std::string& te
 
 // --------------------------------------------------------------- codegen ---
 struct TileLayout {               // packed model tables (variant 2), byte offsets
+    int tw = 32;                  // lanes per trajectory tile
     int gs = 0;                   // reactions per lane group
+    int ch = 0;                   // level-2 chunk per lane
     int n_pad = 0;
-    size_t off_x0 = 0, off_sp = 0, off_c = 0, off_hill_rep = 0, off_hill_k = 0, off_hill_n = 0;
-    size_t off_chg = 0, off_dep_off = 0, off_dep_idx = 0, bytes = 0;
+    size_t tile_bytes = 0;        // smem per trajectory
+    size_t off_x0 = 0, off_law = 0, off_hill_rep = 0, off_hill_k = 0, off_hill_n = 0;
+    size_t off_chg = 0, off_dep_off = 0, off_dep = 0, bytes = 0;
     bool any_hill = false;
     int max_dep = 0;
     std::vector<uint8_t> blob;    // host copy

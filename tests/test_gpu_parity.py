@@ -216,6 +216,26 @@ def test_large_networks_vs_oracle_fixture(smc, name):
     assert m.last_launch(p)["variant"] == 2
 
 
+@pytest.mark.parametrize("width", ["8", "16", "32"])
+def test_tile_widths_vs_fixture(smc, width, monkeypatch):
+    """Every tile width of variant 2 (8/16/32 lanes per trajectory) gives the oracle's replicas."""
+    import json
+    import os
+    monkeypatch.setenv("SMC_TILE_WIDTH", width)
+    fx = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "c4_oracle.json")))
+    cfg = workloads.c4()
+    m, p = _pair(smc, cfg)
+    n = 600
+    v, e = m.run_verdicts(p, 0, n, fx["seed"])
+    v, e = v.cpu().numpy(), e.cpu().numpy()
+    mism = int(((v != np.array(fx["verdicts"][:n])) | (e != np.array(fx["events"][:n]))).sum())
+    assert mism <= 1
+    for name in ("C2", "C3"):
+        cfg = workloads.get(name)
+        a, ae, *_ = _compare(smc, cfg, cfg["seed"], 0, 300, variant=2)
+        assert ae >= 299 / 300
+
+
 def test_c4_full_size_shard_sampled(smc):
     """C4 (configs[3]: 10^7 replicas over 8 GPUs): rank 0's shard of 1.25e6 replicas in the bench
     launch configuration; the oracle checks sampled replicas one by one."""
@@ -234,6 +254,19 @@ def test_c4_full_size_shard_sampled(smc):
         bad += int(ov[0] != v[i] or oe[0] != e[i])
     assert bad == 0
     assert abs(v.mean() - 0.54) < 0.03          # fixture estimate 0.5415 (2000 oracle replicas)
+
+
+@pytest.mark.parametrize("name,eps", [("C1", 0.01), ("C2", 0.005), ("C3", 0.02)])
+def test_speculative_rounds_identical(smc, name, eps):
+    """Prefix-exact speculation changes only the schedule: the
+    Fig. 2 estimate equals the one from exactly-sized rounds, bit for bit."""
+    cfg = workloads.get(name)
+    m, p = _pair(smc, cfg)
+    on = smc.estimate(m, p, 0.99, eps, 17)
+    m.set_speculation(False)
+    off = smc.estimate(m, p, 0.99, eps, 17)
+    assert on == off
+    assert on["rounds"] >= 2
 
 
 def test_c5_first_round_sampled(smc):
