@@ -1,6 +1,11 @@
-"""Cross-compile the generated SSA kernels for C1..C5 with nvcc (sm_100a) on a
-machine without a GPU: catches codegen errors and shows registers / spills /
-shared memory (-Xptxas -v).  Writes build/gen/<cfg>.cu and .cubin."""
+"""Compile the generated SSA kernels for C1..C5 with NVRTC (the same library and
+options jit.cpp uses on the GPU box, so the cubin is the binary that runs) on a
+machine without a GPU: catches codegen errors and reports registers / spills /
+static SASS size.  Writes build/gen/<cfg>_v<variant>.cu and .cubin.
+
+  python scripts/check_codegen.py [C1 C2 ...]       (SMC_TILE_WIDTH honoured)
+"""
+import ctypes
 import os
 import subprocess
 import sys
@@ -10,6 +15,29 @@ sys.path.insert(0, ROOT)
 
 import workloads  # noqa: E402
 import paper_0912_2551_b200 as smc  # noqa: E402
+
+# keep in sync with jit.cpp
+OPTS = [b"--gpu-architecture=sm_100a", b"--std=c++17", b"--fmad=false", b"-lineinfo",
+        b"--extra-device-vectorization", b"-DNDEBUG", b"-Xptxas=-v"]
+
+
+def nvrtc_cubin(src, name):
+    lib = ctypes.CDLL("/usr/local/cuda/lib64/libnvrtc.so.12")
+    prog = ctypes.c_void_p()
+    assert lib.nvrtcCreateProgram(ctypes.byref(prog), src.encode(), name.encode(), 0, None, None) == 0
+    opts = (ctypes.c_char_p * len(OPTS))(*OPTS)
+    rc = lib.nvrtcCompileProgram(prog, len(OPTS), opts)
+    n = ctypes.c_size_t()
+    lib.nvrtcGetProgramLogSize(prog, ctypes.byref(n))
+    log = ctypes.create_string_buffer(n.value)
+    lib.nvrtcGetProgramLog(prog, log)
+    if rc != 0:
+        raise SystemExit("NVRTC failed for %s:\n%s" % (name, log.value.decode()[:4000]))
+    lib.nvrtcGetCUBINSize(prog, ctypes.byref(n))
+    buf = ctypes.create_string_buffer(n.value)
+    lib.nvrtcGetCUBIN(prog, buf)
+    lib.nvrtcDestroyProgram(ctypes.byref(prog))
+    return buf.raw, log.value.decode()
 
 
 def main(names):
@@ -25,14 +53,13 @@ def main(names):
             path = os.path.join(out, "%s_v%d.cu" % (name, variant))
             with open(path, "w") as fh:
                 fh.write(src)
-            cmd = ["nvcc", "-cubin", "-gencode", "arch=compute_100a,code=sm_100a", "-std=c++17", "--fmad=false",
-                   "-lineinfo", "-Xptxas", "-v", "-o", path[:-3] + ".cubin", path]
-            r = subprocess.run(cmd, capture_output=True, text=True)
-            if r.returncode != 0:
-                print(r.stderr)
-                raise SystemExit("codegen check failed for %s variant %d" % (name, variant))
-            info = [ln.strip() for ln in r.stderr.splitlines() if "registers" in ln or "spill" in ln]
-            print(name, "v%d" % variant, " | ".join(info))
+            cubin, log = nvrtc_cubin(src, path)
+            with open(path[:-3] + ".cubin", "wb") as fh:
+                fh.write(cubin)
+            sass = subprocess.run(["cuobjdump", "-sass", path[:-3] + ".cubin"], capture_output=True, text=True).stdout
+            n_inst = sum(1 for ln in sass.splitlines() if ln.strip().startswith("/*") and "*/" in ln[:12])
+            info = [ln.strip() for ln in log.splitlines() if "registers" in ln or "spill" in ln]
+            print(name, "v%d" % variant, "sass=%d" % n_inst, " | ".join(info))
 
 
 if __name__ == "__main__":

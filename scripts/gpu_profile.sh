@@ -1,19 +1,17 @@
-# ncu evidence: launch list of the default bench, full capture of the SSA kernels (one per variant)
+# ncu evidence: launch list of the default bench, one full capture of the SSA kernel per workload.
+# usage: bash scripts/gpu_profile.sh TAG [WORKLOAD:N[:TW] ...]
 set -x
-python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/plain_c2.log 2>&1 &&
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c2.csv \
-    python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launches.log 2>&1
+TAG=${1:-v1}; shift
+mkdir -p gpurun_out
+python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/plain_default_$TAG.log 2>&1 &&
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_default_$TAG.csv \
+    python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launches_$TAG.log 2>&1
 echo "launches rc=$?"
-python bench.py --workload C3 --n 200000 --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/plain_c3.log 2>&1 &&
-ncu --set full --clock-control none --import-source on -k regex:smc_ssa -s 2 -c 1 -o gpurun_out/prof_c3 \
-    python bench.py --workload C3 --n 200000 --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_c3.log 2>&1
-echo "c3 rc=$?"
-python bench.py --workload C2 --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/plain_c2b.log 2>&1 &&
-ncu --set full --clock-control none --import-source on -k regex:smc_ssa -s 4 -c 2 -o gpurun_out/prof_c2 \
-    python bench.py --workload C2 --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_c2.log 2>&1
-echo "c2 rc=$?"
-python bench.py --workload C4 --n 20000 --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/plain_c4.log 2>&1 &&
-ncu --set full --clock-control none --import-source on -k regex:smc_ssa -s 2 -c 1 -o gpurun_out/prof_c4 \
-    python bench.py --workload C4 --n 20000 --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_c4.log 2>&1
-echo "c4 rc=$?"
-tail -2 gpurun_out/plain_c4.log
+for spec in "$@"; do
+  IFS=: read W N TW <<< "$spec"
+  if [ -n "$TW" ]; then export SMC_TILE_WIDTH=$TW; else unset SMC_TILE_WIDTH; fi
+  timeout 600 python scripts/prof_run.py $W $N > gpurun_out/plain_${W}_${TW}_$TAG.log 2>&1 &&
+  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:smc_ssa -s 1 -c 1 \
+      -o gpurun_out/prof_${W}_${TW}_$TAG python scripts/prof_run.py $W $N > gpurun_out/ncu_${W}_${TW}_$TAG.log 2>&1
+  echo "$W tw=$TW rc=$?"; tail -1 gpurun_out/plain_${W}_${TW}_$TAG.log
+done
