@@ -318,10 +318,21 @@ TileLayout pack_tables(const Model& m) {
     const int N = m.N, M = m.M;
     L.tw = tile_width(m);
     L.gs = (M + L.tw - 1) / L.tw;
-    L.ch = (L.gs + L.tw - 1) / L.tw;
+    L.ch = 1;
+    while (L.ch * L.tw < L.gs) L.ch *= 2;      // chunk per lane in the in-group selection (power of two)
     L.n_pad = (N + 3) & ~3;
-    L.tile_bytes = (size_t)L.gs * L.tw * 8 + 4 * (size_t)L.n_pad;
-    for (auto& r : m.R) L.any_hill |= r.hill;
+    // per-trajectory slice: a[GS*TW] (fp64) + x[NPAD] (int32), 16-byte aligned; with several
+    // tiles per warp the slice is padded to 64 mod 128 bytes so that neighbouring tiles use
+    // opposite halves of the 32 banks
+    L.tile_bytes = align16((size_t)L.gs * L.tw * 8 + 4 * (size_t)L.n_pad);
+    if (L.tw < 32)
+        while (L.tile_bytes % 128 != 64) L.tile_bytes += 16;
+    for (auto& r : m.R) {
+        L.any_hill |= r.hill;
+        int order = 0;
+        for (int q = 0; q < 2; ++q) order += r.s[q] >= 0 ? r.st[q] : 0;
+        L.any_general |= order > 2;
+    }
     size_t nnz = 0;
     for (auto& d : m.dep) { nnz += d.size(); L.max_dep = std::max<int>(L.max_dep, (int)d.size()); }
     size_t o = 0;
@@ -340,11 +351,16 @@ TileLayout pack_tables(const Model& m) {
     auto* chg = (uint16_t*)(L.blob.data() + L.off_chg);
     for (int j = 0; j < M; ++j) {
         const Reaction& r = m.R[(size_t)j];
-        uint32_t w0 = 0xFFFF, w1 = 0xFFFF;
-        if (r.s[0] >= 0) w0 = (uint32_t)r.s[0] | ((uint32_t)r.st[0] << 16);
-        if (r.s[1] >= 0) w1 = (uint32_t)r.s[1] | ((uint32_t)r.st[1] << 16);
+        // law kind (ssa_tile.cuh smc_law_tab): 0 h=1, 1 x0, 2 x0(x0-1)/2, 3 x0*x1, 4 general
+        uint32_t kind, s0 = 0, s1 = 0;
+        if (r.s[0] < 0) kind = 0;
+        else if (r.s[1] < 0) { kind = r.st[0] == 1 ? 1u : 2u; s0 = s1 = (uint32_t)r.s[0]; }
+        else { kind = (r.st[0] == 1 && r.st[1] == 1) ? 3u : 4u; s0 = (uint32_t)r.s[0]; s1 = (uint32_t)r.s[1]; }
+        uint32_t w0 = s0 | (kind << 16) | ((uint32_t)(r.s[0] >= 0 ? r.st[0] : 1) << 20);
+        uint32_t w1 = s1 | ((uint32_t)(r.s[1] >= 0 ? r.st[1] : 1) << 16);
+        if (kind == 4 && r.s[1] < 0) fail(SMC_E_MODEL, "internal: general law with one reactant");
         if (r.hill) w0 |= 0x80000000u;
-        unsigned char* law = L.blob.data() + L.off_law + 16 * (size_t)j;   // {int s0, int s1, double c}
+        unsigned char* law = L.blob.data() + L.off_law + 16 * (size_t)j;   // {u0, u1, double c}
         std::memcpy(law, &w0, 4);
         std::memcpy(law + 4, &w1, 4);
         std::memcpy(law + 8, &r.c, 8);
@@ -362,12 +378,13 @@ TileLayout pack_tables(const Model& m) {
     }
     auto* doff = (uint32_t*)(L.blob.data() + L.off_dep_off);
     auto* dep = (uint32_t*)(L.blob.data() + L.off_dep);
+    if ((size_t)L.gs * L.tw > 65536) fail(SMC_E_MODEL, "tile variant: too many reactions for 16-bit slots");
     size_t pos = 0;
     for (int j = 0; j < M; ++j) {
         doff[j] = (uint32_t)pos;
         for (int k : m.dep[(size_t)j]) {
-            const int l = k / L.gs, mm = k % L.gs;
-            const uint32_t slot = (uint32_t)(mm * L.tw + (l ^ (mm % L.tw)));   // swizzled smem slot of a_k
+            const int l = k / L.gs, mm = k % L.gs;       // owner lane, member (ssa_tile.cuh smc_slot)
+            const uint32_t slot = (uint32_t)(mm * L.tw + (l ^ ((mm / L.ch) % L.tw)));
             dep[pos++] = (uint32_t)k | (slot << 16);
         }
     }
@@ -393,6 +410,7 @@ std::string generate_source(const Model& m, const Property& p, int variant, cons
         o << "#define SMC_TAB_BYTES " << tl->bytes << "\n";
         o << "#define SMC_TILE_BYTES " << tl->tile_bytes << "\n";
         o << "#define SMC_ANY_HILL " << (tl->any_hill ? 1 : 0) << "\n";
+        o << "#define SMC_ANY_GENERAL " << (tl->any_general ? 1 : 0) << "\n";
     }
     o << embedded_source("ssa_common.cuh") << "\n";
     if (variant == 1) o << model_code_thread(m) << "\n";

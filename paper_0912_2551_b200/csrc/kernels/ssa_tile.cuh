@@ -5,22 +5,29 @@
 //   CTA from HBM into shared memory by a TMA bulk copy (cp.async.bulk ...
 //   mbarrier::complete_tx) and then read from smem only.
 // * A tile of SMC_TW lanes (8, 16 or 32) owns one trajectory; a warp runs
-//   32/SMC_TW trajectories in lock step.  x[N] and a[M] live in the tile's
+//   TPW = 32/SMC_TW trajectories in lock step.  x[N] and a[M] live in the tile's
 //   shared-memory slice; lane l of a tile owns the contiguous reaction group
-//   [l*GS, (l+1)*GS) and keeps its group sum S_l in a register.  a is stored
-//   XOR-swizzled, a(l, m) at m*TW + (l ^ (m % TW)), so both the per-lane
-//   group walk and the in-group selection are bank-conflict free.
+//   [l*GS, (l+1)*GS) and keeps its group sum S_l in a register.
+//   a(l, m) is stored at m*TW + (l ^ ((m / CH) % TW)): the group walk of the
+//   resum (all lanes at the same m) and the chunked in-group selection (lane c
+//   reads m = c*CH + i) are both bank-conflict free; tile slices are padded so
+//   the TPW tiles of a warp fall in alternate halves of the 32 banks.
 // * Per event: a0 = inclusive tile scan of the TW group sums (fixed order),
 //   two-level selection (group by ballot on the scan, member by chunked scan
-//   inside the group), x += v_j by <= 4 lanes, dep(j) evaluated one law per
-//   lane, and only the touched groups re-summed left to right (reading R12:
-//   never incremental deltas).
+//   inside the group), x += v_j by <= 4 lanes, then the dependency work of ALL
+//   tiles of the warp is flattened over the 32 lanes (a_k = law_k(x), k in
+//   dep(j)), and only the touched groups are re-summed (reading R12: a fixed
+//   order, never incremental deltas).
+// * Propensity laws are evaluated in fp64 on integer-valued doubles; for
+//   reaction order <= 2 this is exactly (double)h with h the int64 combinatorial
+//   count (see smc_law_tab), order 3-4 takes the int64 path.
 // * The Philox + log draws of the next SMC_TW steps of every tile are computed
 //   together at the start of each burst of SMC_TW events, one draw per lane
 //   (state-independent, so batching them is exact).
 //
 // Generated hooks (codegen.cpp): SMC_N, SMC_M, SMC_TW, SMC_GS, SMC_CH, SMC_NPAD,
-//   SMC_OFF_*, SMC_TAB_BYTES, SMC_TILE_BYTES, SMC_ANY_HILL, SMC_TMAX, SmcMon.
+//   SMC_OFF_*, SMC_TAB_BYTES, SMC_TILE_BYTES, SMC_ANY_HILL, SMC_ANY_GENERAL,
+//   SMC_TMAX, SmcMon.
 
 __device__ __forceinline__ void smc_mbar_init(unsigned long long* bar, unsigned count) {
     const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
@@ -46,10 +53,13 @@ __device__ __forceinline__ void smc_mbar_wait(unsigned long long* bar, unsigned 
     }
 }
 
-// Law table entry: reactant species/stoichiometry and the rate, one 16-byte load.
+// Law table entry, one 16-byte load:
+//   u0 = s0 | kind << 16 | hill << 31, u1 = s1 (both species indices are valid:
+//   unused slots repeat s0), c = rate.  kind: 0 h = 1, 1 h = x0, 2 h = x0(x0-1)/2,
+//   3 h = x0 x1, 4 general (order 3-4: C(x0,st0) C(x1,st1) in int64; st in u1 >> 16).
 struct __align__(16) SmcLaw {
-    int s0;      // s | st << 16 | hill << 31, 0xFFFF = none
-    int s1;
+    unsigned u0;
+    unsigned u1;
     double c;
 };
 
@@ -61,36 +71,66 @@ struct SmcTabs {
     const int* hill_n;
     const unsigned short* chg;       // [M][4]: species << 4 | (delta + 8), 0xFFFF = none
     const unsigned* dep_off;         // [M+1]
-    const unsigned* dep;             // [nnz]: k | slot << 16 (slot = swizzled smem index of a_k)
+    const unsigned* dep;             // [nnz]: k | slot(k) << 16
 };
 
-// a_j(x) from the shared-memory law table (readings R8/R9);
-// h_j is exact in int64, then one conversion and one multiply.
-__device__ __forceinline__ double smc_law_tab(int j, const int* xs, const SmcTabs& T) {
-    const SmcLaw L = T.law[j];
-    smc_i64 h = 1;
-    const int s0 = L.s0 & 0xFFFF, s1 = L.s1 & 0xFFFF;
-    if (s0 != 0xFFFF) {
-        const smc_i64 v = xs[s0];
-        h = (((L.s0 >> 16) & 3) == 1) ? v : (v * (v - 1)) / 2;
+// a_k(x) (readings R8/R9).  For order <= 2 the combinatorial count h is
+// formed in fp64 from the integer counts: x0, x0*x1 and x0*(x0-1) are single roundings
+// of the exact integer products (counts < 2^31, so the int64 product is exact), and
+// halving is exact, hence h equals (double)(int64 h) bit for bit; a = c * h.
+__device__ __forceinline__ double smc_law_tab(int k, const int* xs, const SmcTabs& T) {
+    const SmcLaw L = T.law[k];
+    const int kind = (int)((L.u0 >> 16) & 7u);
+    const int v0 = xs[L.u0 & 0xFFFFu];
+    const int v1 = xs[L.u1 & 0xFFFFu];
+    double h;
+#if SMC_ANY_GENERAL
+    if (kind == 4) {
+        const smc_i64 y0 = v0, y1 = v1;
+        const smc_i64 h0 = ((L.u0 >> 20) & 3u) == 1u ? y0 : (y0 * (y0 - 1)) / 2;
+        const smc_i64 h1 = ((L.u1 >> 16) & 3u) == 1u ? y1 : (y1 * (y1 - 1)) / 2;
+        h = (double)(h0 * h1);
+    } else
+#endif
+    {
+        int xa = v0, xb = v1;
+        if (kind == 2) xb = max(v0 - 1, 0);
+        if (kind <= 1) xb = 1;
+        if (kind == 0) xa = 1;
+        h = __dmul_rn((double)xa, (double)xb);
+        if (kind == 2) h = __dmul_rn(h, 0.5);
     }
-    if (s1 != 0xFFFF) {
-        const smc_i64 v = xs[s1];
-        h = h * ((((L.s1 >> 16) & 3) == 1) ? v : (v * (v - 1)) / 2);
-    }
-    double a = __dmul_rn(L.c, (double)h);
+    double a = __dmul_rn(L.c, h);
 #if SMC_ANY_HILL
-    if (L.s0 < 0) {
-        const double q = __ddiv_rn((double)xs[T.hill_rep[j]], T.hill_k[j]);
+    if ((int)L.u0 < 0) {
+        const double q = __ddiv_rn((double)xs[T.hill_rep[k]], T.hill_k[k]);
         double qn = q;
-        for (int i = 1; i < T.hill_n[j]; ++i) qn = __dmul_rn(qn, q);
+        for (int i = 1; i < T.hill_n[k]; ++i) qn = __dmul_rn(qn, q);
         a = __ddiv_rn(a, __dadd_rn(1.0, qn));
     }
 #endif
     return a;
 }
 
-__device__ __forceinline__ int smc_slot(int l, int m) { return m * SMC_TW + (l ^ (m % SMC_TW)); }
+// smem slot of a(l, m), l = group (owner lane), m = member (SMC_CH is a power of two)
+__device__ __forceinline__ int smc_slot(int l, int m) { return m * SMC_TW + (l ^ ((m / SMC_CH) % SMC_TW)); }
+// owner lane of a slot (inverse of smc_slot)
+__device__ __forceinline__ int smc_owner(int slot) { return (slot % SMC_TW) ^ ((slot / SMC_TW / SMC_CH) % SMC_TW); }
+
+// Group sum of lane l: two interleaved partial sums (even / odd members, each left to
+// right), then added -- a fixed order (reading R12) with half the dependent-add chain.
+__device__ __forceinline__ double smc_group_sum(const double* at, int l) {
+    double se = at[smc_slot(l, 0)];
+    if (SMC_GS == 1) return se;
+    double so = at[smc_slot(l, 1)];
+#pragma unroll
+    for (int m = 2; m + 1 < SMC_GS; m += 2) {
+        se = __dadd_rn(se, at[smc_slot(l, m)]);
+        so = __dadd_rn(so, at[smc_slot(l, m + 1)]);
+    }
+    if (SMC_GS & 1) se = __dadd_rn(se, at[smc_slot(l, SMC_GS - 1)]);
+    return __dadd_rn(se, so);
+}
 
 extern "C" __global__ void __launch_bounds__(512, 1) smc_ssa_tile(SmcParams P) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -121,7 +161,8 @@ extern "C" __global__ void __launch_bounds__(512, 1) smc_ssa_tile(SmcParams P) {
     T.chg = (const unsigned short*)(smem + SMC_OFF_CHG);
     T.dep_off = (const unsigned*)(smem + SMC_OFF_DOFF);
     T.dep = (const unsigned*)(smem + SMC_OFF_DEP);
-    double* at = (double*)(smem + SMC_TAB_BYTES + (size_t)(warp * TPW + tile) * SMC_TILE_BYTES);
+    unsigned char* const warp_base = smem + SMC_TAB_BYTES + (size_t)warp * TPW * SMC_TILE_BYTES;
+    double* at = (double*)(warp_base + (size_t)tile * SMC_TILE_BYTES);
     int* xs = (int*)(at + SMC_GS * TW);
 
     // ---- per-tile trajectory state (replicated in the tile's lanes)
@@ -155,14 +196,14 @@ extern "C" __global__ void __launch_bounds__(512, 1) smc_ssa_tile(SmcParams P) {
             }
             __syncwarp();
             if (init) {
-                double s2 = 0.0;
                 for (int m = 0; m < SMC_GS; ++m) {
                     const int j = tl * SMC_GS + m;
-                    const double val = (j < SMC_M) ? smc_law_tab(j, xs, T) : 0.0;
-                    at[smc_slot(tl, m)] = val;
-                    s2 = (m == 0) ? val : __dadd_rn(s2, val);
+                    at[smc_slot(tl, m)] = (j < SMC_M) ? smc_law_tab(j, xs, T) : 0.0;
                 }
-                S = s2;
+            }
+            __syncwarp();
+            if (init) {
+                S = smc_group_sum(at, tl);
                 t = 0.0;
                 tp = 0.0;
                 k = 0;
@@ -178,7 +219,6 @@ extern "C" __global__ void __launch_bounds__(512, 1) smc_ssa_tile(SmcParams P) {
                     act = true;
                 }
             }
-            __syncwarp();
         }
         if (!__any_sync(SMC_FULL, act)) break;
 
@@ -268,26 +308,49 @@ extern "C" __global__ void __launch_bounds__(512, 1) smc_ssa_tile(SmcParams P) {
             }
             const bool tile_ovf = ((__ballot_sync(SMC_FULL, ovf) & tbits) != 0u);
             __syncwarp();
-            // ---- a_k = law_k(x) for k in dep(j), one reaction per lane
-            const unsigned d0 = go ? T.dep_off[j] : 0u, d1 = go ? T.dep_off[j + 1] : 0u;
-            smc_u32 touched = 0;
-            for (unsigned b = d0; __any_sync(SMC_FULL, b < d1); b += TW) {
-                if (b + (unsigned)tl < d1) {
-                    const unsigned e = T.dep[b + tl];
-                    const int kk = (int)(e & 0xFFFFu), slot = (int)(e >> 16);
-                    at[slot] = smc_law_tab(kk, xs, T);
-                    touched |= 1u << ((slot ^ (slot / TW)) & (TW - 1));
+            // ---- a_k = law_k(x) for k in dep(j) of every tile, flattened over the 32 lanes
+            smc_u32 touched = 0;                         // bit (tile' * TW + owner lane)
+            {
+                const unsigned d0 = go ? T.dep_off[j] : 0u;
+                const unsigned nd = go ? T.dep_off[j + 1] - d0 : 0u;
+                if (TPW == 1) {
+                    for (unsigned b = (unsigned)lane; __any_sync(SMC_FULL, b < nd); b += 32u) {
+                        if (b < nd) {
+                            const unsigned e = T.dep[d0 + b];
+                            const int slot = (int)(e >> 16);
+                            at[slot] = smc_law_tab((int)(e & 0xFFFFu), xs, T);
+                            touched |= 1u << smc_owner(slot);
+                        }
+                    }
+                } else {
+                    unsigned pre[TPW], off[TPW], tot = 0;
+#pragma unroll
+                    for (int u = 0; u < TPW; ++u) {
+                        pre[u] = tot;
+                        off[u] = __shfl_sync(SMC_FULL, d0, u * TW);
+                        tot += __shfl_sync(SMC_FULL, nd, u * TW);
+                    }
+                    for (unsigned b = (unsigned)lane; b < tot; b += 32u) {
+                        int u = 0;
+#pragma unroll
+                        for (int w = 1; w < TPW; ++w) u += (b >= pre[w]) ? 1 : 0;
+                        unsigned o = off[0], p0 = pre[0];
+#pragma unroll
+                        for (int w = 1; w < TPW; ++w)
+                            if (u == w) { o = off[w]; p0 = pre[w]; }
+                        const unsigned e = T.dep[o + (b - p0)];
+                        const int slot = (int)(e >> 16);
+                        double* at_u = (double*)(warp_base + (size_t)u * SMC_TILE_BYTES);
+                        const int* xs_u = (const int*)(at_u + SMC_GS * TW);
+                        at_u[slot] = smc_law_tab((int)(e & 0xFFFFu), xs_u, T);
+                        touched |= 1u << (u * TW + smc_owner(slot));
+                    }
                 }
             }
-#pragma unroll
-            for (int o = TW / 2; o > 0; o >>= 1) touched |= __shfl_xor_sync(SMC_FULL, touched, o, TW);
+            touched = __reduce_or_sync(SMC_FULL, touched);
             __syncwarp();
-            // ---- re-sum only the touched groups, left to right
-            if ((touched >> tl) & 1u) {
-                double s2 = at[smc_slot(tl, 0)];
-                for (int m = 1; m < SMC_GS; ++m) s2 = __dadd_rn(s2, at[smc_slot(tl, m)]);
-                S = s2;
-            }
+            // ---- re-sum only the touched groups (fixed order)
+            if ((touched >> lane) & 1u) S = smc_group_sum(at, tl);
             if (go) {
                 if (tile_ovf) {
                     v = 2;                                // count overflow

@@ -112,6 +112,7 @@ struct TileLayout {               // packed model tables (variant 2), byte offse
     size_t off_x0 = 0, off_law = 0, off_hill_rep = 0, off_hill_k = 0, off_hill_n = 0;
     size_t off_chg = 0, off_dep_off = 0, off_dep = 0, bytes = 0;
     bool any_hill = false;
+    bool any_general = false;     // a reaction of order 3-4 (int64 law path)
     int max_dep = 0;
     std::vector<uint8_t> blob;    // host copy
 };

@@ -57,7 +57,7 @@ def main(names):
             with open(path[:-3] + ".cubin", "wb") as fh:
                 fh.write(cubin)
             sass = subprocess.run(["cuobjdump", "-sass", path[:-3] + ".cubin"], capture_output=True, text=True).stdout
-            n_inst = sum(1 for ln in sass.splitlines() if ln.strip().startswith("/*") and "*/" in ln[:12])
+            n_inst = sum(1 for ln in sass.splitlines() if ln.strip().startswith("/*") and "*/" in ln.strip()[:10])
             info = [ln.strip() for ln in log.splitlines() if "registers" in ln or "spill" in ln]
             print(name, "v%d" % variant, "sass=%d" % n_inst, " | ".join(info))
 
