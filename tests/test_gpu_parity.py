@@ -285,3 +285,28 @@ def test_c5_first_round_sampled(smc):
         c, ov, oe = O.run(om, of, cfg["seed"], int(i), 1)
         bad += int(ov[0] != v[i] or oe[0] != e[i])
     assert bad == 0
+
+
+def _law_kinds_cfg():
+    """Every propensity law shape (readings R8/S8): h = 1, x, x(x-1)/2, x*y with a product
+    above 2^31, C(x,2)*y (order 3) and C(x,2)*C(y,2) (order 4), at counts where the int64
+    count and its double differ from any 32-bit shortcut."""
+    rx = workloads._rx
+    return dict(name="laws", species=["A", "B", "C", "D"], x0=[40000, 50000, 3, 100],
+                reactions=[rx([(0, 2)], [(2, 1)], 1e-9),            # 2A -> C        (homodimer)
+                           rx([(0, 1), (1, 1)], [(3, 1)], 1e-10),   # A + B -> D     (h ~ 2e9)
+                           rx([(0, 2), (1, 1)], [(2, 1)], 1e-15),   # 2A + B -> C    (order 3)
+                           rx([(2, 2), (3, 2)], [(0, 1)], 1e-5),    # 2C + 2D -> A   (order 4)
+                           rx([(3, 1)], [], 0.1),                   # D -> 0
+                           rx([], [(2, 1)], 1.0)],                  # 0 -> C         (h = 1)
+                formula="F[0,5](C > 8)", t_max=0.0, seed=11, sampling=dict(mode="fixed", n=2000))
+
+
+@pytest.mark.parametrize("variant", [1, 2])
+def test_all_law_kinds_vs_oracle(smc, variant):
+    """The tile kernel forms h in fp64 for order <= 2 and in int64 for order 3-4; the thread
+    kernel always in int64.  Both must reproduce the oracle's replicas exactly."""
+    cfg = _law_kinds_cfg()
+    a, ae, v, e, ov, oe = _compare(smc, cfg, cfg["seed"], 0, 2000, variant)
+    assert ae >= 1999 / 2000, (variant, a, ae)
+    assert 0 < v.mean() < 1 and e.mean() > 20
