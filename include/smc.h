@@ -218,6 +218,13 @@ int smc_run_verdicts(smc_model* m, const smc_property* p, uint64_t first, uint64
  * the device code path, copied to host_out[4 n]. */
 int smc_philox_blocks(uint64_t seed, uint64_t trajectory, uint64_t step0, uint32_t n, uint32_t* host_out);
 
+/* n SSA draws of steps step0 + q, q < n, of (seed, trajectory) computed by the
+ * device code path the kernels use (Eq. 2a numerator and the
+ * Eq. 2b uniform): host_out[2q] = e = -log(u1), host_out[2q+1] = u2.
+ * u2 is bit-exact with the oracle; e is within 1 ulp of glibc's -log(u1)
+ * (reading R18).  Errors: SMC_E_ARG for NULL, SMC_E_CUDA. */
+int smc_draw_blocks(uint64_t seed, uint64_t trajectory, uint64_t step0, uint32_t n, double* host_out);
+
 typedef struct {
     int32_t variant;          /* 1 thread-owned, 2 warp-owned tile                 */
     int32_t block_threads;    /* threads per CTA                                    */

@@ -11,7 +11,7 @@ kernel calls) every call raises.
 from ._native import (  # noqa: F401
     SmcError, lib, smc_last_error,
     smc_normal_quantile, smc_wilson_interval, smc_wilson_sample_size, smc_shard_range,
-    smc_philox_blocks, smc_set_shard, smc_set_stream,
+    smc_philox_blocks, smc_draw_blocks, smc_set_shard, smc_set_stream,
 )
 from .api import (  # noqa: F401
     Model, Property, estimate, estimate_with_runner, use_torch, set_allreduce_torch, clear_allreduce,

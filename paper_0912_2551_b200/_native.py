@@ -57,6 +57,7 @@ SIGNATURES = [
     ("smc_set_allreduce", c_i32, [ALLREDUCE_FN, c_vp]),
     ("smc_run_verdicts", c_i32, [c_vp, c_vp, c_u64, c_u64, c_u64, c_vp, c_vp]),
     ("smc_philox_blocks", c_i32, [c_u64, c_u64, c_u64, c_u32, c_vp]),
+    ("smc_draw_blocks", c_i32, [c_u64, c_u64, c_u64, c_u32, c_vp]),
     ("smc_last_launch", c_i32, [c_vp, c_vp, ctypes.POINTER(SmcLaunchInfo)]),
     ("smc_kernel_source", c_i32, [c_vp, c_vp, ctypes.c_char_p, ctypes.POINTER(c_sz)]),
 ]
@@ -128,6 +129,13 @@ def smc_philox_blocks(seed, trajectory, step0, n):
     buf = (c_u32 * (4 * n))()
     check(lib().smc_philox_blocks(seed, trajectory, step0, n, ctypes.cast(buf, c_vp)))
     return [[buf[4 * q + i] for i in range(4)] for q in range(n)]
+
+
+def smc_draw_blocks(seed, trajectory, step0, n):
+    """[(e, u2)] of steps step0 .. step0+n-1 from the device draw (e = -log(u1))."""
+    buf = (ctypes.c_double * (2 * n))()
+    check(lib().smc_draw_blocks(seed, trajectory, step0, n, ctypes.cast(buf, c_vp)))
+    return [(buf[2 * q], buf[2 * q + 1]) for q in range(n)]
 
 
 def smc_set_shard(rank, world):

@@ -19,6 +19,15 @@ __global__ void smc_philox_debug(smc_u64 seed, smc_u64 traj, smc_u64 step0, smc_
     out[4 * q + 3] = r[3];
 }
 
+__global__ void smc_draw_debug(smc_u64 seed, smc_u64 traj, smc_u64 step0, smc_u32 n, double* out) {
+    const smc_u32 q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= n) return;
+    double e, u2;
+    smc_draw(seed, traj, step0 + q, e, u2);
+    out[2 * q] = e;
+    out[2 * q + 1] = u2;
+}
+
 // Counts of the replicas [i0, i1) of a speculative batch whose per-replica
 // verdicts / event counts sit at v[i - base], e[i - base] (prefix-exact Wilson
 // rounds).  Adds into counters {n_true, n_false, events, errors}.
@@ -47,5 +56,12 @@ cudaError_t smc_launch_philox_debug(uint64_t seed, uint64_t traj, uint64_t step0
                                     cudaStream_t stream) {
     if (n == 0) return cudaSuccess;
     smc_philox_debug<<<(n + 127) / 128, 128, 0, stream>>>(seed, traj, step0, n, dev_out);
+    return cudaGetLastError();
+}
+
+cudaError_t smc_launch_draw_debug(uint64_t seed, uint64_t traj, uint64_t step0, uint32_t n, double* dev_out,
+                                  cudaStream_t stream) {
+    if (n == 0) return cudaSuccess;
+    smc_draw_debug<<<(n + 127) / 128, 128, 0, stream>>>(seed, traj, step0, n, dev_out);
     return cudaGetLastError();
 }

@@ -260,18 +260,15 @@ std::string model_code_thread(const Model& m) {
         if (pos) o << "    grown |= x[" << s << "];\n";
     }
     o << "    return grown >= 0;\n}\n";
-    // dependency graph: a_k recomputed iff k in dep(j)
+    // Propensity update after R_j fired.  In a thread-owned warp the 32 lanes fire
+    // different reactions, so the union of dep(j) over the warp is (nearly) every
+    // reaction and a masked update executes every law anyway plus the mask tests and
+    // branches; the kernel therefore recomputes all M laws (straight-line, bit-identical
+    // to recomputing only dep(j)).  The dependency graph drives the tile variant, where
+    // M >> 32.
     o << "__device__ __forceinline__ void smc_update(int j, double (&a)[SMC_M], const int (&x)[SMC_N], const double* __restrict__ H) {\n";
-    for (int k = 0; k < M; ++k) {
-        uint64_t mask = 0;
-        for (int j = 0; j < M; ++j)
-            for (int d : m.dep[(size_t)j])
-                if (d == k) mask |= 1ull << j;
-        uint64_t all = (M == 64) ? ~0ull : ((1ull << M) - 1ull);
-        if (mask == 0) continue;
-        if (mask == all) o << "    a[" << k << "] = smc_law" << k << "(x, H);\n";
-        else o << "    if ((0x" << std::hex << mask << std::dec << "ull >> j) & 1ull) a[" << k << "] = smc_law" << k << "(x, H);\n";
-    }
+    o << "    (void)j;\n";
+    for (int k = 0; k < M; ++k) o << "    a[" << k << "] = smc_law" << k << "(x, H);\n";
     o << "}\n";
     o << "__device__ __forceinline__ int smc_last_positive(const double (&a)[SMC_M]) {\n    return ";
     for (int k = M - 1; k >= 1; --k) o << "a[" << k << "] > 0.0 ? " << k << " : ";

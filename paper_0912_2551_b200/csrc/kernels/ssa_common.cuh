@@ -45,6 +45,55 @@ __device__ __forceinline__ void smc_philox(smc_u32 c0, smc_u32 c1, smc_u32 c2, s
     r[0] = c0; r[1] = c1; r[2] = c2; r[3] = c3;
 }
 
+// Quotient num / den for a positive normal den: reciprocal seed (MUFU), two Newton
+// steps, then one residual correction q + r (num - q den).  The result is the
+// correctly rounded quotient except in rare last-ulp cases; it is used where the
+// parity bar tolerates ulp differences (tau = e / a0: the oracle's glibc log already
+// differs from any device log by an ulp now and then).
+__device__ __forceinline__ double smc_fdiv(double num, double den) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(den));
+    double e = __fma_rn(-den, r, 1.0);
+    r = __fma_rn(r, e, r);
+    e = __fma_rn(-den, r, 1.0);
+    r = __fma_rn(r, e, r);
+    const double q = __dmul_rn(num, r);
+    return __fma_rn(__fma_rn(-q, den, num), r, q);
+}
+
+// -log(x) for x in [2^-53, 1] (the u1 of smc_draw: positive, normal, <= 1).
+// The classic argument reduction of fdlibm's __ieee754_log: x = 2^k m with
+// m in [sqrt(2)/2, sqrt(2)), f = m - 1, s = f / (2 + f),
+// log(1 + f) = f - (hfsq - s (hfsq + R(s^2))), R the minimax series of fdlibm's
+// Lg1..Lg7, k ln2 split in ln2_hi + ln2_lo.  About 35 instructions instead of the
+// ~80 of the general libdevice log (no special cases: x is never 0, negative,
+// subnormal, inf or NaN here).  Accuracy: checked against glibc on the GPU
+// (tests/test_gpu_parity.py::test_draws_vs_oracle).
+__device__ __forceinline__ double smc_neglog(double x) {
+    int hx = __double2hiint(x);
+    const int lx = __double2loint(x);
+    int k = (hx >> 20) - 1023;
+    hx &= 0x000fffff;
+    const int i = (hx + 0x95f64) & 0x100000;
+    const double m = __hiloint2double(hx | (i ^ 0x3ff00000), lx);
+    k += i >> 20;
+    const double f = __dadd_rn(m, -1.0);
+    const double s = smc_fdiv(f, __dadd_rn(2.0, f));
+    const double dk = (double)k;
+    const double z = __dmul_rn(s, s), w = __dmul_rn(z, z);
+    const double t1 = __dmul_rn(w, __fma_rn(w, __fma_rn(w, 1.531383769920937332e-01, 2.222219843214978396e-01),
+                                            3.999999999940941908e-01));
+    const double t2 = __dmul_rn(z, __fma_rn(w, __fma_rn(w, __fma_rn(w, 1.479819860511658591e-01,
+                                                                       1.818357216161805012e-01),
+                                                             2.857142874366239149e-01),
+                                            6.666666666666735130e-01));
+    const double R = __dadd_rn(t2, t1);
+    const double hfsq = __dmul_rn(__dmul_rn(0.5, f), f);
+    const double inner = __fma_rn(s, __dadd_rn(hfsq, R), __dmul_rn(dk, 1.90821492927058770002e-10));
+    const double lg = __fma_rn(dk, 6.93147180369123816490e-01, -__dadd_rn(__dadd_rn(hfsq, -inner), -f));
+    return -lg;
+}
+
 // The draw of SSA step `step` of trajectory `traj` ("standard Monte Carlo
 // methods"):  e = -log(u1) (Eq. 2a numerator), u2 (Eq. 2b).
 //   u1 = ((((r0<<32)|r1) >> 11) + 1) * 2^-53 in (0,1],  u2 = (((r2<<32)|r3) >> 11) * 2^-53 in [0,1)
@@ -56,7 +105,13 @@ __device__ __forceinline__ void smc_draw(smc_u64 seed, smc_u64 traj, smc_u64 ste
     const smc_u64 w2 = ((smc_u64)r[2] << 32) | r[3];
     const double u1 = __dmul_rn(__ull2double_rn((w1 >> 11) + 1ull), 0x1p-53);   // 2^-53, exact
     u2 = __dmul_rn(__ull2double_rn(w2 >> 11), 0x1p-53);
-    e = -log(u1);
+    e = smc_neglog(u1);
+}
+
+// tau = e / a0 (Eq. 2a) for a0 > 0 finite; IEEE division below the range where the
+// reciprocal seed is exact enough (|log2 a0| > 1000 never occurs for physical rates).
+__device__ __forceinline__ double smc_tau(double e, double a0) {
+    return (a0 > 0x1p-1000 && a0 < 0x1p+1000) ? smc_fdiv(e, a0) : __ddiv_rn(e, a0);
 }
 
 // Kleene three-valued logic (reading R4): 0 false, 1 true, 2 unknown/pending.

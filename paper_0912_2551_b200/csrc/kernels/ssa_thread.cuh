@@ -94,7 +94,7 @@ extern "C" __global__ void __launch_bounds__(SMC_BLOCK, SMC_MINB) smc_ssa_thread
 #pragma unroll
             for (int m = 1; m < SMC_M; ++m) c[m] = __dadd_rn(c[m - 1], a[m]);
             const double A = c[SMC_M - 1];
-            const double tn = __dadd_rn(t, __ddiv_rn(e_cur, A));
+            const double tn = __dadd_rn(t, smc_tau(e_cur, A));
             int v = -1;
             if (!(A > 0.0) || A > 1.7976931348623157e308) {
                 if (A == 0.0) {                           // absorbed (reading R7)

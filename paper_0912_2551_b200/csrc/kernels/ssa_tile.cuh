@@ -239,7 +239,7 @@ extern "C" __global__ void __launch_bounds__(512, 1) smc_ssa_tile(SmcParams P) {
             const int q = (int)(k - kb) & (TW - 1);
             const double E = __shfl_sync(SMC_FULL, Eb, q, TW);
             const double U = __shfl_sync(SMC_FULL, Ub, q, TW);
-            const double tn = __dadd_rn(t, __ddiv_rn(E, A));
+            const double tn = __dadd_rn(t, smc_tau(E, A));
             int v = -1;
             if (act) {
                 if (!(A > 0.0) || A > 1.7976931348623157e308) {

@@ -13,6 +13,8 @@
 // AOT kernel launcher (aot_kernels.cu)
 cudaError_t smc_launch_philox_debug(uint64_t seed, uint64_t traj, uint64_t step0, uint32_t n, uint32_t* dev_out,
                                     cudaStream_t stream);
+cudaError_t smc_launch_draw_debug(uint64_t seed, uint64_t traj, uint64_t step0, uint32_t n, double* dev_out,
+                                  cudaStream_t stream);
 cudaError_t smc_launch_count_range(const unsigned char* v, const int* e, uint64_t n, long long* counters,
                                    cudaStream_t stream);
 
@@ -503,6 +505,23 @@ int smc_philox_blocks(uint64_t seed, uint64_t trajectory, uint64_t step0, uint32
         void* d = dalloc((size_t)n * 16 + 16);
         try {
             ck(smc_launch_philox_debug(seed, trajectory, step0, n, (uint32_t*)d, stream()), "philox kernel");
+            ck(cudaMemcpyAsync(host_out, d, (size_t)n * 16, cudaMemcpyDeviceToHost, stream()), "D2H");
+            ck(cudaStreamSynchronize(stream()), "sync");
+        } catch (...) {
+            dfree(d);
+            throw;
+        }
+        dfree(d);
+        return SMC_OK;
+    });
+}
+
+int smc_draw_blocks(uint64_t seed, uint64_t trajectory, uint64_t step0, uint32_t n, double* host_out) {
+    if (!host_out) { set_error("smc_draw_blocks: NULL"); return SMC_E_ARG; }
+    return guard([&] {
+        void* d = dalloc((size_t)n * 16 + 16);
+        try {
+            ck(smc_launch_draw_debug(seed, trajectory, step0, n, (double*)d, stream()), "draw kernel");
             ck(cudaMemcpyAsync(host_out, d, (size_t)n * 16, cudaMemcpyDeviceToHost, stream()), "D2H");
             ck(cudaStreamSynchronize(stream()), "sync");
         } catch (...) {

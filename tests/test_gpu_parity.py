@@ -310,3 +310,21 @@ def test_all_law_kinds_vs_oracle(smc, variant):
     a, ae, v, e, ov, oe = _compare(smc, cfg, cfg["seed"], 0, 2000, variant)
     assert ae >= 1999 / 2000, (variant, a, ae)
     assert 0 < v.mean() < 1 and e.mean() > 20
+
+
+def test_draws_vs_oracle(smc):
+    """The device draw (Philox -> u53 -> fast -log, reading R18) against the oracle's:
+    u2 bit-exact, e = -log(u1) within 1 ulp of glibc and bit-identical for >= 90 %."""
+    import struct
+    n_exact = n_tot = 0
+    for seed, traj, step0 in [(1, 0, 0), (7, 123456, 10_000), (2**64 - 1, 2**40 + 7, 2**33)]:
+        d = smc.smc_draw_blocks(seed, traj, step0, 4096)
+        for q, (e, u2) in enumerate(d):
+            u1o, u2o = O.uniforms(seed, traj, step0 + q)
+            assert u2 == u2o
+            eo = -math.log(u1o)
+            ulp = abs(struct.unpack("<q", struct.pack("<d", e))[0] - struct.unpack("<q", struct.pack("<d", eo))[0])
+            assert ulp <= 1, (seed, traj, step0 + q, e, eo)
+            n_exact += ulp == 0
+            n_tot += 1
+    assert n_exact / n_tot >= 0.90
