@@ -397,6 +397,7 @@ std::string generate_source(const Model& m, const Property& p, int variant, cons
     if (variant == 1) {
         // >= 4 resident CTAs of 128 threads: at most 128 registers per thread
         o << "#define SMC_BLOCK 128\n#define SMC_MINB 4\n";
+        if (const char* e = std::getenv("SMC_STRAIGHT")) o << "#define SMC_STRAIGHT " << std::atoi(e) << "\n";
     } else {
         o << "#define SMC_TW " << tl->tw << "\n#define SMC_GS " << tl->gs << "\n#define SMC_CH " << tl->ch
           << "\n#define SMC_NPAD " << tl->n_pad << "\n";

@@ -108,11 +108,12 @@ __device__ __forceinline__ void smc_draw(smc_u64 seed, smc_u64 traj, smc_u64 ste
     e = smc_neglog(u1);
 }
 
-// tau = e / a0 (Eq. 2a) for a0 > 0 finite; IEEE division below the range where the
-// reciprocal seed is exact enough (|log2 a0| > 1000 never occurs for physical rates).
-__device__ __forceinline__ double smc_tau(double e, double a0) {
-    return (a0 > 0x1p-1000 && a0 < 0x1p+1000) ? smc_fdiv(e, a0) : __ddiv_rn(e, a0);
-}
+// tau = e / a0 (Eq. 2a).  The kernels call it only for a0 in [2^-1000, 2^1000], where
+// the reciprocal seed is accurate; a0 outside that range (but > 0) ends the replica as
+// an error (reading R19) instead of taking a slow IEEE path inside the event loop.
+#define SMC_A_MIN 0x1p-1000
+#define SMC_A_MAX 0x1p+1000
+__device__ __forceinline__ double smc_tau(double e, double a0) { return smc_fdiv(e, a0); }
 
 // Kleene three-valued logic (reading R4): 0 false, 1 true, 2 unknown/pending.
 __device__ __forceinline__ int smc_knot(int a) { return a == 2 ? 2 : 1 - a; }

@@ -242,7 +242,7 @@ extern "C" __global__ void __launch_bounds__(512, 1) smc_ssa_tile(SmcParams P) {
             const double tn = __dadd_rn(t, smc_tau(E, A));
             int v = -1;
             if (act) {
-                if (!(A > 0.0) || A > 1.7976931348623157e308) {
+                if (!(A >= SMC_A_MIN) || A > SMC_A_MAX) {            // A == 0: absorbed; else error (R19)
                     if (A == 0.0) { mon.absorb(); v = mon.verdict(); }     // absorbed (reading R7)
                     else v = 2;                                            // bad propensity
                 } else {
