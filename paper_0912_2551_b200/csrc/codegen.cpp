@@ -398,6 +398,11 @@ std::string generate_source(const Model& m, const Property& p, int variant, cons
         // >= 4 resident CTAs of 128 threads: at most 128 registers per thread
         o << "#define SMC_BLOCK 128\n#define SMC_MINB 4\n";
         if (const char* e = std::getenv("SMC_STRAIGHT")) o << "#define SMC_STRAIGHT " << std::atoi(e) << "\n";
+        // two-stage draw pipeline: shorter per-event chain (-12 % at low occupancy, C2) for
+        // register-light models; heavier models are throughput-bound and keep one stage
+        int pipe2 = (m.M <= 8 && m.N <= 8) ? 1 : 0;
+        if (const char* e = std::getenv("SMC_PIPE2")) pipe2 = std::atoi(e);
+        o << "#define SMC_PIPE2 " << pipe2 << "\n";
     } else {
         o << "#define SMC_TW " << tl->tw << "\n#define SMC_GS " << tl->gs << "\n#define SMC_CH " << tl->ch
           << "\n#define SMC_NPAD " << tl->n_pad << "\n";

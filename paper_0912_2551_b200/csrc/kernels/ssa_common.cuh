@@ -97,15 +97,23 @@ __device__ __forceinline__ double smc_neglog(double x) {
 // The draw of SSA step `step` of trajectory `traj` ("standard Monte Carlo
 // methods"):  e = -log(u1) (Eq. 2a numerator), u2 (Eq. 2b).
 //   u1 = ((((r0<<32)|r1) >> 11) + 1) * 2^-53 in (0,1],  u2 = (((r2<<32)|r3) >> 11) * 2^-53 in [0,1)
-__device__ __forceinline__ void smc_draw(smc_u64 seed, smc_u64 traj, smc_u64 step, double& e, double& u2) {
-    smc_u32 r[4];
+// Split in its integer half (the Philox block) and its fp64 half (u53 + log) so the
+// thread kernel can pipeline them one step apart.
+__device__ __forceinline__ void smc_draw_words(smc_u64 seed, smc_u64 traj, smc_u64 step, smc_u32 r[4]) {
     smc_philox((smc_u32)step, (smc_u32)(step >> 32), (smc_u32)traj, (smc_u32)(traj >> 32), (smc_u32)seed,
                (smc_u32)(seed >> 32), r);
+}
+__device__ __forceinline__ void smc_draw_from(const smc_u32 r[4], double& e, double& u2) {
     const smc_u64 w1 = ((smc_u64)r[0] << 32) | r[1];
     const smc_u64 w2 = ((smc_u64)r[2] << 32) | r[3];
     const double u1 = __dmul_rn(__ull2double_rn((w1 >> 11) + 1ull), 0x1p-53);   // 2^-53, exact
     u2 = __dmul_rn(__ull2double_rn(w2 >> 11), 0x1p-53);
     e = smc_neglog(u1);
+}
+__device__ __forceinline__ void smc_draw(smc_u64 seed, smc_u64 traj, smc_u64 step, double& e, double& u2) {
+    smc_u32 r[4];
+    smc_draw_words(seed, traj, step, r);
+    smc_draw_from(r, e, u2);
 }
 
 // tau = e / a0 (Eq. 2a).  The kernels call it only for a0 in [2^-1000, 2^1000], where

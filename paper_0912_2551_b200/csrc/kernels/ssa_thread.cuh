@@ -31,6 +31,9 @@
 #ifndef SMC_STRAIGHT
 #define SMC_STRAIGHT 0
 #endif
+#ifndef SMC_PIPE2
+#define SMC_PIPE2 0
+#endif
 #ifndef SMC_BURST
 #define SMC_BURST 8
 #endif
@@ -43,6 +46,9 @@ extern "C" __global__ void __launch_bounds__(SMC_BLOCK, SMC_MINB) smc_ssa_thread
     double a[SMC_M];
     double t = 0.0, tp = 0.0;
     double e_cur = 0.0, u_cur = 0.0;      // draw of the current step k
+#if SMC_PIPE2
+    smc_u32 r_nx[4] = {0u, 0u, 0u, 0u};   // Philox block of step k+1 (its u53 + log run in step k)
+#endif
     smc_u32 k = 0;
     smc_u64 rel = 0, traj = 0;
     SmcMon mon;
@@ -80,6 +86,9 @@ extern "C" __global__ void __launch_bounds__(SMC_BLOCK, SMC_MINB) smc_ssa_thread
                     } else {
                         busy = true;
                         smc_draw(P.seed, traj, 0ull, e_cur, u_cur);
+#if SMC_PIPE2
+                        smc_draw_words(P.seed, traj, 1ull, r_nx);
+#endif
                     }
                 }
             }
@@ -91,7 +100,14 @@ extern "C" __global__ void __launch_bounds__(SMC_BLOCK, SMC_MINB) smc_ssa_thread
             if (!busy) continue;
             // ---- one SSA event of this lane's trajectory
             double e_nx, u_nx;                            // step k+1's draw, off the critical path
+#if SMC_PIPE2
+            // two independent chains: fp64 half of step k+1's draw, integer half of step k+2's
+            smc_draw_from(r_nx, e_nx, u_nx);
+            smc_u32 r_nx2[4];
+            smc_draw_words(P.seed, traj, (smc_u64)k + 2ull, r_nx2);
+#else
             smc_draw(P.seed, traj, (smc_u64)k + 1ull, e_nx, u_nx);
+#endif
             double c[SMC_M];
             c[0] = a[0];
 #pragma unroll
@@ -130,6 +146,9 @@ extern "C" __global__ void __launch_bounds__(SMC_BLOCK, SMC_MINB) smc_ssa_thread
                     ++k;
                     e_cur = e_nx;
                     u_cur = u_nx;
+#if SMC_PIPE2
+                    for (int q = 0; q < 4; ++q) r_nx[q] = r_nx2[q];
+#endif
                     mon.enter(k, t, tp, x);
                     v = mon.verdict();
                     if (v < 0 && k >= cap) v = 2;
@@ -166,6 +185,9 @@ extern "C" __global__ void __launch_bounds__(SMC_BLOCK, SMC_MINB) smc_ssa_thread
                         ++k;
                         e_cur = e_nx;
                         u_cur = u_nx;
+#if SMC_PIPE2
+                        for (int q = 0; q < 4; ++q) r_nx[q] = r_nx2[q];
+#endif
                         mon.enter(k, t, tp, x);
                         v = mon.verdict();
                         if (v < 0 && k >= cap) v = 2;
