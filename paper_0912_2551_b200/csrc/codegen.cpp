@@ -305,7 +305,7 @@ HillTables pack_hill_tables(const Model& m) {
 int tile_width(const Model& m) {
     if (const char* e = std::getenv("SMC_TILE_WIDTH")) {
         int w = std::atoi(e);
-        if (w == 8 || w == 16 || w == 32) return w;
+        if (w == 4 || w == 8 || w == 16 || w == 32) return w;
     }
     return m.M <= 256 ? 8 : (m.M <= 512 ? 16 : 32);
 }
@@ -319,11 +319,11 @@ TileLayout pack_tables(const Model& m) {
     while (L.ch * L.tw < L.gs) L.ch *= 2;      // chunk per lane in the in-group selection (power of two)
     L.n_pad = (N + 3) & ~3;
     // per-trajectory slice: a[GS*TW] (fp64) + x[NPAD] (int32), 16-byte aligned; with several
-    // tiles per warp the slice is padded to 64 mod 128 bytes so that neighbouring tiles use
-    // opposite halves of the 32 banks
+    // tiles per warp the slice is padded to 8*TW mod 128 bytes so that the TPW tiles of a
+    // warp cover consecutive bank ranges (minimum wavefronts per warp access)
     L.tile_bytes = align16((size_t)L.gs * L.tw * 8 + 4 * (size_t)L.n_pad);
-    if (L.tw < 32)
-        while (L.tile_bytes % 128 != 64) L.tile_bytes += 16;
+    if (L.tw < 16)      // TW lanes x 8 B per access: tiles of a warp cover consecutive bank ranges
+        while (L.tile_bytes % 128 != (size_t)(8 * L.tw)) L.tile_bytes += 16;
     for (auto& r : m.R) {
         L.any_hill |= r.hill;
         int order = 0;

@@ -4,14 +4,14 @@
 // * Model tables (law table, change lists, dependency CSR) are staged ONCE per
 //   CTA from HBM into shared memory by a TMA bulk copy (cp.async.bulk ...
 //   mbarrier::complete_tx) and then read from smem only.
-// * A tile of SMC_TW lanes (8, 16 or 32) owns one trajectory; a warp runs
+// * A tile of SMC_TW lanes (4, 8, 16 or 32) owns one trajectory; a warp runs
 //   TPW = 32/SMC_TW trajectories in lock step.  x[N] and a[M] live in the tile's
 //   shared-memory slice; lane l of a tile owns the contiguous reaction group
 //   [l*GS, (l+1)*GS) and keeps its group sum S_l in a register.
 //   a(l, m) is stored at m*TW + (l ^ ((m / CH) % TW)): the group walk of the
 //   resum (all lanes at the same m) and the chunked in-group selection (lane c
 //   reads m = c*CH + i) are both bank-conflict free; tile slices are padded so
-//   the TPW tiles of a warp fall in alternate halves of the 32 banks.
+//   the TPW tiles of a warp cover consecutive bank ranges.
 // * Per event: a0 = inclusive tile scan of the TW group sums (fixed order),
 //   two-level selection (group by ballot on the scan, member by chunked scan
 //   inside the group), x += v_j by <= 4 lanes, then the dependency work of ALL

@@ -216,9 +216,9 @@ def test_large_networks_vs_oracle_fixture(smc, name):
     assert m.last_launch(p)["variant"] == 2
 
 
-@pytest.mark.parametrize("width", ["8", "16", "32"])
+@pytest.mark.parametrize("width", ["4", "8", "16", "32"])
 def test_tile_widths_vs_fixture(smc, width, monkeypatch):
-    """Every tile width of variant 2 (8/16/32 lanes per trajectory) gives the oracle's replicas."""
+    """Every tile width of variant 2 (4/8/16/32 lanes per trajectory) gives the oracle's replicas."""
     import json
     import os
     monkeypatch.setenv("SMC_TILE_WIDTH", width)
