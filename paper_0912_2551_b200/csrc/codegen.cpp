@@ -340,7 +340,11 @@ TileLayout pack_tables(const Model& m) {
     L.off_hill_n = o; o = align16(o + (L.any_hill ? 4 * (size_t)M : 0));
     L.off_chg = o; o = align16(o + 2 * 4 * (size_t)M);
     L.off_dep_off = o; o = align16(o + 4 * ((size_t)M + 1));
-    L.off_dep = o; o = align16(o + 4 * nnz);
+    // large networks: 2-byte dependency entries (k only, slot recomputed in the kernel) so
+    // the tables leave room for more resident trajectories
+    L.dep16 = M > 512;
+    if (const char* e = std::getenv("SMC_DEP16")) L.dep16 = std::atoi(e) != 0;
+    L.off_dep = o; o = align16(o + (L.dep16 ? 2 : 4) * nnz);
     L.bytes = o;
     L.blob.assign(L.bytes, 0);
     auto* x0 = (int32_t*)(L.blob.data() + L.off_x0);
@@ -375,6 +379,7 @@ TileLayout pack_tables(const Model& m) {
     }
     auto* doff = (uint32_t*)(L.blob.data() + L.off_dep_off);
     auto* dep = (uint32_t*)(L.blob.data() + L.off_dep);
+    auto* dep16 = (uint16_t*)(L.blob.data() + L.off_dep);
     if ((size_t)L.gs * L.tw > 65536) fail(SMC_E_MODEL, "tile variant: too many reactions for 16-bit slots");
     size_t pos = 0;
     for (int j = 0; j < M; ++j) {
@@ -382,7 +387,8 @@ TileLayout pack_tables(const Model& m) {
         for (int k : m.dep[(size_t)j]) {
             const int l = k / L.gs, mm = k % L.gs;       // owner lane, member (ssa_tile.cuh smc_slot)
             const uint32_t slot = (uint32_t)(mm * L.tw + (l ^ ((mm / L.ch) % L.tw)));
-            dep[pos++] = (uint32_t)k | (slot << 16);
+            if (L.dep16) dep16[pos++] = (uint16_t)k;
+            else dep[pos++] = (uint32_t)k | (slot << 16);
         }
     }
     doff[M] = (uint32_t)pos;
@@ -414,6 +420,7 @@ std::string generate_source(const Model& m, const Property& p, int variant, cons
         o << "#define SMC_TILE_BYTES " << tl->tile_bytes << "\n";
         o << "#define SMC_ANY_HILL " << (tl->any_hill ? 1 : 0) << "\n";
         o << "#define SMC_ANY_GENERAL " << (tl->any_general ? 1 : 0) << "\n";
+        o << "#define SMC_DEP16 " << (tl->dep16 ? 1 : 0) << "\n";
     }
     o << embedded_source("ssa_common.cuh") << "\n";
     if (variant == 1) o << model_code_thread(m) << "\n";

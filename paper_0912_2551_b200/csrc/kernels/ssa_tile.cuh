@@ -26,7 +26,7 @@
 //   (state-independent, so batching them is exact).
 //
 // Generated hooks (codegen.cpp): SMC_N, SMC_M, SMC_TW, SMC_GS, SMC_CH, SMC_NPAD,
-//   SMC_OFF_*, SMC_TAB_BYTES, SMC_TILE_BYTES, SMC_ANY_HILL, SMC_ANY_GENERAL,
+//   SMC_OFF_*, SMC_TAB_BYTES, SMC_TILE_BYTES, SMC_ANY_HILL, SMC_ANY_GENERAL, SMC_DEP16,
 //   SMC_TMAX, SmcMon.
 
 __device__ __forceinline__ void smc_mbar_init(unsigned long long* bar, unsigned count) {
@@ -71,7 +71,11 @@ struct SmcTabs {
     const int* hill_n;
     const unsigned short* chg;       // [M][4]: species << 4 | (delta + 8), 0xFFFF = none
     const unsigned* dep_off;         // [M+1]
+#if SMC_DEP16
+    const unsigned short* dep;       // [nnz]: k (slot computed: halves the largest table)
+#else
     const unsigned* dep;             // [nnz]: k | slot(k) << 16
+#endif
 };
 
 // a_k(x) (readings R8/R9).  For order <= 2 the combinatorial count h is
@@ -114,6 +118,17 @@ __device__ __forceinline__ double smc_law_tab(int k, const int* xs, const SmcTab
 
 // smem slot of a(l, m), l = group (owner lane), m = member (SMC_CH is a power of two)
 __device__ __forceinline__ int smc_slot(int l, int m) { return m * SMC_TW + (l ^ ((m / SMC_CH) % SMC_TW)); }
+// dependency entry -> (reaction k, smem slot of a_k)
+__device__ __forceinline__ void smc_dep_entry(unsigned e, int& k, int& slot) {
+#if SMC_DEP16
+    k = (int)e;
+    const int l = k / SMC_GS, m = k - l * SMC_GS;
+    slot = smc_slot(l, m);
+#else
+    k = (int)(e & 0xFFFFu);
+    slot = (int)(e >> 16);
+#endif
+}
 // owner lane of a slot (inverse of smc_slot)
 __device__ __forceinline__ int smc_owner(int slot) { return (slot % SMC_TW) ^ ((slot / SMC_TW / SMC_CH) % SMC_TW); }
 
@@ -132,7 +147,7 @@ __device__ __forceinline__ double smc_group_sum(const double* at, int l) {
     return __dadd_rn(se, so);
 }
 
-extern "C" __global__ void __launch_bounds__(512, 1) smc_ssa_tile(SmcParams P) {
+extern "C" __global__ void __launch_bounds__(640, 1) smc_ssa_tile(SmcParams P) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ __align__(8) unsigned long long bar;
     const int lane = (int)(threadIdx.x & 31u), warp = (int)(threadIdx.x >> 5);
@@ -160,7 +175,11 @@ extern "C" __global__ void __launch_bounds__(512, 1) smc_ssa_tile(SmcParams P) {
     T.hill_n = (const int*)(smem + SMC_OFF_HN);
     T.chg = (const unsigned short*)(smem + SMC_OFF_CHG);
     T.dep_off = (const unsigned*)(smem + SMC_OFF_DOFF);
+#if SMC_DEP16
+    T.dep = (const unsigned short*)(smem + SMC_OFF_DEP);
+#else
     T.dep = (const unsigned*)(smem + SMC_OFF_DEP);
+#endif
     unsigned char* const warp_base = smem + SMC_TAB_BYTES + (size_t)warp * TPW * SMC_TILE_BYTES;
     double* at = (double*)(warp_base + (size_t)tile * SMC_TILE_BYTES);
     int* xs = (int*)(at + SMC_GS * TW);
@@ -316,9 +335,9 @@ extern "C" __global__ void __launch_bounds__(512, 1) smc_ssa_tile(SmcParams P) {
                 if (TPW == 1) {
                     for (unsigned b = (unsigned)lane; __any_sync(SMC_FULL, b < nd); b += 32u) {
                         if (b < nd) {
-                            const unsigned e = T.dep[d0 + b];
-                            const int slot = (int)(e >> 16);
-                            at[slot] = smc_law_tab((int)(e & 0xFFFFu), xs, T);
+                            int kk, slot;
+                            smc_dep_entry(T.dep[d0 + b], kk, slot);
+                            at[slot] = smc_law_tab(kk, xs, T);
                             touched |= 1u << smc_owner(slot);
                         }
                     }
@@ -338,11 +357,11 @@ extern "C" __global__ void __launch_bounds__(512, 1) smc_ssa_tile(SmcParams P) {
 #pragma unroll
                         for (int w = 1; w < TPW; ++w)
                             if (u == w) { o = off[w]; p0 = pre[w]; }
-                        const unsigned e = T.dep[o + (b - p0)];
-                        const int slot = (int)(e >> 16);
+                        int kk, slot;
+                        smc_dep_entry(T.dep[o + (b - p0)], kk, slot);
                         double* at_u = (double*)(warp_base + (size_t)u * SMC_TILE_BYTES);
                         const int* xs_u = (const int*)(at_u + SMC_GS * TW);
-                        at_u[slot] = smc_law_tab((int)(e & 0xFFFFu), xs_u, T);
+                        at_u[slot] = smc_law_tab(kk, xs_u, T);
                         touched |= 1u << (u * TW + smc_owner(slot));
                     }
                 }

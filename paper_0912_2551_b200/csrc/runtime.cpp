@@ -169,7 +169,7 @@ PropKernel& prepare(Model& m, const Property& p) {
         const size_t max_dyn = (size_t)d.max_smem_optin - fa.sharedSizeBytes;
         ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)max_dyn), "smem attr");
         int best_total = 0, best_w = 0, best_nb = 0;
-        for (int W = 16; W >= 1; --W) {
+        for (int W = 20; W >= 1; --W) {   // <= 640 threads (__launch_bounds__ of smc_ssa_tile)
             size_t smem = tl->bytes + (size_t)W * wb;
             if (smem > max_dyn) continue;
             int nb = 0;

@@ -113,6 +113,7 @@ struct TileLayout {               // packed model tables (variant 2), byte offse
     size_t off_chg = 0, off_dep_off = 0, off_dep = 0, bytes = 0;
     bool any_hill = false;
     bool any_general = false;     // a reaction of order 3-4 (int64 law path)
+    bool dep16 = false;           // 2-byte dependency entries (k only)
     int max_dep = 0;
     std::vector<uint8_t> blob;    // host copy
 };
