@@ -71,6 +71,19 @@ def model_stats(cfg):
     return [len(d) for d in deps], [len(c) for c in changes], sum(hill) / M
 
 
+def measured_traffic(workload, kernel):
+    """DRAM bytes (read + write) per launch of the SSA kernel from the committed ncu
+    --set full capture summary (profiles/traffic_<round>.json, scripts/ncu_traffic.py)."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "traffic_r*.json")))
+    if not files:
+        return None, None
+    d = json.load(open(files[-1])).get(workload)
+    if not d or d.get("kernel") != kernel:
+        return None, None
+    return d["dram_bytes_per_launch"], "%s: %s (%s)" % (os.path.basename(files[-1]), d["capture"], d["note"])
+
+
 # ------------------------------------------------------------------- clocks
 class ClockSampler:
     """nvidia-smi sampled every 100 ms from before the warm-up to after the timed region;
@@ -289,7 +302,7 @@ def main():
         tot_ms += e0.elapsed_time(e1)
         info = model.last_launch(prop)
         tot_kernel_ms += info["kernel_ms"]
-        launches += info["launches"]
+        launches += info["launches"] + info["aux_launches"]
         events += ev
         trajectories += tr
     clocks.window = (t_window0, time.time())
@@ -312,8 +325,11 @@ def main():
     peak = sms * 4 * sm_mhz * 1e6 / 1e9           # G warp-instructions / s (1 per SMSP per clock)
     per_gpu_events = events / world
     achieved = per_gpu_events * ipe / 32.0 / (tot_kernel_ms / 1e3) / 1e9
+    traffic, traffic_src = measured_traffic(cfg["name"], "smc_ssa_%s" % ("thread" if info["variant"] == 1 else "tile"))
     roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Gwarp-inst/s", "frac": achieved / peak,
-                "traffic": None, "kernel": "smc_ssa_%s" % ("thread" if info["variant"] == 1 else "tile"),
+                "traffic": traffic, "traffic_source": traffic_src,
+                "algorithmic_bytes_per_launch": "tables once per CTA + 64 B control block (no per-event HBM traffic)",
+                "kernel": "smc_ssa_%s" % ("thread" if info["variant"] == 1 else "tile"),
                 "inst_per_event": ipe, "kernel_ms_per_step": tot_kernel_ms / args.steps,
                 "kernel_share_of_step": tot_kernel_ms / tot_ms,
                 "peak_source": "148 SM x 4 SMSP x 1 warp-inst/clk x sm_max_mhz (MEASURED_PEAKS.json)"}

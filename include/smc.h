@@ -235,6 +235,8 @@ typedef struct {
     float kernel_ms;          /* CUDA-event time of the SSA kernels of that call    */
     float compile_ms;         /* NVRTC time of the kernel (first use)               */
     double table_bytes;       /* packed model + monitor tables read per CTA         */
+    int32_t aux_launches;     /* other kernels of that call (per-round count kernels) */
+    int32_t pad_;
 } smc_launch_info;
 /* Launch configuration and timing of the last run of (m, p). */
 int smc_last_launch(const smc_model* m, const smc_property* p, smc_launch_info* out);

@@ -263,10 +263,12 @@ void spec_round(Model& m, PropKernel& pk, uint64_t seed, uint64_t base, uint64_t
     auto count = [&](uint64_t a, uint64_t b) {       // [a, b) within this rank's slice of the batch
         a = std::max(a, d.spec_lo);
         b = std::min(b, d.spec_hi);
-        if (b > a)
+        if (b > a) {
             ck(smc_launch_count_range(d.spec_v + (a - d.spec_lo), d.spec_e + (a - d.spec_lo), b - a,
                                       (long long*)d.counters(), stream()),
                "count kernel");
+            pk.info.aux_launches += 1;
+        }
     };
     uint64_t covered = base;
     if (d.spec_valid && base >= d.spec_begin && base < d.spec_end) {
@@ -411,6 +413,7 @@ int smc_run(smc_model* h, const smc_property* ph, uint64_t n, uint64_t seed, smc
         if (!m.has_seed || m.last_seed != seed) { m.cursor = 0; m.last_seed = seed; m.has_seed = true; }
         PropKernel& pk = prepare(m, *ph->p);
         pk.info.launches = 0;
+        pk.info.aux_launches = 0;
         pk.info.kernel_ms = 0.f;
         int rc = run_round(m, *ph->p, seed, m.cursor, n, out);
         if (rc == SMC_OK) m.cursor += n;
@@ -429,6 +432,7 @@ int smc_estimate(smc_model* h, const smc_property* ph, double confidence, double
         std::lock_guard<std::mutex> lk(m.mu);
         PropKernel& pk = prepare(m, *ph->p);
         pk.info.launches = 0;
+        pk.info.aux_launches = 0;
         pk.info.kernel_ms = 0.f;
         m.dev->spec_valid = false;
         // no Fig. 2 round can reach past the conservative size Eq. 4(0.5) (N' <= Eq. 4(0.5))
@@ -490,6 +494,7 @@ int smc_run_verdicts(smc_model* h, const smc_property* ph, uint64_t first, uint6
         std::lock_guard<std::mutex> lk(m.mu);
         PropKernel& pk = prepare(m, *ph->p);
         pk.info.launches = 0;
+        pk.info.aux_launches = 0;
         pk.info.kernel_ms = 0.f;
         launch_slice(m, pk, seed, first, first + n, dev_verdict, dev_events);
         ck(cudaGetLastError(), "kernel launch");
