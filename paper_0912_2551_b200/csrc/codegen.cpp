@@ -421,6 +421,7 @@ std::string generate_source(const Model& m, const Property& p, int variant, cons
         o << "#define SMC_ANY_HILL " << (tl->any_hill ? 1 : 0) << "\n";
         o << "#define SMC_ANY_GENERAL " << (tl->any_general ? 1 : 0) << "\n";
         o << "#define SMC_DEP16 " << (tl->dep16 ? 1 : 0) << "\n";
+        if (const char* e = std::getenv("SMC_FLAT")) o << "#define SMC_FLAT " << std::atoi(e) << "\n";
     }
     o << embedded_source("ssa_common.cuh") << "\n";
     if (variant == 1) o << model_code_thread(m) << "\n";

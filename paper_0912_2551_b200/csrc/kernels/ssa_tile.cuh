@@ -116,6 +116,10 @@ __device__ __forceinline__ double smc_law_tab(int k, const int* xs, const SmcTab
     return a;
 }
 
+#ifndef SMC_FLAT
+#define SMC_FLAT 1      // dependency work of all tiles of a warp flattened over the 32 lanes
+#endif
+
 // smem slot of a(l, m), l = group (owner lane), m = member (SMC_CH is a power of two)
 __device__ __forceinline__ int smc_slot(int l, int m) { return m * SMC_TW + (l ^ ((m / SMC_CH) % SMC_TW)); }
 // dependency entry -> (reaction k, smem slot of a_k)
@@ -332,13 +336,14 @@ extern "C" __global__ void __launch_bounds__(640, 1) smc_ssa_tile(SmcParams P) {
             {
                 const unsigned d0 = go ? T.dep_off[j] : 0u;
                 const unsigned nd = go ? T.dep_off[j + 1] - d0 : 0u;
-                if (TPW == 1) {
-                    for (unsigned b = (unsigned)lane; __any_sync(SMC_FULL, b < nd); b += 32u) {
+                if (TPW == 1 || !SMC_FLAT) {              // each tile walks its own dep(j) with its TW lanes
+                    const smc_u32 tb = (TPW == 1) ? 0u : (smc_u32)(tile * TW);
+                    for (unsigned b = (unsigned)tl; __any_sync(SMC_FULL, b < nd); b += (unsigned)TW) {
                         if (b < nd) {
                             int kk, slot;
                             smc_dep_entry(T.dep[d0 + b], kk, slot);
                             at[slot] = smc_law_tab(kk, xs, T);
-                            touched |= 1u << smc_owner(slot);
+                            touched |= 1u << (tb + (smc_u32)smc_owner(slot));
                         }
                     }
                 } else {
