@@ -165,6 +165,14 @@ typedef struct {
 int smc_estimate(smc_model* m, const smc_property* p, double confidence, double half_width,
                  uint64_t seed, smc_estimate_t* out);
 
+/* smc_estimate with the start estimate of the first round as an argument
+ * (SURVEY §8(f) NEXT-4): start = 1.0 (or 0.0) is the iterative
+ * method of Fig. 2 (smc_estimate), start = 0.5 the conservative sample size
+ * Eq. 4(0.5) in one round (every later N' <= Eq. 4(0.5), so the loop stops
+ * after it).  start in [0, 1]; other errors as smc_estimate. */
+int smc_estimate_ex(smc_model* m, const smc_property* p, double confidence, double half_width,
+                    double start, uint64_t seed, smc_estimate_t* out);
+
 /* Same loop as smc_estimate with start estimate `start` (1.0 = iterative,
  * 0.5 = conservative) and the per-round replica runner supplied by the
  * caller (run(first, n, user, out) must return 0 and fill out with the counts

@@ -131,10 +131,14 @@ def _est(e):
                 events=int(e.events), errors=int(e.errors), rounds=int(e.rounds), z=e.z)
 
 
-def estimate(model, prop, confidence, half_width, seed):
-    """Fig. 2 iterative Wilson estimate (smc_estimate)."""
+def estimate(model, prop, confidence, half_width, seed, start=1.0):
+    """Fig. 2 Wilson estimate: start=1.0 iterative (smc_estimate), 0.5 conservative
+    (smc_estimate_ex)."""
     e = SmcEstimate()
-    check(lib().smc_estimate(model.h, prop.h, confidence, half_width, seed, ctypes.byref(e)))
+    if start == 1.0:
+        check(lib().smc_estimate(model.h, prop.h, confidence, half_width, seed, ctypes.byref(e)))
+    else:
+        check(lib().smc_estimate_ex(model.h, prop.h, confidence, half_width, start, seed, ctypes.byref(e)))
     return _est(e)
 
 

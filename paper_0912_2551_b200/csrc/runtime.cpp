@@ -423,8 +423,15 @@ int smc_run(smc_model* h, const smc_property* ph, uint64_t n, uint64_t seed, smc
 
 int smc_estimate(smc_model* h, const smc_property* ph, double confidence, double half_width, uint64_t seed,
                  smc_estimate_t* out) {
-    if (!h || !ph || !out || !(confidence > 0 && confidence < 1) || !(half_width > 0 && half_width < 0.5)) {
-        set_error("smc_estimate: need model, property, out, confidence in (0,1), half_width in (0,0.5)");
+    return smc_estimate_ex(h, ph, confidence, half_width, 1.0, seed, out);
+}
+
+int smc_estimate_ex(smc_model* h, const smc_property* ph, double confidence, double half_width, double start,
+                    uint64_t seed, smc_estimate_t* out) {
+    if (!h || !ph || !out || !(confidence > 0 && confidence < 1) || !(half_width > 0 && half_width < 0.5) ||
+        !(start >= 0.0 && start <= 1.0)) {
+        set_error("smc_estimate: need model, property, out, confidence in (0,1), half_width in (0,0.5), "
+                  "start in [0,1]");
         return SMC_E_ARG;
     }
     return guard([&] {
@@ -446,7 +453,7 @@ int smc_estimate(smc_model* h, const smc_property* ph, double confidence, double
                 }
                 return run_round(m, *ph->p, seed, base, n, c);
             },
-            confidence, half_width, 1.0, out);
+            confidence, half_width, start, out);
         m.dev->spec_valid = false;
         return rc;
     });

@@ -328,3 +328,25 @@ def test_draws_vs_oracle(smc):
             n_exact += ulp == 0
             n_tot += 1
     assert n_exact / n_tot >= 0.90
+
+
+@pytest.mark.parametrize("p", [0.0, 0.05, 0.5, 0.95, 1.0])
+def test_fig3_modes_vs_oracle(smc, p):
+    """NEXT-4: conservative (start 0.5) and iterative (Fig. 2) estimates of a
+    Bernoulli(p) CTMC through the GPU path equal the oracle's Fig. 2 on the oracle SSA,
+    replica for replica; the conservative size is Eq. 4(0.5) = 2648 at 2 eps = 0.05 / 99 %."""
+    cfg = workloads.bernoulli(p)
+    m, prop = _pair(smc, cfg)
+    om = O.OracleModel(cfg)
+    of = O.OracleFormula(cfg["formula"], cfg["species"])
+    for seed in (1, 2, 3):
+        for start in (1.0, 0.5):
+            g = smc.estimate(m, prop, 0.99, 0.025, seed, start=start)
+            o = wilson_procedure(lambda f, n: O.run(om, of, seed, f, n, per_traj=False)[0]["n_true"], 0.025, 0.99,
+                                 start=start)
+            assert (g["n_total"], g["n_true"]) == (o["n_total"], o["n_true"]), (p, seed, start)
+            assert (g["p_hat"], g["lower"], g["upper"]) == (o["p_hat"], o["lower"], o["upper"])
+            if start == 0.5:
+                assert g["n_total"] == 2648 and g["rounds"] == 1
+    if p in (0.0, 1.0):                          # the 88 % of P:392: 1 - 304 / 2648
+        assert smc.estimate(m, prop, 0.99, 0.025, 1)["n_total"] == 304

@@ -148,6 +148,17 @@ def c5():
     return _load("c5")
 
 
+def bernoulli(p, seed=0):
+    """A CTMC whose property is a Bernoulli(p) trial (Fig. 3 workload):
+    one molecule A, decay A -> 0 at rate 1, F[0,T](A == 0) with T = -ln(1 - p), so
+    P = 1 - e^{-T} = p (T = 0 for p = 0; T = 1000 for p = 1, e^{-1000} = 0 in binary64).
+    Each replica applies at most one event."""
+    T = 0.0 if p <= 0.0 else (1000.0 if p >= 1.0 else -math.log1p(-p))
+    return dict(name="BERN(%g)" % p, species=["A"], x0=[1], reactions=[_rx([(0, 1)], [], 1.0)],
+                formula="F[0,%r](A == 0)" % T, t_max=0.0, seed=seed,
+                sampling=dict(mode="wilson", confidence=0.99, half_width=0.025))
+
+
 CONFIGS = dict(C1=c1, C2=c2, C3=c3, C4=c4, C5=c5)
 
 
