@@ -409,6 +409,7 @@ std::string generate_source(const Model& m, const Property& p, int variant, cons
         int pipe2 = (m.M <= 8 && m.N <= 8) ? 1 : 0;
         if (const char* e = std::getenv("SMC_PIPE2")) pipe2 = std::atoi(e);
         o << "#define SMC_PIPE2 " << pipe2 << "\n";
+        if (const char* e = std::getenv("SMC_UNROLL")) o << "#define SMC_UNROLL " << std::atoi(e) << "\n";
     } else {
         o << "#define SMC_TW " << tl->tw << "\n#define SMC_GS " << tl->gs << "\n#define SMC_CH " << tl->ch
           << "\n#define SMC_NPAD " << tl->n_pad << "\n";

@@ -34,6 +34,9 @@
 #ifndef SMC_PIPE2
 #define SMC_PIPE2 0
 #endif
+#ifndef SMC_UNROLL
+#define SMC_UNROLL 1
+#endif
 #ifndef SMC_BURST
 #define SMC_BURST 8
 #endif
@@ -95,7 +98,7 @@ extern "C" __global__ void __launch_bounds__(SMC_BLOCK, SMC_MINB) smc_ssa_thread
         }
         if (!__any_sync(SMC_FULL, busy)) break;
 
-#pragma unroll 1
+#pragma unroll SMC_UNROLL
         for (int burst = 0; burst < SMC_BURST; ++burst) {
             if (!busy) continue;
             // ---- one SSA event of this lane's trajectory
