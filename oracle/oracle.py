@@ -36,6 +36,7 @@ def lib():
             L.orc_model_new.restype = c_vp
             L.orc_model_new.argtypes = [c_i32, c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp]
             L.orc_model_set_hill.argtypes = [c_vp, c_i32, c_i32, ctypes.c_double, c_i32]
+            L.orc_model_set_rate.argtypes = [c_vp, c_i32, ctypes.c_char_p, c_vp]
             L.orc_model_free.argtypes = [c_vp]
             L.orc_propensity.restype = ctypes.c_double
             L.orc_propensity.argtypes = [c_vp, c_i32, c_vp]
@@ -111,6 +112,10 @@ class OracleModel:
                 h = r["hill"]
                 if lib().orc_model_set_hill(self.h, j, h["repressor"], float(h["K"]), int(h["n"])) != 0:
                     raise ValueError("bad hill parameters")
+            if r.get("rate_expr"):
+                names = (ctypes.c_char_p * N)(*[n.encode() for n in cfg["species"]])
+                if lib().orc_model_set_rate(self.h, j, r["rate_expr"].encode(), ctypes.cast(names, ctypes.c_void_p)) != 0:
+                    raise ValueError(_err())
         self.N, self.M = N, M
 
     def propensity(self, j, x):

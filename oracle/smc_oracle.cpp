@@ -28,6 +28,7 @@
 //   streaming   -- pinned to the literal semantics (above).
 // Nothing in this file is "parity unpinned".
 // =============================================================================
+#include <cctype>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -90,6 +91,16 @@ void step_uniforms(uint64_t seed, uint64_t traj, uint64_t step, double* u1, doub
 // 2. The model: species counts x and reaction channels
 //    R_j with propensity a_j(x) and change vector v_j.
 // -----------------------------------------------------------------------------
+// Explicit rate expression (Table 2): a tree over
+// species counts (promoted to binary64) and decimal constants with + - * / and
+// unary minus, evaluated recursively in IEEE binary64 (left-associative).
+struct RateNode {
+    char op;            // 'c' constant, 'x' species, '+', '-', '*', '/', 'n' (negate)
+    double value = 0.0; // 'c'
+    int species = -1;   // 'x'
+    int a = -1, b = -1; // children
+};
+
 struct Reaction {
     std::vector<std::pair<int, int>> reactants;  // (species, stoichiometry), merged
     std::vector<std::pair<int, int>> change;     // (species, delta), delta != 0
@@ -98,6 +109,89 @@ struct Reaction {
     int repressor = -1;
     double K = 0.0;
     int n = 0;
+    std::vector<RateNode> rate;                  // explicit rate (root = back()), empty = mass action
+};
+
+double rate_eval(const std::vector<RateNode>& t, int i, const int64_t* x) {
+    const RateNode& n = t[(size_t)i];
+    switch (n.op) {
+        case 'c': return n.value;
+        case 'x': return (double)x[n.species];
+        case 'n': return -rate_eval(t, n.a, x);
+        case '+': return rate_eval(t, n.a, x) + rate_eval(t, n.b, x);
+        case '-': return rate_eval(t, n.a, x) - rate_eval(t, n.b, x);
+        case '*': return rate_eval(t, n.a, x) * rate_eval(t, n.b, x);
+        default: return rate_eval(t, n.a, x) / rate_eval(t, n.b, x);
+    }
+}
+
+// Recursive-descent parser: expr := term (('+'|'-') term)*, term := unary (('*'|'/') unary)*,
+// unary := '-' unary | primary, primary := number | name | '(' expr ')'.
+struct RateParser {
+    const std::string& s;
+    const std::vector<std::string>& names;
+    std::vector<RateNode>& out;
+    size_t p = 0;
+    [[noreturn]] void fail(const std::string& m) {
+        throw std::runtime_error("rate expression: " + m + " at " + std::to_string(p));
+    }
+    void ws() { while (p < s.size() && std::isspace((unsigned char)s[p])) ++p; }
+    int push(RateNode n) { out.push_back(n); return (int)out.size() - 1; }
+    int expr() {
+        int l = term();
+        for (;;) {
+            ws();
+            if (p < s.size() && (s[p] == '+' || s[p] == '-')) {
+                char o = s[p++];
+                int r = term();
+                RateNode n; n.op = o; n.a = l; n.b = r; l = push(n);
+            } else return l;
+        }
+    }
+    int term() {
+        int l = unary();
+        for (;;) {
+            ws();
+            if (p < s.size() && (s[p] == '*' || s[p] == '/')) {
+                char o = s[p++];
+                int r = unary();
+                RateNode n; n.op = o; n.a = l; n.b = r; l = push(n);
+            } else return l;
+        }
+    }
+    int unary() {
+        ws();
+        if (p < s.size() && s[p] == '-') { ++p; RateNode n; n.op = 'n'; n.a = unary(); return push(n); }
+        return primary();
+    }
+    int primary() {
+        ws();
+        if (p >= s.size()) fail("unexpected end");
+        if (s[p] == '(') {
+            ++p;
+            int e = expr();
+            ws();
+            if (p >= s.size() || s[p] != ')') fail("')' expected");
+            ++p;
+            return e;
+        }
+        if (std::isdigit((unsigned char)s[p]) || s[p] == '.') {
+            char* end = nullptr;
+            double v = std::strtod(s.c_str() + p, &end);
+            if (end == s.c_str() + p) fail("bad number");
+            p = (size_t)(end - s.c_str());
+            RateNode n; n.op = 'c'; n.value = v; return push(n);
+        }
+        if (std::isalpha((unsigned char)s[p]) || s[p] == '_') {
+            size_t q = p;
+            while (p < s.size() && (std::isalnum((unsigned char)s[p]) || s[p] == '_')) ++p;
+            std::string id = s.substr(q, p - q);
+            for (size_t i = 0; i < names.size(); ++i)
+                if (names[i] == id) { RateNode n; n.op = 'x'; n.species = (int)i; return push(n); }
+            fail("unknown species '" + id + "'");
+        }
+        fail("unexpected character");
+    }
 };
 
 struct Model {
@@ -110,6 +204,9 @@ struct Model {
 // combinations: x for stoichiometry 1 ("a_1 = c_1 x_1 x_2") and
 // x(x-1)/2 for a homodimer (reading R8); zero when a reactant is missing.
 // Hill repression (reading R9): a_j = c_j h_j / (1 + (x_r/K)^n).
+// Explicit rate: a_j = v(x), the propensity guard still applies (zero when a
+// reactant count is below its stoichiometry); a negative or NaN v is a bad
+// propensity (returned as NaN, the replica ends in error).
 double propensity(const Reaction& r, const int64_t* x) {
     int64_t h = 1;
     for (const auto& rs : r.reactants) {
@@ -117,6 +214,10 @@ double propensity(const Reaction& r, const int64_t* x) {
         if (xs < rs.second) return 0.0;
         if (rs.second == 1) h = h * xs;
         else h = h * (xs * (xs - 1) / 2);
+    }
+    if (!r.rate.empty()) {
+        double v = rate_eval(r.rate, (int)r.rate.size() - 1, x);
+        return (v >= 0.0) ? v : std::nan("");
     }
     double a = r.c * (double)h;
     if (r.hill) {
@@ -972,6 +1073,26 @@ int orc_model_set_hill(void* mp, int32_t j, int32_t repressor, double K, int32_t
     m->R[(size_t)j].K = K;
     m->R[(size_t)j].n = n;
     return 0;
+}
+// explicit rate expression for reaction j over species names[0..N) (replaces mass action)
+int orc_model_set_rate(void* mp, int32_t j, const char* expr, const char* const* names) {
+    auto* m = (Model*)mp;
+    if (j < 0 || j >= (int)m->R.size() || !expr || !names) return -1;
+    try {
+        std::vector<std::string> nm;
+        for (int i = 0; i < m->N; ++i) nm.push_back(names[i]);
+        std::vector<RateNode> t;
+        std::string text(expr);
+        RateParser P{text, nm, t};
+        P.expr();
+        P.ws();
+        if (P.p != text.size()) P.fail("trailing input");
+        m->R[(size_t)j].rate = t;
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
 }
 void orc_model_free(void* m) { delete (Model*)m; }
 
