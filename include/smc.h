@@ -81,6 +81,17 @@ int smc_model_create(int32_t n_species, const int32_t* init_counts,
  * K > 0, 1 <= n <= 8.  Must be called before the first run.  SMC_E_ARG otherwise. */
 int smc_model_set_hill(smc_model* m, int32_t reaction, int32_t repressor, double K, int32_t n);
 
+/* Explicit propensity for reaction j (Table 2),
+ * replacing c_j h_j(x): an expression over species names (species_names[N],
+ * NULL = S0..S{N-1}) and decimal constants with + - * /, unary minus and
+ * parentheses, evaluated in IEEE binary64 in tree order (left-associative;
+ * counts promoted to double).  The guard still applies: a_j = 0 while a
+ * reactant count is below its stoichiometry.  A negative or NaN value is a
+ * bad propensity (the replica ends as an error).  Not combinable with Hill.
+ * Must be called before the first run.  SMC_E_PARSE (message with the
+ * position) / SMC_E_ARG otherwise. */
+int smc_model_set_rate_expr(smc_model* m, int32_t reaction, const char* expr, const char* const* species_names);
+
 /* Force a kernel variant: 0 = automatic, 1 = thread-owned (registers;
  * requires N <= 32 and M <= 32), 2 = warp-owned tile (shared memory).
  * Variant 1 and 2 compute the same replicas; they differ only in where the

@@ -57,6 +57,7 @@ SIGNATURES = [
     ("smc_set_shard", c_i32, [c_i32, c_i32]),
     ("smc_set_allreduce", c_i32, [ALLREDUCE_FN, c_vp]),
     ("smc_run_verdicts", c_i32, [c_vp, c_vp, c_u64, c_u64, c_u64, c_vp, c_vp]),
+    ("smc_model_set_rate_expr", c_i32, [c_vp, c_i32, ctypes.c_char_p, c_vp]),
     ("smc_philox_blocks", c_i32, [c_u64, c_u64, c_u64, c_u32, c_vp]),
     ("smc_draw_blocks", c_i32, [c_u64, c_u64, c_u64, c_u32, c_vp]),
     ("smc_last_launch", c_i32, [c_vp, c_vp, ctypes.POINTER(SmcLaunchInfo)]),

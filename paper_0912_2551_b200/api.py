@@ -49,10 +49,15 @@ class Model:
                                      ctypes.byref(h)))
         self.h = h
         self.N, self.M = N, M
+        names = None
         for j, r in enumerate(reactions):
             hl = r.get("hill")
             if hl:
                 check(lib().smc_model_set_hill(self.h, j, int(hl["repressor"]), float(hl["K"]), int(hl["n"])))
+            if r.get("rate_expr"):
+                if names is None:
+                    names = (ctypes.c_char_p * N)(*[str(n).encode() for n in self.species])
+                check(lib().smc_model_set_rate_expr(self.h, j, r["rate_expr"].encode(), ctypes.cast(names, c_vp)))
 
     @classmethod
     def from_config(cls, cfg):

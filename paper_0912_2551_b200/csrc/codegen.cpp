@@ -201,6 +201,33 @@ struct MonGen {
     }
 };
 
+// ------------------------------------------------ explicit rate expressions ---
+// Straight-line IEEE binary64 code of an explicit rate tree (rates.cpp), in tree
+// order; xa = the count array expression ("x" in registers, "xs" in smem).
+std::string rate_code(const std::vector<RNode>& t, int i, const char* xa) {
+    const RNode& n = t[(size_t)i];
+    switch (n.k) {
+        case RNode::CONST: return dlit(n.v);
+        case RNode::SPECIES: return std::string("(double)") + xa + "[" + std::to_string(n.species) + "]";
+        case RNode::NEG: return "(-" + rate_code(t, n.a, xa) + ")";
+        case RNode::ADD: return "__dadd_rn(" + rate_code(t, n.a, xa) + ", " + rate_code(t, n.b, xa) + ")";
+        case RNode::SUB: return "__dadd_rn(" + rate_code(t, n.a, xa) + ", -" + rate_code(t, n.b, xa) + ")";
+        case RNode::MUL: return "__dmul_rn(" + rate_code(t, n.a, xa) + ", " + rate_code(t, n.b, xa) + ")";
+        case RNode::DIV: return "__ddiv_rn(" + rate_code(t, n.a, xa) + ", " + rate_code(t, n.b, xa) + ")";
+    }
+    return "0.0";
+}
+// body of an explicit law: the guard (a reactant below its stoichiometry -> 0), then
+// v(x); a negative or NaN value is returned as NaN (bad propensity, the replica errs)
+std::string explicit_body(const Reaction& r, const char* xa, const char* indent) {
+    std::ostringstream o;
+    for (int q = 0; q < 2; ++q)
+        if (r.s[q] >= 0) o << indent << "if (" << xa << "[" << r.s[q] << "] < " << r.st[q] << ") return 0.0;\n";
+    o << indent << "{ const double v = " << rate_code(r.rate, (int)r.rate.size() - 1, xa) << ";\n";
+    o << indent << "  return v >= 0.0 ? v : __longlong_as_double(0x7ff8000000000000LL); }\n";
+    return o.str();
+}
+
 // ------------------------------------------------- variant 1 model code ---
 std::string law_expr(const Reaction& r) {
     // h exact in int64, a = c * (double)h, Hill: a / (1 + q^n)
@@ -227,6 +254,10 @@ std::string model_code_thread(const Model& m) {
     for (int k = 0; k < M; ++k) {
         const Reaction& r = m.R[(size_t)k];
         o << "__device__ __forceinline__ double smc_law" << k << "(const int (&x)[SMC_N], const double* __restrict__ H) {\n";
+        if (!r.rate.empty()) {
+            o << "    (void)H;\n" << explicit_body(r, "x", "    ") << "}\n";
+            continue;
+        }
         if (ht.offset[(size_t)k] >= 0)   // zero-order Hill law: a_k(x_r) tabulated (same IEEE ops, host side)
             o << "    if (x[" << r.rep << "] < " << ht.size << ") return __ldg(H + " << ht.offset[(size_t)k] << " + x["
               << r.rep << "]);\n";
@@ -354,12 +385,14 @@ TileLayout pack_tables(const Model& m) {
         const Reaction& r = m.R[(size_t)j];
         // law kind (ssa_tile.cuh smc_law_tab): 0 h=1, 1 x0, 2 x0(x0-1)/2, 3 x0*x1, 4 general
         uint32_t kind, s0 = 0, s1 = 0;
-        if (r.s[0] < 0) kind = 0;
+        if (!r.rate.empty()) kind = 5;                  // explicit rate (generated smc_explicit)
+        else if (r.s[0] < 0) kind = 0;
         else if (r.s[1] < 0) { kind = r.st[0] == 1 ? 1u : 2u; s0 = s1 = (uint32_t)r.s[0]; }
         else { kind = (r.st[0] == 1 && r.st[1] == 1) ? 3u : 4u; s0 = (uint32_t)r.s[0]; s1 = (uint32_t)r.s[1]; }
         uint32_t w0 = s0 | (kind << 16) | ((uint32_t)(r.s[0] >= 0 ? r.st[0] : 1) << 20);
         uint32_t w1 = s1 | ((uint32_t)(r.s[1] >= 0 ? r.st[1] : 1) << 16);
         if (kind == 4 && r.s[1] < 0) fail(SMC_E_MODEL, "internal: general law with one reactant");
+        L.any_explicit |= kind == 5;
         if (r.hill) w0 |= 0x80000000u;
         unsigned char* law = L.blob.data() + L.off_law + 16 * (size_t)j;   // {u0, u1, double c}
         std::memcpy(law, &w0, 4);
@@ -422,10 +455,18 @@ std::string generate_source(const Model& m, const Property& p, int variant, cons
         o << "#define SMC_ANY_HILL " << (tl->any_hill ? 1 : 0) << "\n";
         o << "#define SMC_ANY_GENERAL " << (tl->any_general ? 1 : 0) << "\n";
         o << "#define SMC_DEP16 " << (tl->dep16 ? 1 : 0) << "\n";
+        o << "#define SMC_ANY_EXPLICIT " << (tl->any_explicit ? 1 : 0) << "\n";
         if (const char* e = std::getenv("SMC_FLAT")) o << "#define SMC_FLAT " << std::atoi(e) << "\n";
     }
     o << embedded_source("ssa_common.cuh") << "\n";
     if (variant == 1) o << model_code_thread(m) << "\n";
+    if (variant == 2 && tl->any_explicit) {          // explicit laws of the tile variant
+        o << "__device__ __noinline__ double smc_explicit(int k, const int* xs) {\n    switch (k) {\n";
+        for (int k = 0; k < m.M; ++k)
+            if (!m.R[(size_t)k].rate.empty())
+                o << "    case " << k << ":\n" << explicit_body(m.R[(size_t)k], "xs", "        ");
+        o << "    }\n    return 0.0;\n}\n";
+    }
     o << MonGen(p).emit() << "\n";
     o << embedded_source(variant == 1 ? "ssa_thread.cuh" : "ssa_tile.cuh") << "\n";
     return o.str();

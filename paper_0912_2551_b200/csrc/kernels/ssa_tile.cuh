@@ -27,6 +27,7 @@
 //
 // Generated hooks (codegen.cpp): SMC_N, SMC_M, SMC_TW, SMC_GS, SMC_CH, SMC_NPAD,
 //   SMC_OFF_*, SMC_TAB_BYTES, SMC_TILE_BYTES, SMC_ANY_HILL, SMC_ANY_GENERAL, SMC_DEP16,
+//   SMC_ANY_EXPLICIT (+ smc_explicit),
 //   SMC_TMAX, SmcMon.
 
 __device__ __forceinline__ void smc_mbar_init(unsigned long long* bar, unsigned count) {
@@ -85,6 +86,9 @@ struct SmcTabs {
 __device__ __forceinline__ double smc_law_tab(int k, const int* xs, const SmcTabs& T) {
     const SmcLaw L = T.law[k];
     const int kind = (int)((L.u0 >> 16) & 7u);
+#if SMC_ANY_EXPLICIT
+    if (kind == 5) return smc_explicit(k, xs);           // explicit rate (codegen.cpp)
+#endif
     const int v0 = xs[L.u0 & 0xFFFFu];
     const int v1 = xs[L.u1 & 0xFFFFu];
     double h;

@@ -21,6 +21,7 @@ std::vector<int> Model::law_species(int k) const {
     for (int q = 0; q < 2; ++q)
         if (r.s[q] >= 0) s.push_back(r.s[q]);
     if (r.hill) s.push_back(r.rep);
+    rate_species(r.rate, s);
     std::sort(s.begin(), s.end());
     s.erase(std::unique(s.begin(), s.end()), s.end());
     return s;
@@ -133,11 +134,31 @@ int smc_model_set_hill(smc_model* h, int32_t reaction, int32_t repressor, double
         return SMC_E_ARG;
     }
     if (m.dev) { set_error("smc_model_set_hill: model already used by a run"); return SMC_E_ARG; }
+    if (!m.R[(size_t)reaction].rate.empty()) { set_error("smc_model_set_hill: reaction has an explicit rate"); return SMC_E_ARG; }
     Reaction& r = m.R[(size_t)reaction];
     r.hill = true;
     r.rep = repressor;
     r.K = K;
     r.n = n;
+    m.deps_built = false;
+    return SMC_OK;
+}
+
+int smc_model_set_rate_expr(smc_model* h, int32_t reaction, const char* expr, const char* const* species_names) {
+    if (!h || !expr) { set_error("smc_model_set_rate_expr: NULL argument"); return SMC_E_ARG; }
+    Model& m = h->m;
+    std::lock_guard<std::mutex> lk(m.mu);
+    if (reaction < 0 || reaction >= m.M) { set_error("smc_model_set_rate_expr: reaction out of range"); return SMC_E_ARG; }
+    if (m.dev) { set_error("smc_model_set_rate_expr: model already used by a run"); return SMC_E_ARG; }
+    if (m.R[(size_t)reaction].hill) { set_error("smc_model_set_rate_expr: reaction has Hill repression"); return SMC_E_ARG; }
+    std::vector<std::string> names;
+    for (int s = 0; s < m.N; ++s) names.push_back(species_names ? std::string(species_names[s]) : "S" + std::to_string(s));
+    try {
+        m.R[(size_t)reaction].rate = parse_rate(expr, names);
+    } catch (const Error& e) {
+        set_error(e.msg);
+        return e.code;
+    }
     m.deps_built = false;
     return SMC_OK;
 }

@@ -21,6 +21,16 @@ struct Error {
 [[noreturn]] void fail(int code, const std::string& msg);
 
 // ----------------------------------------------------------------- model ---
+// Explicit rate expression node (rates.cpp); the root is the last node.
+struct RNode {
+    enum K { CONST, SPECIES, ADD, SUB, MUL, DIV, NEG } k = CONST;
+    double v = 0.0;
+    int species = -1;
+    int a = -1, b = -1;
+};
+std::vector<RNode> parse_rate(const std::string& expr, const std::vector<std::string>& names);
+void rate_species(const std::vector<RNode>& t, std::vector<int>& out);
+
 // One reaction channel R_j after normalisation.
 struct Reaction {
     int s[2] = {-1, -1};     // reactant species (merged), -1 = none
@@ -31,6 +41,7 @@ struct Reaction {
     int rep = -1;
     double K = 0.0;
     int n = 0;
+    std::vector<RNode> rate;   // explicit propensity (replaces c * h), empty = mass action
 };
 
 struct Kernel;        // compiled + loaded module (jit.cpp)
@@ -114,6 +125,7 @@ struct TileLayout {               // packed model tables (variant 2), byte offse
     bool any_hill = false;
     bool any_general = false;     // a reaction of order 3-4 (int64 law path)
     bool dep16 = false;           // 2-byte dependency entries (k only)
+    bool any_explicit = false;    // an explicit rate expression (generated smc_explicit)
     int max_dep = 0;
     std::vector<uint8_t> blob;    // host copy
 };

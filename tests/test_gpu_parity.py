@@ -350,3 +350,32 @@ def test_fig3_modes_vs_oracle(smc, p):
                 assert g["n_total"] == 2648 and g["rounds"] == 1
     if p in (0.0, 1.0):                          # the 88 % of P:392: 1 - 304 / 2648
         assert smc.estimate(m, prop, 0.99, 0.025, 1)["n_total"] == 304
+
+
+@pytest.mark.parametrize("variant", [1, 2])
+def test_explicit_rates_vs_oracle(smc, variant):
+    """NEXT-3: explicit propensities (repressed production, Michaelis-Menten conversion,
+    explicit decay) mixed with mass-action laws, thread and tile variants, replica by
+    replica against the oracle's independent parser / evaluator."""
+    cfg = workloads.explicit_demo()
+    a, ae, v, e, ov, oe = _compare(smc, cfg, cfg["seed"], 0, 3000, variant)
+    assert ae >= AGREE, (variant, a, ae)
+    assert 0.5 < v.mean() < 0.7
+
+
+def test_explicit_michaelis_menten_degradation_gpu_vs_matrix_exponential(smc):
+    """The GPU estimate of F[0,2.5](S == 0) for S -> 0 at 10 S/(5+S), S0 = 20, contains the
+    matrix-exponential value (the same pin as the oracle's, tests/test_oracle_rates.py)."""
+    from scipy.linalg import expm
+    rx = workloads._rx
+    cfg = dict(name="MMdeg", species=["S"], x0=[20], reactions=[dict(rx([(0, 1)], [], 1.0), rate_expr="10*S/(5+S)")],
+               formula="F[0,2.5](S == 0)", t_max=0.0, seed=3, sampling=dict(mode="fixed", n=10 ** 6))
+    Q = np.zeros((21, 21))
+    for s in range(1, 21):
+        Q[s, s], Q[s, s - 1] = -10 * s / (5 + s), 10 * s / (5 + s)
+    exact = float(expm(Q * 2.5)[20, 0])
+    m, p = _pair(smc, cfg)
+    c = m.run(p, 10 ** 6, 3)
+    n = c["n_true"] + c["n_false"]
+    lo, hi = wilson_interval(c["n_true"] / n, n, normal_quantile(0.999))
+    assert c["errors"] == 0 and lo <= exact <= hi

@@ -25,7 +25,7 @@ def header_symbols():
 def test_exports_every_declared_symbol():
     L = smc.lib()
     syms = header_symbols()
-    assert len(syms) == 27
+    assert len(syms) == 28
     for s in syms:
         assert hasattr(L, s), s
     assert sorted(n for n, _, _ in _native.SIGNATURES) == syms
@@ -136,3 +136,27 @@ def test_fig2_driver_matches_oracle_loop():
     assert lib_est["n_total"] == ref["n_total"] and lib_est["n_true"] == ref["n_true"]
     assert (lib_est["p_hat"], lib_est["lower"], lib_est["upper"]) == (ref["p_hat"], ref["lower"], ref["upper"])
     assert lib_est["rounds"] == ref["rounds"] == len(calls)
+
+
+def test_rate_expression_errors_and_codegen():
+    """smc_model_set_rate_expr: parse errors carry the position, unknown species and
+    Hill conflicts are rejected, and the generated law is straight-line IEEE code in
+    tree order with the guard."""
+    rx = workloads._rx
+    base = dict(name="r", species=["S", "P"], x0=[5, 0], formula="F[0,1](P > 2)", t_max=0.0, seed=1,
+                sampling=dict(mode="fixed", n=10))
+    for expr, where in [("2*", "at 2"), ("(S", "at 2"), ("S $ 2", "at 2"), ("Q", "at 0"), ("2 S", "at 2")]:
+        cfg = dict(base, reactions=[dict(rx([(0, 1)], [(1, 1)], 1.0), rate_expr=expr)])
+        with pytest.raises(smc.SmcError) as e:
+            smc.Model.from_config(cfg)
+        assert e.value.name == "SMC_E_PARSE" and where in str(e.value), (expr, str(e.value))
+    cfg = dict(base, reactions=[dict(rx([(0, 1)], [(1, 1)], 1.0), rate_expr="10*S/(5+S)",
+                                     hill=dict(repressor=1, K=2.0, n=2))])
+    with pytest.raises(smc.SmcError):
+        smc.Model.from_config(cfg)
+    cfg = dict(base, reactions=[dict(rx([(0, 1)], [(1, 1)], 1.0), rate_expr="-S*2 - 3/P + 1")])
+    m = smc.Model.from_config(cfg)
+    src = m.kernel_source(smc.Property(m, cfg["formula"]))
+    assert ("__dadd_rn(__dadd_rn(__dmul_rn((-(double)x[0]), 0x1p+1), -__ddiv_rn(0x1.8p+1, (double)x[1])), 0x1p+0)"
+            in src)
+    assert "if (x[0] < 1) return 0.0;" in src

@@ -159,7 +159,20 @@ def bernoulli(p, seed=0):
                 sampling=dict(mode="wilson", confidence=0.99, half_width=0.025))
 
 
-CONFIGS = dict(C1=c1, C2=c2, C3=c3, C4=c4, C5=c5)
+def explicit_demo():
+    """Explicit (non-mass-action) propensities (NEXT-3, Table 2 P:513-538 style):
+    repressed production 0 -> S at 20/(1 + I/10), Michaelis-Menten conversion S -> P at
+    10 S/(5 + S), mass-action P -> 0 (0.1) and P -> P + I (0.05), explicit I -> 0 at 0.2 I;
+    x0 = 0; F[0,20](P > 80) (p ~ 0.61, ~540 events per replica); seed 12."""
+    R = [dict(_rx([], [(0, 1)], 1.0), rate_expr="20/(1+I/10)"),
+         dict(_rx([(0, 1)], [(1, 1)], 1.0), rate_expr="10*S/(5+S)"),
+         _rx([(1, 1)], [], 0.1), _rx([(1, 1)], [(1, 1), (2, 1)], 0.05),
+         dict(_rx([(2, 1)], [], 1.0), rate_expr="0.2*I")]
+    return dict(name="EXPL", species=["S", "P", "I"], x0=[0, 0, 0], reactions=R, formula="F[0,20](P > 80)",
+                t_max=0.0, seed=12, sampling=dict(mode="fixed", n=100_000))
+
+
+CONFIGS = dict(C1=c1, C2=c2, C3=c3, C4=c4, C5=c5, EXPL=explicit_demo)
 
 
 def get(name):
