@@ -379,3 +379,12 @@ def test_explicit_michaelis_menten_degradation_gpu_vs_matrix_exponential(smc):
     n = c["n_true"] + c["n_false"]
     lo, hi = wilson_interval(c["n_true"] / n, n, normal_quantile(0.999))
     assert c["errors"] == 0 and lo <= exact <= hi
+
+
+@pytest.mark.parametrize("row", [0, 1, 2])
+def test_cell_cycle_rows_vs_oracle(smc, row):
+    """NEXT-3 workload: the best-effort cell-cycle model (explicit Table 2 rates) with the
+    three Table 3 formulas, GPU replicas against the oracle's."""
+    cfg = workloads.cell_cycle(workloads.CELL_CYCLE_FORMULAS[row])
+    a, ae, *_ = _compare(smc, cfg, cfg["seed"], 0, 2000)
+    assert ae >= AGREE, (row, a, ae)

@@ -172,7 +172,46 @@ def explicit_demo():
                 t_max=0.0, seed=12, sampling=dict(mode="fixed", n=100_000))
 
 
-CONFIGS = dict(C1=c1, C2=c2, C3=c3, C4=c4, C5=c5, EXPL=explicit_demo)
+CELL_CYCLE_FORMULAS = ["(a <= 4) U[0,1000] (y >= 5)", "(a <= 20) U[0,1000] (y >= 35)",
+                       "(a <= 40) U[0,1000] (y >= 40 & y <= 42)"]      # Table 3 rows
+
+
+def cell_cycle(formula=CELL_CYCLE_FORMULAS[0], seed=21):
+    """Best-effort budding-yeast cell-cycle toy model (Table 1 P:475-511,
+    Table 2).  Species x (Cdk/CycB), y (active APC/Cdh1),
+    y_in (inactive APC/Cdh1), a (Cdc20).  Counts n = c / alpha (alpha = 0.00236012,
+    Omega = 1/alpha ~ 424); propensities in counts per unit time:
+      R1x 0 -> x              k1 / alpha
+      R2x x -> 0              k2' x
+      R3x x + y -> y          k2'' alpha x y
+      R1y y_in -> y           k3' y_in / (J3 + alpha y_in)
+      R2y y_in + a -> y + a   k3'' alpha a y_in / (J3 + alpha y_in)   (Table 2's k3-triple-prime)
+      R3y x + y -> x + y_in   k4 m alpha x y / (J4 + alpha y)         (Table 2's k3-star)
+      R1a 0 -> a              k5' / alpha
+      R2a x -> x + a          k5'' m x / J5                           (Table 2's k5-star)
+      R3a a -> 0              k6 a
+    with Table 2's constants.  The paper gives no initial state; x0 = (212, 0, 424, 0)
+    (CycB at half of Omega, APC all inactive, no Cdc20: "low level of activated APC, high
+    Cdk/CycB, low Cdc20") is an assumption, so Table 3's probabilities are not
+    reproduced (reading G4)."""
+    alpha = 0.00236012
+    k1, k2p, k2pp, k3p, k3pp, k4, J3, J4 = 0.04, 0.04, 1.0, 1.0, 10.0, 35.0, 0.04, 0.04
+    k5p, k5pp, k6, J5, m = 0.005, 0.2, 0.1, 0.3, 0.8
+    A = repr(alpha)
+    R = [dict(_rx([], [(0, 1)], 1.0), rate_expr=repr(k1 / alpha)),
+         _rx([(0, 1)], [], k2p),
+         dict(_rx([(0, 1), (1, 1)], [(1, 1)], 1.0), rate_expr="%r*x*y" % (k2pp * alpha)),
+         dict(_rx([(2, 1)], [(1, 1)], 1.0), rate_expr="%r*y_in/(%r+%s*y_in)" % (k3p, J3, A)),
+         dict(_rx([(2, 1), (3, 1)], [(1, 1), (3, 1)], 1.0), rate_expr="%r*%s*a*y_in/(%r+%s*y_in)" % (k3pp, A, J3, A)),
+         dict(_rx([(0, 1), (1, 1)], [(0, 1), (2, 1)], 1.0), rate_expr="%r*%r*%s*x*y/(%r+%s*y)" % (k4, m, A, J4, A)),
+         dict(_rx([], [(3, 1)], 1.0), rate_expr=repr(k5p / alpha)),
+         dict(_rx([(0, 1)], [(0, 1), (3, 1)], 1.0), rate_expr="%r*%r*x/%r" % (k5pp, m, J5)),
+         _rx([(3, 1)], [], k6)]
+    return dict(name="CC", species=["x", "y", "y_in", "a"], x0=[212, 0, 424, 0], reactions=R, formula=formula,
+                t_max=0.0, seed=seed, sampling=dict(mode="wilson", confidence=0.99, half_width=0.025))
+
+
+CONFIGS = dict(C1=c1, C2=c2, C3=c3, C4=c4, C5=c5, EXPL=explicit_demo, CC=cell_cycle)
 
 
 def get(name):
