@@ -234,10 +234,16 @@ double propensity(const Reaction& r, const int64_t* x) {
 //    Atoms compare integer expressions over species counts, evaluated exactly
 //    in int64.
 // -----------------------------------------------------------------------------
-enum ExprKind { E_CONST, E_VAR, E_ADD, E_SUB, E_MUL, E_NEG };
+//    The general val of P:209 (val ~ val with ~ in {+,-,*,/}, func, Int, Real):
+//    an atom built only from Int constants, species, +, -, * is evaluated
+//    exactly in int64; an atom with '/', a Real constant or a function
+//    (sqrt, abs, min, max, pow(val, k) with an Int k >= 0) is evaluated in IEEE
+//    binary64, recursively in tree order, counts promoted to double.
+enum ExprKind { E_CONST, E_VAR, E_ADD, E_SUB, E_MUL, E_NEG, E_DIV, E_REAL, E_SQRT, E_ABS, E_MIN, E_MAX, E_POW };
 struct Expr {
     ExprKind kind;
-    int64_t value = 0;
+    int64_t value = 0;   // E_CONST; E_POW exponent
+    double real = 0.0;   // E_REAL
     int var = -1;
     int lhs = -1, rhs = -1;
 };
@@ -246,6 +252,7 @@ enum CmpOp { C_LT, C_LE, C_GE, C_GT, C_EQ, C_NE };
 struct Atom {
     int lhs, rhs;
     CmpOp op;
+    bool real = false;   // binary64 evaluation (see above)
 };
 
 struct Interval {  // I subset of R>=0; [0,inf) when omitted
@@ -289,9 +296,47 @@ int64_t eval_expr(const Formula& f, int e, const int64_t* x) {
     return 0;
 }
 
+double eval_real(const Formula& f, int e, const int64_t* x) {
+    const Expr& ex = f.exprs[e];
+    switch (ex.kind) {
+        case E_CONST: return (double)ex.value;
+        case E_REAL: return ex.real;
+        case E_VAR: return (double)x[ex.var];
+        case E_ADD: return eval_real(f, ex.lhs, x) + eval_real(f, ex.rhs, x);
+        case E_SUB: return eval_real(f, ex.lhs, x) - eval_real(f, ex.rhs, x);
+        case E_MUL: return eval_real(f, ex.lhs, x) * eval_real(f, ex.rhs, x);
+        case E_DIV: return eval_real(f, ex.lhs, x) / eval_real(f, ex.rhs, x);
+        case E_NEG: return -eval_real(f, ex.lhs, x);
+        case E_SQRT: return std::sqrt(eval_real(f, ex.lhs, x));
+        case E_ABS: return std::fabs(eval_real(f, ex.lhs, x));
+        case E_MIN: { double a = eval_real(f, ex.lhs, x), b = eval_real(f, ex.rhs, x); return a < b ? a : b; }
+        case E_MAX: { double a = eval_real(f, ex.lhs, x), b = eval_real(f, ex.rhs, x); return a > b ? a : b; }
+        case E_POW: {
+            double b = eval_real(f, ex.lhs, x), r = 1.0;
+            for (int64_t i = 0; i < ex.value; ++i) r = (i == 0) ? b : r * b;   // left-to-right product
+            return r;
+        }
+    }
+    return 0.0;
+}
+
+template <class T>
+bool compare(T l, T r, CmpOp op) {
+    switch (op) {
+        case C_LT: return l < r;
+        case C_LE: return l <= r;
+        case C_GE: return l >= r;
+        case C_GT: return l > r;
+        case C_EQ: return l == r;
+        case C_NE: return l != r;
+    }
+    return false;
+}
+
 // sigma |= (val' <| val'') iff Eval(sigma[0],val') <| Eval(sigma[0],val'')
 bool eval_atom(const Formula& f, int a, const int64_t* x) {
     const Atom& at = f.atoms[a];
+    if (at.real) return compare(eval_real(f, at.lhs, x), eval_real(f, at.rhs, x), at.op);
     int64_t l = eval_expr(f, at.lhs, x), r = eval_expr(f, at.rhs, x);
     switch (at.op) {
         case C_LT: return l < r;
@@ -385,17 +430,27 @@ struct Parser {
     }
     int term() {
         int l = factor();
-        while (eat("*")) { Expr e{E_MUL}; e.lhs = l; e.rhs = factor(); l = add_expr(e); }
-        return l;
+        for (;;) {
+            if (eat("*")) { Expr e{E_MUL}; e.lhs = l; e.rhs = factor(); l = add_expr(e); }
+            else if (eat("/")) { Expr e{E_DIV}; e.lhs = l; e.rhs = factor(); l = add_expr(e); }
+            else return l;
+        }
     }
     int factor() {
         ws();
         if (eat("-")) { Expr e{E_NEG}; e.lhs = factor(); return add_expr(e); }
         if (eat("(")) { int e = expr(); if (!eat(")")) fail("')' expected"); return e; }
-        if (p < s.size() && std::isdigit((unsigned char)s[p])) {
+        if (p < s.size() && (std::isdigit((unsigned char)s[p]) || s[p] == '.')) {
             size_t q = p;
             while (q < s.size() && std::isdigit((unsigned char)s[q])) ++q;
-            if (q < s.size() && (s[q] == '.' || s[q] == 'e' || s[q] == 'E')) fail("integer constant expected");
+            if (q < s.size() && (s[q] == '.' || s[q] == 'e' || s[q] == 'E')) {   // Real constant
+                char* end = nullptr;
+                Expr e{E_REAL};
+                e.real = std::strtod(s.c_str() + p, &end);
+                if (end == s.c_str() + p) fail("number expected");
+                p = (size_t)(end - s.c_str());
+                return add_expr(e);
+            }
             Expr e{E_CONST};
             e.value = std::stoll(s.substr(p, q - p));
             p = q;
@@ -405,6 +460,34 @@ struct Parser {
             size_t q = p;
             while (q < s.size() && is_ident_char(s[q])) ++q;
             std::string id = s.substr(p, q - p);
+            size_t r = q;
+            while (r < s.size() && std::isspace((unsigned char)s[r])) ++r;
+            if (r < s.size() && s[r] == '(') {                                 // func(...)
+                ExprKind k;
+                if (id == "sqrt") k = E_SQRT;
+                else if (id == "abs") k = E_ABS;
+                else if (id == "min") k = E_MIN;
+                else if (id == "max") k = E_MAX;
+                else if (id == "pow") k = E_POW;
+                else fail("unknown function '" + id + "'");
+                p = r + 1;
+                Expr e{k};
+                e.lhs = expr();
+                if (k == E_MIN || k == E_MAX) {
+                    if (!eat(",")) fail("',' expected");
+                    e.rhs = expr();
+                } else if (k == E_POW) {
+                    if (!eat(",")) fail("',' expected");
+                    ws();
+                    size_t t = p;
+                    while (t < s.size() && std::isdigit((unsigned char)s[t])) ++t;
+                    if (t == p) fail("integer exponent expected");
+                    e.value = std::stoll(s.substr(p, t - p));
+                    p = t;
+                }
+                if (!eat(")")) fail("')' expected");
+                return add_expr(e);
+            }
             for (size_t i = 0; i < names.size(); ++i)
                 if (names[i] == id) {
                     p = q;
@@ -415,6 +498,14 @@ struct Parser {
             fail("unknown species '" + id + "'");
         }
         fail("expression expected");
+    }
+    // an atom needs binary64 when it contains '/', a Real constant or a function
+    bool has_real(int e) {
+        const Expr& ex = f.exprs[(size_t)e];
+        if (ex.kind == E_DIV || ex.kind == E_REAL || ex.kind == E_SQRT || ex.kind == E_ABS || ex.kind == E_MIN ||
+            ex.kind == E_MAX || ex.kind == E_POW)
+            return true;
+        return (ex.lhs >= 0 && has_real(ex.lhs)) || (ex.rhs >= 0 && has_real(ex.rhs));
     }
     bool cmp_op(CmpOp* op) {
         ws();
@@ -476,7 +567,7 @@ struct Parser {
             CmpOp op;
             if (!cmp_op(&op)) throw std::runtime_error("no comparison");
             int r = expr();
-            f.atoms.push_back(Atom{l, r, op});
+            f.atoms.push_back(Atom{l, r, op, has_real(l) || has_real(r)});
             Node n{N_ATOM};
             n.atom = (int)f.atoms.size() - 1;
             return add_node(n);

@@ -186,3 +186,36 @@ def test_streaming_equals_literal_on_models():
         c2, v2, e2 = _estimate(cfg, cfg["formula"], n, cfg["seed"], mode="literal")
         assert (v1 == v2).all(), cfg["name"]
         assert (e1 <= e2).all()          # on-the-fly never generates more events
+
+
+@pytest.mark.parametrize("atom", ["A*A >= 64", "A/2 >= 4", "sqrt(A) > 2.8", "pow(A, 3) >= 512", "min(A, 100) >= 7.5",
+                                  "max(A, 0.5) > 7.9", "abs(-A) >= 8", "8.0 <= A", "(A - 0.5) * 2 >= 15"])
+def test_general_val_atoms_pure_birth(atom):
+    """General val atoms (val ~ val, func, Int, Real) that are equivalent to A >= 8 on
+    integer counts give the pure-birth closed form P(Poisson(6) >= 8) -- and, on the same
+    Philox streams, exactly the replicas of the integer atom (binary64 path vs int64 path)."""
+    cfg = _model(["A"], [0], [([], [(0, 1)], 2.0)])
+    exact = float(stats.poisson.sf(7, 6.0))
+    c, v, e = _estimate(cfg, "F[0,3](%s)" % atom, 20_000, 71)
+    ci, vi, ei = _estimate(cfg, "F[0,3](A >= 8)", 20_000, 71)
+    assert (v == vi).all() and (e == ei).all()
+    assert _contains(exact, c["n_true"], 20_000)
+
+
+def test_general_val_atom_values():
+    """Hand states for the paper's example atom X1 < sqrt(X2) and the binary64
+    corner cases: division by zero gives inf (X2 / X1 > 1e300 true at X1 = 0), 0/0 is NaN
+    (every comparison false, != true)."""
+    cfg = _model(["X1", "X2"], [0, 0], [([], [(0, 1)], 1.0)])
+    m = O.OracleModel(cfg)
+
+    def holds(f, x1, x2):
+        fo = O.OracleFormula(f, cfg["species"])
+        t = np.array([0.0])
+        return fo.check_literal(t, np.array([]), np.array([[x1, x2]]), True) == 1
+    assert holds("X1 < sqrt(X2)", 3, 10) and not holds("X1 < sqrt(X2)", 4, 16) and holds("X1 <= sqrt(X2)", 4, 16)
+    assert holds("X2 / X1 > 1e300", 0, 5) and not holds("X2 / X1 > 1e300", 1, 5)
+    assert not holds("X1 / X2 >= 0", 0, 0) and not holds("X1 / X2 < 0", 0, 0) and holds("X1 / X2 != 0", 0, 0)
+    assert holds("pow(X1, 0) == 1", 7, 0) and holds("min(X1, X2) == 2", 2, 9) and holds("max(X1, X2) == 9", 2, 9)
+    assert holds("X2 / 3 == 3", 0, 9) and not holds("X2 / 3 == 3", 0, 10)
+    del m
