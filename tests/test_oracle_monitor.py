@@ -148,6 +148,6 @@ def test_unsupported_outside_fragment():
 
 
 def test_parse_errors():
-    for bad in ["F[0,1](Z > 1)", "F[0,1](A >)", "(A > 1", "F[2,1](A > 1)", "A > 1.5"]:
+    for bad in ["F[0,1](Z > 1)", "F[0,1](A >)", "(A > 1", "F[2,1](A > 1)", "sqr(A) > 1", "pow(A, 1.5) > 1"]:
         with pytest.raises(ValueError):
             O.OracleFormula(bad, NAMES)
