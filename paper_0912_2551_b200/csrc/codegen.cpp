@@ -31,8 +31,31 @@ struct MonGen {
     const Property& P;
     explicit MonGen(const Property& p) : P(p) {}
 
+    // general val tree: int64 (Int, species, + - *) or binary64 in tree order
+    static std::string val(const Atom& at, int i) {
+        const VNode& n = at.v[(size_t)i];
+        const bool R = at.real;
+        switch (n.k) {
+            case VNode::INT: return R ? dlit((double)n.i) : ilit(n.i);
+            case VNode::REAL: return dlit(n.d);
+            case VNode::SPECIES: return (R ? "(double)x[" : "(smc_i64)x[") + std::to_string(n.s) + "]";
+            case VNode::NEG: return "(-" + val(at, n.a) + ")";
+            case VNode::ADD: return R ? "__dadd_rn(" + val(at, n.a) + ", " + val(at, n.b) + ")" : "(" + val(at, n.a) + " + " + val(at, n.b) + ")";
+            case VNode::SUB: return R ? "__dadd_rn(" + val(at, n.a) + ", -" + val(at, n.b) + ")" : "(" + val(at, n.a) + " - " + val(at, n.b) + ")";
+            case VNode::MUL: return R ? "__dmul_rn(" + val(at, n.a) + ", " + val(at, n.b) + ")" : "(" + val(at, n.a) + " * " + val(at, n.b) + ")";
+            case VNode::DIV: return "__ddiv_rn(" + val(at, n.a) + ", " + val(at, n.b) + ")";
+            case VNode::SQRT: return "__dsqrt_rn(" + val(at, n.a) + ")";
+            case VNode::ABS: return "fabs(" + val(at, n.a) + ")";
+            case VNode::MIN: return "smc_vmin(" + val(at, n.a) + ", " + val(at, n.b) + ")";
+            case VNode::MAX: return "smc_vmax(" + val(at, n.a) + ", " + val(at, n.b) + ")";
+            case VNode::POW: return "smc_vpow(" + val(at, n.a) + ", " + std::to_string(n.i) + ")";
+        }
+        return "0";
+    }
     std::string atom(int i) const {
         const Atom& a = P.atoms[(size_t)i];
+        static const char* cops[] = {" < ", " <= ", " >= ", " > ", " == ", " != "};
+        if (a.general) return "(" + val(a, a.lhs) + cops[(int)a.op] + val(a, a.rhs) + ")";
         std::string s = "(";
         for (auto& kv : a.coef) s += "(smc_i64)x[" + std::to_string(kv.first) + "] * " + ilit(kv.second) + " + ";
         s += ilit(a.cst) + ")";

@@ -123,6 +123,16 @@ __device__ __forceinline__ void smc_draw(smc_u64 seed, smc_u64 traj, smc_u64 ste
 #define SMC_A_MAX 0x1p+1000
 __device__ __forceinline__ double smc_tau(double e, double a0) { return smc_fdiv(e, a0); }
 
+// functions of general val atoms, identical on both sides of the parity
+// contract: min/max by comparison, pow(v, k) a left-to-right product (k = 0: 1)
+__device__ __forceinline__ double smc_vmin(double a, double b) { return a < b ? a : b; }
+__device__ __forceinline__ double smc_vmax(double a, double b) { return a > b ? a : b; }
+__device__ __forceinline__ double smc_vpow(double b, int k) {
+    double r = 1.0;
+    for (int i = 0; i < k; ++i) r = (i == 0) ? b : __dmul_rn(r, b);
+    return r;
+}
+
 // Kleene three-valued logic (reading R4): 0 false, 1 true, 2 unknown/pending.
 __device__ __forceinline__ int smc_knot(int a) { return a == 2 ? 2 : 1 - a; }
 __device__ __forceinline__ int smc_kand(int a, int b) { return (a == 0 || b == 0) ? 0 : ((a == 1 && b == 1) ? 1 : 2); }

@@ -54,7 +54,7 @@ std::vector<Tok> tokenize(const std::string& src) {
         for (const char* op : two)
             if (src.compare(i, 2, op) == 0) { out.push_back({Tok::OP, op, st}); i += 2; matched = true; break; }
         if (matched) continue;
-        if (std::string("()[],!&|<>=+-*").find(c) != std::string::npos) {
+        if (std::string("()[],!&|<>=+-*/").find(c) != std::string::npos) {
             out.push_back({Tok::OP, std::string(1, c), st});
             ++i;
             continue;
@@ -137,55 +137,101 @@ struct Parser {
         if (!(I.lo >= 0.0) || std::isinf(I.lo) || !(I.hi >= I.lo)) err("interval needs 0 <= a <= b");
         return I;
     }
-    // ---- integer-linear arithmetic
-    Lin lin_expr() {
-        Lin l = lin_term();
-        for (;;) {
-            if (accept("+")) { Lin r = lin_term(); add(l, r, +1); }
-            else if (accept("-")) { Lin r = lin_term(); add(l, r, -1); }
-            else return l;
-        }
-    }
+    // ---- integer-linear forms
     static void add(Lin& l, const Lin& r, int64_t s) {
         for (auto& kv : r.coef) l.coef[kv.first] += s * kv.second;
         l.cst += s * r.cst;
-    }
-    Lin lin_term() {
-        Lin l = lin_factor();
-        while (accept("*")) {
-            size_t at = p;
-            Lin r = lin_factor();
-            if (l.is_const()) { scale(r, l.cst); l = r; }
-            else if (r.is_const()) scale(l, r.cst);
-            else { p = at; fail(SMC_E_UNSUPPORTED, "col " + std::to_string(tk[at].pos) + ": non-linear atom (product of species counts)"); }
-        }
-        return l;
     }
     static void scale(Lin& l, int64_t s) {
         for (auto& kv : l.coef) kv.second *= s;
         l.cst *= s;
     }
-    Lin lin_factor() {
-        if (accept("-")) { Lin l = lin_factor(); scale(l, -1); return l; }
-        if (accept("(")) { Lin l = lin_expr(); expect(")"); return l; }
-        if (cur().t == Tok::INT) {
-            Lin l;
-            l.cst = std::stoll(cur().s);
-            ++p;
-            return l;
+    // ---- general val: expr := term (('+'|'-') term)*, term := factor (('*'|'/') factor)*,
+    // factor := '-' factor | '(' expr ')' | Int | Real | species | func '(' args ')'
+    std::vector<VNode>* vn = nullptr;
+    int vadd(VNode n) { vn->push_back(n); return (int)vn->size() - 1; }
+    int val_expr() {
+        int l = val_term();
+        for (;;) {
+            VNode n;
+            if (accept("+")) n.k = VNode::ADD;
+            else if (accept("-")) n.k = VNode::SUB;
+            else return l;
+            n.a = l;
+            n.b = val_term();
+            l = vadd(n);
         }
-        if (cur().t == Tok::NUM) fail(SMC_E_UNSUPPORTED, "col " + std::to_string(cur().pos) + ": real constant in an atom (atoms are integer-linear)");
+    }
+    int val_term() {
+        int l = val_factor();
+        for (;;) {
+            VNode n;
+            if (accept("*")) n.k = VNode::MUL;
+            else if (accept("/")) n.k = VNode::DIV;
+            else return l;
+            n.a = l;
+            n.b = val_factor();
+            l = vadd(n);
+        }
+    }
+    int val_factor() {
+        if (accept("-")) { VNode n; n.k = VNode::NEG; n.a = val_factor(); return vadd(n); }
+        if (accept("(")) { int e = val_expr(); expect(")"); return e; }
+        if (cur().t == Tok::INT) { VNode n; n.k = VNode::INT; n.i = std::stoll(cur().s); ++p; return vadd(n); }
+        if (cur().t == Tok::NUM) { VNode n; n.k = VNode::REAL; n.d = std::strtod(cur().s.c_str(), nullptr); ++p; return vadd(n); }
         if (cur().t == Tok::ID) {
-            for (size_t i = 0; i < names.size(); ++i)
-                if (names[i] == cur().s) {
-                    Lin l;
-                    l.coef[(int)i] = 1;
+            const std::string id = cur().s;
+            if (p + 1 < tk.size() && tk[p + 1].t == Tok::OP && tk[p + 1].s == "(") {
+                VNode n;
+                if (id == "sqrt") n.k = VNode::SQRT;
+                else if (id == "abs") n.k = VNode::ABS;
+                else if (id == "min") n.k = VNode::MIN;
+                else if (id == "max") n.k = VNode::MAX;
+                else if (id == "pow") n.k = VNode::POW;
+                else err("unknown function '" + id + "'");
+                p += 2;
+                n.a = val_expr();
+                if (n.k == VNode::MIN || n.k == VNode::MAX) { expect(","); n.b = val_expr(); }
+                if (n.k == VNode::POW) {
+                    expect(",");
+                    if (cur().t != Tok::INT) err("integer exponent expected");
+                    n.i = std::stoll(cur().s);
                     ++p;
-                    return l;
                 }
-            err("unknown species '" + cur().s + "'");
+                expect(")");
+                return vadd(n);
+            }
+            for (size_t i = 0; i < names.size(); ++i)
+                if (names[i] == id) { VNode n; n.k = VNode::SPECIES; n.s = (int)i; ++p; return vadd(n); }
+            err("unknown species '" + id + "'");
         }
         err("expression expected");
+    }
+    static bool needs_real(const std::vector<VNode>& v, int i) {
+        const VNode& n = v[(size_t)i];
+        if (n.k == VNode::REAL || n.k == VNode::DIV || n.k >= VNode::SQRT) return true;
+        return (n.a >= 0 && needs_real(v, n.a)) || (n.b >= 0 && needs_real(v, n.b));
+    }
+    // integer tree -> linear form, false when a product of two species terms occurs
+    static bool to_lin(const std::vector<VNode>& v, int i, Lin& out) {
+        const VNode& n = v[(size_t)i];
+        Lin l, r;
+        switch (n.k) {
+            case VNode::INT: out = Lin(); out.cst = n.i; return true;
+            case VNode::SPECIES: out = Lin(); out.coef[n.s] = 1; return true;
+            case VNode::NEG: if (!to_lin(v, n.a, out)) return false; scale(out, -1); return true;
+            case VNode::ADD: case VNode::SUB:
+                if (!to_lin(v, n.a, l) || !to_lin(v, n.b, r)) return false;
+                add(l, r, n.k == VNode::ADD ? 1 : -1);
+                out = l;
+                return true;
+            case VNode::MUL:
+                if (!to_lin(v, n.a, l) || !to_lin(v, n.b, r)) return false;
+                if (l.is_const()) { scale(r, l.cst); out = r; return true; }
+                if (r.is_const()) { scale(l, r.cst); out = l; return true; }
+                return false;
+            default: return false;
+        }
     }
     bool cmp(Cmp* c) {
         if (accept("<=")) { *c = Cmp::LE; return true; }
@@ -238,16 +284,27 @@ struct Parser {
         size_t save = p;
         Error atom_err{0, ""};
         try {
-            Lin l = lin_expr();
+            std::vector<VNode> v;
+            vn = &v;
+            const int lv = val_expr();
             Cmp c;
             if (cmp(&c)) {
-                Lin r = lin_expr();
-                add(l, r, -1);
+                const int rv = val_expr();
                 Atom at;
-                for (auto& kv : l.coef)
-                    if (kv.second != 0) at.coef.push_back(kv);
-                at.cst = l.cst;
                 at.op = c;
+                Lin l, r;
+                if (!needs_real(v, lv) && !needs_real(v, rv) && to_lin(v, lv, l) && to_lin(v, rv, r)) {
+                    add(l, r, -1);                       // integer-linear: exact int64 form
+                    for (auto& kv : l.coef)
+                        if (kv.second != 0) at.coef.push_back(kv);
+                    at.cst = l.cst;
+                } else {                                 // general val
+                    at.general = true;
+                    at.real = needs_real(v, lv) || needs_real(v, rv);
+                    at.v = v;
+                    at.lhs = lv;
+                    at.rhs = rv;
+                }
                 atoms.push_back(at);
                 Node n{NK::ATOM};
                 n.atom = (int)atoms.size() - 1;

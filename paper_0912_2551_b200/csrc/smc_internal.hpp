@@ -71,10 +71,25 @@ struct Model {
 
 // -------------------------------------------------------------- property ---
 enum class Cmp { LT, LE, GE, GT, EQ, NE };
-struct Atom {                       // sum_s coef[s] x_s + cst  (cmp)  0, exact int64
+// general val of P:209 (val ~ val, func, Int, Real)
+struct VNode {
+    enum K { INT, REAL, SPECIES, ADD, SUB, MUL, DIV, NEG, SQRT, ABS, MIN, MAX, POW } k = INT;
+    int64_t i = 0;      // INT value, POW exponent
+    double d = 0.0;     // REAL value
+    int s = -1;         // SPECIES
+    int a = -1, b = -1;
+};
+struct Atom {
+    // integer-linear atoms: sum_s coef[s] x_s + cst  (cmp)  0, exact int64
     std::vector<std::pair<int, int64_t>> coef;
     int64_t cst = 0;
     Cmp op = Cmp::GT;
+    // general atoms: lhs (cmp) rhs over the trees in v; int64 when only Int constants,
+    // species, + - * occur (non-linear products), binary64 otherwise ('/', Real, func)
+    bool general = false;
+    bool real = false;
+    std::vector<VNode> v;
+    int lhs = -1, rhs = -1;
 };
 struct Interval {
     double lo = 0.0, hi = 0.0;      // hi = +inf when unbounded

@@ -388,3 +388,16 @@ def test_cell_cycle_rows_vs_oracle(smc, row):
     cfg = workloads.cell_cycle(workloads.CELL_CYCLE_FORMULAS[row])
     a, ae, *_ = _compare(smc, cfg, cfg["seed"], 0, 2000)
     assert ae >= AGREE, (row, a, ae)
+
+
+@pytest.mark.parametrize("variant", [1, 2])
+def test_general_val_atoms_vs_oracle(smc, variant):
+    """NEXT-2: general val atoms -- non-linear int64 products, '/', Real constants,
+    sqrt / abs / min / max / pow -- in the GPU monitors, replica by replica against the
+    oracle (the decision event is part of the comparison)."""
+    cfg = workloads.c2()
+    for f in ["F[0,50](sqrt(P) > 22.5)", "(E < sqrt(S) + 70) U[0,50] (P / 2 >= 250.5)",
+              "F[0,50](P * S > 140000)", "F[0,50](abs(ES - 30.5) < 1 & max(E, 60) == E)",
+              "G[0,30](pow(ES, 2) / 7 <= min(E, 90.5) * 30)"]:
+        a, ae, *_ = _compare(smc, dict(cfg, formula=f), 2, 0, 1500, variant)
+        assert ae >= AGREE, (f, variant, a, ae)

@@ -91,8 +91,11 @@ def test_property_compiler_errors():
         smc.Property(m, "F[0,50](P > )")
     assert e.value.name == "SMC_E_PARSE"
     with pytest.raises(smc.SmcError) as e:
-        smc.Property(m, "F[0,50](P * S > 5)")
-    assert e.value.name == "SMC_E_UNSUPPORTED"
+        smc.Property(m, "F[0,50](sqr(P) > 5)")          # unknown function
+    assert e.value.name == "SMC_E_PARSE"
+    with pytest.raises(smc.SmcError) as e:
+        smc.Property(m, "F[0,50](pow(P, 1.5) > 5)")     # pow takes an integer exponent
+    assert e.value.name == "SMC_E_PARSE"
     with pytest.raises(smc.SmcError) as e:
         smc.Property(m, "F[0,5](G[1,2](P > 5))")
     assert e.value.name == "SMC_E_UNSUPPORTED"
@@ -100,7 +103,8 @@ def test_property_compiler_errors():
         smc.Property(m, "F(P > 5)")                 # unbounded needs t_max
     assert e.value.name == "SMC_E_UNSUPPORTED"
     for ok in ["F(P > 5)", "(E <= 4) U (P >= 5)", "G[0,1](2*ES - P + 3 != 0) & !X[0,1](S == 1000)",
-               "F[0,10] G[0,1](E > S)", "(G[0,100](E < 400)) U[0,200] (P > 300)", "F(0,1.5](P >= 2) | true"]:
+               "F[0,10] G[0,1](E > S)", "(G[0,100](E < 400)) U[0,200] (P > 300)", "F(0,1.5](P >= 2) | true",
+               "F[0,50](P * S > 5)", "(E < sqrt(S)) U[0,5] (S >= 10 + ES)", "G[0,1](min(E, S) / 2.5 >= pow(P, 2))"]:
         smc.Property(m, ok, t_max=100.0)
 
 
