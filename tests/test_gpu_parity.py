@@ -401,3 +401,35 @@ def test_general_val_atoms_vs_oracle(smc, variant):
               "G[0,30](pow(ES, 2) / 7 <= min(E, 90.5) * 30)"]:
         a, ae, *_ = _compare(smc, dict(cfg, formula=f), 2, 0, 1500, variant)
         assert ae >= AGREE, (f, variant, a, ae)
+
+
+def test_c2_million_replicas_vs_oracle(smc):
+    """North star at 10^6 samples (C2, configs[1] model, the fixed-N parity run of SURVEY
+    §8(d)): per-replica agreement >= 99.99 %, |p_hat_gpu - p_hat_oracle| <= 5e-4, and both
+    99 % Wilson intervals contain the exact P = 0.2146528874 (uniformisation)."""
+    cfg = workloads.c2()
+    n = 10 ** 6
+    m, p = _pair(smc, cfg)
+    v, e = m.run_verdicts(p, 0, n, cfg["seed"])
+    v, e = v.cpu().numpy(), e.cpu().numpy().astype(np.int64)
+    oc, ov, oe = O.run_parallel(cfg, cfg["formula"], cfg["seed"], 0, n)
+    assert float(((v == ov) & (e == oe)).mean()) >= AGREE
+    pg, po = float(v.mean()), oc["n_true"] / n
+    assert abs(pg - po) <= 5e-4
+    z = normal_quantile(0.99)
+    for ph in (pg, po):
+        lo, hi = wilson_interval(ph, n, z)
+        assert lo <= 0.2146528874 <= hi
+
+
+def test_c3_million_replicas_vs_oracle(smc):
+    """C3 (configs[2]: 10^6 replicas) in full against the oracle on the same streams:
+    per-replica agreement >= 99.99 % and |p_hat_gpu - p_hat_oracle| <= 5e-4 (north star)."""
+    cfg = workloads.c3()
+    n = cfg["sampling"]["n"]
+    m, p = _pair(smc, cfg)
+    v, e = m.run_verdicts(p, 0, n, cfg["seed"])
+    v, e = v.cpu().numpy(), e.cpu().numpy().astype(np.int64)
+    oc, ov, oe = O.run_parallel(cfg, cfg["formula"], cfg["seed"], 0, n)
+    assert float(((v == ov) & (e == oe)).mean()) >= AGREE
+    assert abs(float(v.mean()) - oc["n_true"] / n) <= 5e-4
