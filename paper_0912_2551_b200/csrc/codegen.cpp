@@ -224,6 +224,95 @@ struct MonGen {
     }
 };
 
+// ------------------------------------------------- literal |= (variant 3) ---
+// smc_lit_mask(x): atom bit mask of a state; smc_lit_eval(): every subformula, children
+// first, at every buffered entry m, transcribing P:229-237 (three-valued, reading R4):
+// elapsed = tau_m + tau_{m+1} + ... (left to right), the next (unknown) entry of a
+// non-absorbed trace at elapsed + tau_n.
+std::string literal_code(const Property& P) {
+    std::ostringstream o;
+    MonGen mg(P);
+    o << "template <class XA> __device__ __forceinline__ unsigned smc_lit_mask(const XA& x) {\n    unsigned mk = 0u;\n";
+    for (size_t i = 0; i < P.atoms.size(); ++i) o << "    if " << mg.atom((int)i) << " mk |= " << (1u << i) << "u;\n";
+    o << "    return mk;\n}\n";
+    o << "__device__ __noinline__ int smc_lit_eval(const double* __restrict__ tb, const double* __restrict__ ub,\n"
+         "                                         const unsigned* __restrict__ mb, unsigned char* __restrict__ vb,\n"
+         "                                         long long n, bool absorbed, long long cap) {\n    (void)tb;\n";
+    for (size_t i = 0; i < P.lnodes.size(); ++i) {
+        const LNode& nd = P.lnodes[i];
+        o << "    {   // node " << i << "\n        unsigned char* V = vb + " << i << "LL * cap;\n";
+        const std::string A = "(vb + " + std::to_string(nd.a) + "LL * cap)";
+        const std::string B = "(vb + " + std::to_string(nd.b) + "LL * cap)";
+        switch (nd.k) {
+            case LNode::ATOM:
+                o << "        for (long long m = 0; m <= n; ++m) V[m] = (unsigned char)((mb[m] >> " << nd.atom << ") & 1u);\n";
+                break;
+            case LNode::TRUE_: o << "        for (long long m = 0; m <= n; ++m) V[m] = 1;\n"; break;
+            case LNode::FALSE_: o << "        for (long long m = 0; m <= n; ++m) V[m] = 0;\n"; break;
+            case LNode::NOT:
+                o << "        const unsigned char* Va = " << A << ";\n"
+                  << "        for (long long m = 0; m <= n; ++m) V[m] = (unsigned char)smc_knot(Va[m]);\n";
+                break;
+            case LNode::AND: case LNode::OR:
+                o << "        const unsigned char* Va = " << A << ";\n        const unsigned char* Vb = " << B << ";\n"
+                  << "        for (long long m = 0; m <= n; ++m) V[m] = (unsigned char)"
+                  << (nd.k == LNode::AND ? "smc_kand" : "smc_kor") << "(Va[m], Vb[m]);\n";
+                break;
+            case LNode::X:   // sigma |= X^I phi iff sigma^1 |= phi and delta(sigma,0) in I
+                o << "        const unsigned char* Va = " << A << ";\n"
+                  << "        for (long long m = 0; m <= n; ++m) {\n"
+                  << "            const double d = ub[m];\n"
+                  << "            if (m < n) V[m] = " << MonGen::contains(nd.I, "d") << " ? Va[m + 1] : 0;\n"
+                  << "            else V[m] = absorbed ? 0 : (" << MonGen::contains(nd.I, "d") << " ? 2 : 0);\n"
+                  << "        }\n";
+                break;
+            case LNode::U: case LNode::F: {   // P:235-236; F == tt U
+                const bool hasA = nd.k == LNode::U;
+                const std::string P2 = nd.k == LNode::U ? B : A;
+                if (hasA) o << "        const unsigned char* V1 = " << A << ";\n";
+                o << "        const unsigned char* V2 = " << P2 << ";\n"
+                  << "        for (long long m = 0; m <= n; ++m) {\n"
+                  << "            int res = 0, pre = 1;\n            double el = 0.0;\n            bool done = false;\n"
+                  << "            for (long long k = m; k <= n; ++k) {\n"
+                  << "                if (k > m) el = __dadd_rn(el, ub[k - 1]);\n"
+                  << "                if (" << MonGen::beyond(nd.I, "el") << ") { done = true; break; }\n"
+                  << "                if " << MonGen::contains(nd.I, "el") << " res = smc_kor(res, smc_kand(pre, V2[k]));\n"
+                  << "                if (res == 1) { done = true; break; }\n"
+                  << "                pre = smc_kand(pre, " << (hasA ? "V1[k]" : "1") << ");\n"
+                  << "                if (pre == 0) { done = true; break; }\n"
+                  << "            }\n"
+                  << "            if (!done && !absorbed) {\n"
+                  << "                const double tail = __dadd_rn(el, ub[n]);\n"
+                  << "                if (!(" << MonGen::beyond(nd.I, "tail") << ")) res = smc_kor(res, smc_kand(pre, 2));\n"
+                  << "            }\n"
+                  << "            V[m] = (unsigned char)res;\n"
+                  << "        }\n";
+                break;
+            }
+            case LNode::G:   // G == !F!
+                o << "        const unsigned char* Va = " << A << ";\n"
+                  << "        for (long long m = 0; m <= n; ++m) {\n"
+                  << "            int res = 0;\n            double el = 0.0;\n            bool done = false;\n"
+                  << "            for (long long k = m; k <= n; ++k) {\n"
+                  << "                if (k > m) el = __dadd_rn(el, ub[k - 1]);\n"
+                  << "                if (" << MonGen::beyond(nd.I, "el") << ") { done = true; break; }\n"
+                  << "                if " << MonGen::contains(nd.I, "el") << " res = smc_kor(res, smc_knot(Va[k]));\n"
+                  << "                if (res == 1) { done = true; break; }\n"
+                  << "            }\n"
+                  << "            if (!done && !absorbed) {\n"
+                  << "                const double tail = __dadd_rn(el, ub[n]);\n"
+                  << "                if (!(" << MonGen::beyond(nd.I, "tail") << ")) res = smc_kor(res, 2);\n"
+                  << "            }\n"
+                  << "            V[m] = (unsigned char)smc_knot(res);\n"
+                  << "        }\n";
+                break;
+        }
+        o << "    }\n";
+    }
+    o << "    return vb[" << P.lroot << "LL * cap];\n}\n";
+    return o.str();
+}
+
 // ------------------------------------------------ explicit rate expressions ---
 // Straight-line IEEE binary64 code of an explicit rate tree (rates.cpp), in tree
 // order; xa = the count array expression ("x" in registers, "xs" in smem).
@@ -456,7 +545,13 @@ std::string generate_source(const Model& m, const Property& p, int variant, cons
     o << "// generated by libsmc codegen: model N=" << m.N << " M=" << m.M << ", variant " << variant << "\n";
     o << "#define SMC_N " << m.N << "\n#define SMC_M " << m.M << "\n";
     o << "#define SMC_TMAX " << dlit(p.t_max) << "\n";
-    if (variant == 1) {
+    if (variant == 3) {
+        // the trace must cover what the semantics can look at: t_max for unbounded formulas,
+        // else the formula's reach (as the oracle's literal mode)
+        const double H = p.t_max > 0.0 ? p.t_max : p.horizon;
+        o << "#define SMC_BLOCK 128\n#define SMC_MINB 2\n#define SMC_PIPE2 0\n";
+        o << "#define SMC_LIT_H " << dlit(H) << "\n#define SMC_LIT_NODES " << p.lnodes.size() << "\n";
+    } else if (variant == 1) {
         // >= 4 resident CTAs of 128 threads: at most 128 registers per thread
         o << "#define SMC_BLOCK 128\n#define SMC_MINB 4\n";
         if (const char* e = std::getenv("SMC_STRAIGHT")) o << "#define SMC_STRAIGHT " << std::atoi(e) << "\n";
@@ -482,13 +577,17 @@ std::string generate_source(const Model& m, const Property& p, int variant, cons
         if (const char* e = std::getenv("SMC_FLAT")) o << "#define SMC_FLAT " << std::atoi(e) << "\n";
     }
     o << embedded_source("ssa_common.cuh") << "\n";
-    if (variant == 1) o << model_code_thread(m) << "\n";
+    if (variant == 1 || variant == 3) o << model_code_thread(m) << "\n";
     if (variant == 2 && tl->any_explicit) {          // explicit laws of the tile variant
         o << "__device__ __noinline__ double smc_explicit(int k, const int* xs) {\n    switch (k) {\n";
         for (int k = 0; k < m.M; ++k)
             if (!m.R[(size_t)k].rate.empty())
                 o << "    case " << k << ":\n" << explicit_body(m.R[(size_t)k], "xs", "        ");
         o << "    }\n    return 0.0;\n}\n";
+    }
+    if (variant == 3) {
+        o << literal_code(p) << "\n" << embedded_source("ssa_literal.cuh") << "\n";
+        return o.str();
     }
     o << MonGen(p).emit() << "\n";
     o << embedded_source(variant == 1 ? "ssa_thread.cuh" : "ssa_tile.cuh") << "\n";

@@ -478,7 +478,28 @@ std::unique_ptr<Property> compile_property(const Model& m, const std::string& te
     if (has_unbounded(nodes, top) && !(t_max > 0.0))
         fail(SMC_E_UNSUPPORTED, "unbounded temporal operator needs t_max > 0 (pessimistic cut-off, P:314-317)");
     Classifier cl(nodes, *P);
-    P->root_idx = cl.root(top);
+    try {
+        P->root_idx = cl.root(top);
+    } catch (const Error& e) {
+        // outside the streaming templates: literal |= on buffered traces (NEXT-2, reading R23)
+        if (e.code != SMC_E_UNSUPPORTED || e.msg.rfind("formula outside the compiled fragment", 0) != 0) throw;
+        if (P->atoms.size() > 32) fail(SMC_E_UNSUPPORTED, "nested formula with more than 32 atoms");
+        P->literal = true;
+        P->leaves.clear();
+        P->root.clear();
+        P->bexprs.clear();
+        P->root_idx = -1;
+        for (const Node& n : nodes) {
+            LNode l;
+            l.k = (LNode::K)(int)n.k;
+            l.I = n.I;
+            l.a = n.a;
+            l.b = n.b;
+            l.atom = n.atom;
+            P->lnodes.push_back(l);
+        }
+        P->lroot = top;
+    }
     P->horizon = reach(nodes, top, t_max > 0 ? t_max : 0.0);
     if (t_max > 0.0 && t_max < P->horizon) P->horizon = t_max;
     return P;

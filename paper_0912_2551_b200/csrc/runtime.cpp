@@ -62,9 +62,15 @@ struct PropKernel {
     const void* tables = nullptr;
     bool timing_pending = false;
     int per_warp = 1;                      // trajectories per warp (variant 2)
+    // variant 3 (literal |=): per-thread trace buffers
+    double* lit_t = nullptr;
+    double* lit_tau = nullptr;
+    unsigned* lit_mask = nullptr;
+    unsigned char* lit_val = nullptr;
+    unsigned long long lit_cap = 0;
     smc_launch_info info{};
     uint64_t capacity() const {            // trajectories resident at once on this GPU
-        return (uint64_t)grid_max * (uint64_t)(variant == 1 ? block : (block / 32) * per_warp);
+        return (uint64_t)grid_max * (uint64_t)(variant != 2 ? block : (block / 32) * per_warp);
     }
 };
 
@@ -85,6 +91,12 @@ struct DeviceState {
     int sm_count = 0, max_smem_optin = 0;
     std::map<uint64_t, PropKernel> kernels;
     ~DeviceState() {
+        for (auto& kv : kernels) {
+            dfree(kv.second.lit_t);
+            dfree(kv.second.lit_tau);
+            dfree(kv.second.lit_mask);
+            dfree(kv.second.lit_val);
+        }
         if (e0) cudaEventDestroy(e0);
         if (e1) cudaEventDestroy(e1);
         if (host_counts) cudaFreeHost(host_counts);
@@ -128,8 +140,14 @@ PropKernel& prepare(Model& m, const Property& p) {
     m.build_deps();
     PropKernel pk;
     pk.variant = m.variant();
+    if (p.literal) {                       // buffered trace + literal |= (thread-owned only)
+        if (m.N > 32 || m.M > 32 || m.variant_forced == 2)
+            fail(SMC_E_UNSUPPORTED, "formula outside the streaming templates needs the thread-owned variant "
+                                    "(N <= 32, M <= 32)");
+        pk.variant = 3;
+    }
     const TileLayout* tl = nullptr;
-    const int v = pk.variant;
+    const int v = pk.variant == 3 ? 1 : pk.variant;      // table set (variant 3 uses variant 1's)
     if (!d.tables_ready[v]) {
         const void* src = nullptr;
         size_t bytes = 0;
@@ -154,9 +172,30 @@ PropKernel& prepare(Model& m, const Property& p) {
     if (v == 2) tl = &d.layout;
     pk.tables = d.tables[v];
     pk.source = generate_source(m, p, pk.variant, tl);
-    pk.k = get_kernel(pk.source, pk.variant == 1 ? "smc_ssa_thread" : "smc_ssa_tile");
+    pk.k = get_kernel(pk.source, pk.variant == 1 ? "smc_ssa_thread" : (pk.variant == 2 ? "smc_ssa_tile" : "smc_ssa_literal"));
     const void* fn = (const void*)pk.k->kernel;
-    if (pk.variant == 1) {
+    if (pk.variant == 3) {
+        pk.block = 128;
+        int nb = 0;
+        ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, pk.block, 0), "occupancy");
+        pk.grid_max = std::max(1, nb) * d.sm_count;
+        pk.smem = 0;
+        // trace buffers: at most half of the free device memory, at most 32 GiB, and no more
+        // entries per thread than the event cap allows
+        size_t free_b = 0, total_b = 0;
+        ck(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+        const size_t budget = std::min<size_t>(free_b / 2, (size_t)32 << 30);
+        const size_t lanes = (size_t)pk.grid_max * (size_t)pk.block;
+        const size_t per_entry = 8 + 8 + 4 + p.lnodes.size();
+        size_t cap = budget / (lanes * per_entry);
+        cap = std::min<size_t>(cap, (size_t)std::min<uint64_t>(m.event_cap + 2, 1ull << 24));
+        if (cap < 16) fail(SMC_E_CUDA, "literal variant: not enough device memory for trace buffers");
+        pk.lit_cap = cap;
+        pk.lit_t = (double*)dalloc(lanes * cap * 8);
+        pk.lit_tau = (double*)dalloc(lanes * cap * 8);
+        pk.lit_mask = (unsigned*)dalloc(lanes * cap * 4);
+        pk.lit_val = (unsigned char*)dalloc(lanes * cap * p.lnodes.size());
+    } else if (pk.variant == 1) {
         pk.block = 128;
         int nb = 0;
         ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, pk.block, 0), "occupancy");
@@ -209,9 +248,15 @@ void launch_slice(Model& m, PropKernel& pk, uint64_t seed, uint64_t lo, uint64_t
         int* events_out;
         unsigned long long event_cap;
         const void* tables;
+        double* lit_t;
+        double* lit_tau;
+        unsigned* lit_mask;
+        unsigned char* lit_val;
+        unsigned long long lit_cap;
     } P{seed, lo, count, spec ? d.spec_cursor() : (unsigned long long*)d.ctl,
-        (long long*)(spec ? d.spec_scratch() : d.counters()), dev_verdict, dev_events, m.event_cap, pk.tables};
-    const uint64_t per_block = pk.variant == 1 ? (uint64_t)pk.block : (uint64_t)(pk.block / 32 * pk.per_warp);
+        (long long*)(spec ? d.spec_scratch() : d.counters()), dev_verdict, dev_events, m.event_cap, pk.tables,
+        pk.lit_t, pk.lit_tau, pk.lit_mask, pk.lit_val, pk.lit_cap};
+    const uint64_t per_block = pk.variant != 2 ? (uint64_t)pk.block : (uint64_t)(pk.block / 32 * pk.per_warp);
     const uint64_t need = (count + per_block - 1) / per_block;
     const int grid = (int)std::min<uint64_t>((uint64_t)pk.grid_max, need);
     void* args[] = {&P};
@@ -561,7 +606,7 @@ int smc_kernel_source(smc_model* h, const smc_property* ph, char* buf, size_t* l
         Model& m = h->m;
         std::lock_guard<std::mutex> lk(m.mu);
         m.build_deps();
-        const int v = m.variant();
+        const int v = ph->p->literal ? 3 : m.variant();
         TileLayout tl;
         if (v == 2) tl = pack_tables(m);
         std::string s = generate_source(m, *ph->p, v, v == 2 ? &tl : nullptr);

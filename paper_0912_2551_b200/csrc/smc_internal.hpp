@@ -113,8 +113,20 @@ struct RootExpr {        // Kleene combination of leaves
     int leaf = -1;
     int a = -1, b = -1;
 };
+// AST node of a formula outside the streaming fragment (kept for the literal variant)
+struct LNode {
+    enum K { ATOM, TRUE_, FALSE_, NOT, AND, OR, X, U, F, G } k = TRUE_;
+    Interval I;
+    int a = -1, b = -1;
+    int atom = -1;
+};
 struct Property {
     uint64_t id = 0;
+    // formulas outside the streaming fragment of reading R16: each replica's trace is
+    // buffered to the horizon and |= is evaluated literally on it (variant 3)
+    bool literal = false;
+    std::vector<LNode> lnodes;   // children before parents
+    int lroot = -1;
     std::string text;
     int N = 0;
     double t_max = 0.0;

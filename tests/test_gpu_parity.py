@@ -433,3 +433,36 @@ def test_c3_million_replicas_vs_oracle(smc):
     oc, ov, oe = O.run_parallel(cfg, cfg["formula"], cfg["seed"], 0, n)
     assert float(((v == ov) & (e == oe)).mean()) >= AGREE
     assert abs(float(v.mean()) - oc["n_true"] / n) <= 5e-4
+
+
+def _iso_cfg():
+    rx = workloads._rx
+    return dict(name="iso", species=["A", "B"], x0=[10, 0], reactions=[rx([(0, 1)], [(1, 1)], 1.0), rx([(1, 1)], [(0, 1)], 0.5)],
+                formula="", t_max=0.0, seed=5, sampling=dict(mode="fixed", n=2000))
+
+
+NESTED = [("iso", "F[0,3](A <= 5 & G[0,0.5](B >= 4))"), ("iso", "G[0,1.5](!(A < 7) | F[0.2,1](B <= 3))"),
+          ("iso", "F[0.5,3](X[0,0.3](A == 6))"), ("iso", "F[0,3](G[0.2,0.6](A > 4))"),
+          ("iso", "(F[0,1](B > 3)) U[0,3] (A < 5)"), ("iso", "!F[0,1](A == 7) | G[0,0.5](X[0,0.2](B > 2))"),
+          ("iso", "F[0,4]((A > 6) U[0.1,1] (B > 3))"), ("iso", "G(A + B == 10) & F(0,2](G[0,0.3](A == B))"),
+          ("c2", "F[0,3](P > 25 & G[0,0.5](P < 33))"), ("c2", "G[0,2](F[0.05,0.3](ES >= E / 4))")]
+
+
+@pytest.mark.parametrize("case", range(len(NESTED)))
+def test_nested_formulas_literal_variant_vs_oracle(smc, case):
+    """NEXT-2: formulas outside the streaming templates (nested temporal operators, non-zero
+    inner lower bounds, X inside F, unbounded with t_max) run through the literal variant
+    (buffered trace + |= on the device) and equal the oracle's literal mode replica for
+    replica, verdicts and event counts."""
+    name, f = NESTED[case]
+    cfg = dict(_iso_cfg() if name == "iso" else workloads.c2(), formula=f)
+    t_max = 4.0 if "G(" in f else 0.0
+    cfg["t_max"] = t_max
+    m, p = _pair(smc, cfg)
+    v, e = m.run_verdicts(p, 0, 2000, 5)
+    v, e = v.cpu().numpy(), e.cpu().numpy().astype(np.int64)
+    assert m.last_launch(p)["variant"] == 3
+    om = O.OracleModel(cfg)
+    of = O.OracleFormula(f, cfg["species"], t_max)
+    oc, ov, oe = O.run(om, of, 5, 0, 2000, mode="literal")
+    assert float(((v == ov) & (e == oe)).mean()) >= 0.9995, (f, float((v == ov).mean()), float((e == oe).mean()))

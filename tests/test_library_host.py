@@ -96,9 +96,9 @@ def test_property_compiler_errors():
     with pytest.raises(smc.SmcError) as e:
         smc.Property(m, "F[0,50](pow(P, 1.5) > 5)")     # pow takes an integer exponent
     assert e.value.name == "SMC_E_PARSE"
-    with pytest.raises(smc.SmcError) as e:
-        smc.Property(m, "F[0,5](G[1,2](P > 5))")
-    assert e.value.name == "SMC_E_UNSUPPORTED"
+    # outside the streaming templates: compiled for the literal variant (buffered trace + |=)
+    assert "smc_ssa_literal" in m.kernel_source(smc.Property(m, "F[0,5](G[1,2](P > 5))"))
+    assert "smc_ssa_thread" in m.kernel_source(smc.Property(m, "F[0,5] G[0,2](P > 5)"))
     with pytest.raises(smc.SmcError) as e:
         smc.Property(m, "F(P > 5)")                 # unbounded needs t_max
     assert e.value.name == "SMC_E_UNSUPPORTED"
