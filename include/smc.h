@@ -256,6 +256,8 @@ typedef struct {
     double table_bytes;       /* packed model + monitor tables read per CTA         */
     int32_t aux_launches;     /* other kernels of that call (per-round count kernels) */
     int32_t pad_;
+    double sim_events;        /* SSA events this GPU's launches simulated in that call,
+                                 incl. speculative replicas past the final N_tot */
 } smc_launch_info;
 /* Launch configuration and timing of the last run of (m, p). */
 int smc_last_launch(const smc_model* m, const smc_property* p, smc_launch_info* out);

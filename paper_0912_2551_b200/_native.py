@@ -24,7 +24,8 @@ class SmcEstimate(ctypes.Structure):
 class SmcLaunchInfo(ctypes.Structure):
     _fields_ = [("variant", c_i32), ("block_threads", c_i32), ("grid_blocks", c_i32), ("smem_bytes", c_i32),
                 ("regs_per_thread", c_i32), ("launches", c_i32), ("kernel_ms", ctypes.c_float),
-                ("compile_ms", ctypes.c_float), ("table_bytes", c_dbl), ("aux_launches", c_i32), ("pad_", c_i32)]
+                ("compile_ms", ctypes.c_float), ("table_bytes", c_dbl), ("aux_launches", c_i32), ("pad_", c_i32),
+                ("sim_events", c_dbl)]
 
 
 RUN_FN = ctypes.CFUNCTYPE(c_i32, c_u64, c_u64, c_vp, ctypes.POINTER(SmcCounts))

@@ -292,6 +292,18 @@ void read_counts(Model& m, PropKernel& pk, smc_counts* out) {
     out->errors = m.dev->host_counts[3];
 }
 
+// Events simulated by the previous speculative batch (its own counters, which no
+// round reads) -> launch info; called before the next batch reuses them and at the end.
+void harvest_spec_events(Model& m, PropKernel& pk) {
+    DeviceState& d = *m.dev;
+    if (!d.spec_valid) return;
+    int64_t ev = 0;
+    ck(cudaMemcpyAsync(&ev, d.spec_scratch() + 2, 8, cudaMemcpyDeviceToHost, stream()), "D2H spec events");
+    ck(cudaStreamSynchronize(stream()), "cudaStreamSynchronize");
+    pk.info.sim_events += (double)ev;
+    d.spec_valid = false;
+}
+
 // Prefix-exact speculative round.  The counts of the round
 // range [base, base+n) are summed from per-replica results; when the range is not
 // covered by the current batch, a new batch starting at the first uncovered index
@@ -338,6 +350,7 @@ void spec_round(Model& m, PropKernel& pk, uint64_t seed, uint64_t base, uint64_t
             d.spec_e = (int*)dalloc(4 * c);
             d.spec_cap = c;
         }
+        harvest_spec_events(m, pk);
         launch_slice(m, pk, seed, lo, hi, d.spec_v, d.spec_e, true);
         ck(cudaGetLastError(), "kernel launch");
         d.spec_begin = covered;
@@ -360,6 +373,7 @@ int run_round(Model& m, const Property& p, uint64_t seed, uint64_t base, uint64_
     launch_slice(m, pk, seed, lo, hi, nullptr, nullptr);
     ck(cudaGetLastError(), "kernel launch");
     read_counts(m, pk, out);
+    pk.info.sim_events += (double)out->events / (double)h.world;   // this GPU's share (equal slices)
     return SMC_OK;
 }
 
@@ -459,6 +473,7 @@ int smc_run(smc_model* h, const smc_property* ph, uint64_t n, uint64_t seed, smc
         PropKernel& pk = prepare(m, *ph->p);
         pk.info.launches = 0;
         pk.info.aux_launches = 0;
+        pk.info.sim_events = 0.0;
         pk.info.kernel_ms = 0.f;
         int rc = run_round(m, *ph->p, seed, m.cursor, n, out);
         if (rc == SMC_OK) m.cursor += n;
@@ -485,6 +500,7 @@ int smc_estimate_ex(smc_model* h, const smc_property* ph, double confidence, dou
         PropKernel& pk = prepare(m, *ph->p);
         pk.info.launches = 0;
         pk.info.aux_launches = 0;
+        pk.info.sim_events = 0.0;
         pk.info.kernel_ms = 0.f;
         m.dev->spec_valid = false;
         // no Fig. 2 round can reach past the conservative size Eq. 4(0.5) (N' <= Eq. 4(0.5))
@@ -499,7 +515,7 @@ int smc_estimate_ex(smc_model* h, const smc_property* ph, double confidence, dou
                 return run_round(m, *ph->p, seed, base, n, c);
             },
             confidence, half_width, start, out);
-        m.dev->spec_valid = false;
+        harvest_spec_events(m, pk);
         return rc;
     });
 }
@@ -547,6 +563,7 @@ int smc_run_verdicts(smc_model* h, const smc_property* ph, uint64_t first, uint6
         PropKernel& pk = prepare(m, *ph->p);
         pk.info.launches = 0;
         pk.info.aux_launches = 0;
+        pk.info.sim_events = 0.0;
         pk.info.kernel_ms = 0.f;
         launch_slice(m, pk, seed, first, first + n, dev_verdict, dev_events);
         ck(cudaGetLastError(), "kernel launch");
