@@ -74,6 +74,11 @@ __device__ __forceinline__ double smc_fdiv(double num, double den) {
 // ~80 of the general libdevice log (no special cases: x is never 0, negative,
 // subnormal, inf or NaN here).  Accuracy: checked against glibc on the GPU
 // (tests/test_gpu_parity.py::test_draws_vs_oracle).
+// coefficients in the constant bank: DFMA reads them as c[bank][offset] operands, no
+// per-event materialisation of 64-bit immediates in (uniform) registers
+__constant__ double smc_lg_c[9] = {6.666666666666735130e-01, 3.999999999940941908e-01, 2.857142874366239149e-01,
+                                   2.222219843214978396e-01, 1.818357216161805012e-01, 1.531383769920937332e-01,
+                                   1.479819860511658591e-01, 6.93147180369123816490e-01, 1.90821492927058770002e-10};
 __device__ __forceinline__ double smc_neglog(double x) {
     int hx = __double2hiint(x);
     const int lx = __double2loint(x);
@@ -86,16 +91,13 @@ __device__ __forceinline__ double smc_neglog(double x) {
     const double s = smc_fdiv(f, __dadd_rn(2.0, f));
     const double dk = (double)k;
     const double z = __dmul_rn(s, s), w = __dmul_rn(z, z);
-    const double t1 = __dmul_rn(w, __fma_rn(w, __fma_rn(w, 1.531383769920937332e-01, 2.222219843214978396e-01),
-                                            3.999999999940941908e-01));
-    const double t2 = __dmul_rn(z, __fma_rn(w, __fma_rn(w, __fma_rn(w, 1.479819860511658591e-01,
-                                                                       1.818357216161805012e-01),
-                                                             2.857142874366239149e-01),
-                                            6.666666666666735130e-01));
+    const double* C = smc_lg_c;
+    const double t1 = __dmul_rn(w, __fma_rn(w, __fma_rn(w, C[5], C[3]), C[1]));
+    const double t2 = __dmul_rn(z, __fma_rn(w, __fma_rn(w, __fma_rn(w, C[6], C[4]), C[2]), C[0]));
     const double R = __dadd_rn(t2, t1);
     const double hfsq = __dmul_rn(__dmul_rn(0.5, f), f);
-    const double inner = __fma_rn(s, __dadd_rn(hfsq, R), __dmul_rn(dk, 1.90821492927058770002e-10));
-    const double lg = __fma_rn(dk, 6.93147180369123816490e-01, -__dadd_rn(__dadd_rn(hfsq, -inner), -f));
+    const double inner = __fma_rn(s, __dadd_rn(hfsq, R), __dmul_rn(dk, C[8]));
+    const double lg = __fma_rn(dk, C[7], -__dadd_rn(__dadd_rn(hfsq, -inner), -f));
     return -lg;
 }
 
