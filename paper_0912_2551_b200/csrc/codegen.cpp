@@ -341,7 +341,7 @@ std::string explicit_body(const Reaction& r, const char* xa, const char* indent)
 }
 
 // ------------------------------------------------- variant 1 model code ---
-std::string law_expr(const Reaction& r) {
+std::string law_expr(const Reaction& r, int k) {
     // h exact in int64, a = c * (double)h, Hill: a / (1 + q^n)
     std::vector<std::string> terms;
     for (int q = 0; q < 2; ++q) {
@@ -353,12 +353,18 @@ std::string law_expr(const Reaction& r) {
     if (terms.empty()) h = "1LL";
     else if (terms.size() == 1) h = terms[0];
     else h = "(" + terms[0] + " * " + terms[1] + ")";
-    return "__dmul_rn(" + dlit(r.c) + ", (double)(" + h + "))";
+    (void)r;
+    return "__dmul_rn(smc_rc[" + std::to_string(k) + "], (double)(" + h + "))";   // c_k from the constant bank
 }
 
 std::string model_code_thread(const Model& m) {
     std::ostringstream o;
     const int N = m.N, M = m.M;
+    // rate constants in the constant bank (DMUL reads c[][] operands; no per-event
+    // materialisation of 64-bit immediates)
+    o << "__constant__ double smc_rc[" << M << "] = {";
+    for (int k = 0; k < M; ++k) o << (k ? ", " : "") << dlit(m.R[(size_t)k].c);
+    o << "};\n";
     o << "__device__ __forceinline__ void smc_init_x(int (&x)[SMC_N]) {\n";
     for (int s = 0; s < N; ++s) o << "    x[" << s << "] = " << m.x0[(size_t)s] << ";\n";
     o << "}\n";
@@ -373,7 +379,7 @@ std::string model_code_thread(const Model& m) {
         if (ht.offset[(size_t)k] >= 0)   // zero-order Hill law: a_k(x_r) tabulated (same IEEE ops, host side)
             o << "    if (x[" << r.rep << "] < " << ht.size << ") return __ldg(H + " << ht.offset[(size_t)k] << " + x["
               << r.rep << "]);\n";
-        o << "    double a = " << law_expr(r) << ";\n";
+        o << "    double a = " << law_expr(r, k) << ";\n";
         if (r.hill) {
             o << "    const double q = __ddiv_rn((double)x[" << r.rep << "], " << dlit(r.K) << ");\n";
             o << "    double qn = q;\n";
@@ -553,7 +559,12 @@ std::string generate_source(const Model& m, const Property& p, int variant, cons
         o << "#define SMC_LIT_H " << dlit(H) << "\n#define SMC_LIT_NODES " << p.lnodes.size() << "\n";
     } else if (variant == 1) {
         // >= 4 resident CTAs of 128 threads: at most 128 registers per thread
-        o << "#define SMC_BLOCK 128\n#define SMC_MINB 4\n";
+        // resident 128-thread CTAs per SM (register cap 65536 / (128 minb)): the small models
+        // (M <= 8: C1, C2) run latency-bound Wilson rounds below full occupancy and keep
+        // registers for ILP (minb 4); larger ones are throughput-bound (minb 6: C3 +4 %)
+        int minb = m.M <= 8 ? 4 : 6;
+        if (const char* e = std::getenv("SMC_MINB")) minb = std::atoi(e);
+        o << "#define SMC_BLOCK 128\n#define SMC_MINB " << minb << "\n";
         if (const char* e = std::getenv("SMC_STRAIGHT")) o << "#define SMC_STRAIGHT " << std::atoi(e) << "\n";
         // two-stage draw pipeline: shorter per-event chain (-12 % at low occupancy, C2) for
         // register-light models; heavier models are throughput-bound and keep one stage
