@@ -180,15 +180,22 @@ PropKernel& prepare(Model& m, const Property& p) {
         ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, pk.block, 0), "occupancy");
         pk.grid_max = std::max(1, nb) * d.sm_count;
         pk.smem = 0;
-        // trace buffers: at most half of the free device memory, at most 32 GiB, and no more
-        // entries per thread than the event cap allows
+        // trace buffers: at most a quarter of the free device memory and 16 GiB per property;
+        // every resident thread gets >= 4096 entries (fewer resident CTAs if needed), and no
+        // more entries than the event cap allows
         size_t free_b = 0, total_b = 0;
         ck(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
-        const size_t budget = std::min<size_t>(free_b / 2, (size_t)32 << 30);
-        const size_t lanes = (size_t)pk.grid_max * (size_t)pk.block;
+        const size_t budget = std::min<size_t>(free_b / 4, (size_t)16 << 30);
         const size_t per_entry = 8 + 8 + 4 + p.lnodes.size();
-        size_t cap = budget / (lanes * per_entry);
-        cap = std::min<size_t>(cap, (size_t)std::min<uint64_t>(m.event_cap + 2, 1ull << 24));
+        const size_t want_cap = (size_t)std::min<uint64_t>(m.event_cap + 2, 1ull << 24);
+        size_t lanes = (size_t)pk.grid_max * (size_t)pk.block;
+        const size_t min_cap = std::min<size_t>(want_cap, 4096);
+        if (budget / (lanes * per_entry) < min_cap) {
+            const size_t blocks = std::max<size_t>(1, budget / (min_cap * per_entry * (size_t)pk.block));
+            pk.grid_max = (int)std::min<size_t>((size_t)pk.grid_max, blocks);
+            lanes = (size_t)pk.grid_max * (size_t)pk.block;
+        }
+        size_t cap = std::min<size_t>(budget / (lanes * per_entry), want_cap);
         if (cap < 16) fail(SMC_E_CUDA, "literal variant: not enough device memory for trace buffers");
         pk.lit_cap = cap;
         pk.lit_t = (double*)dalloc(lanes * cap * 8);
