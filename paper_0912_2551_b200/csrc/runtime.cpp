@@ -87,6 +87,7 @@ struct DeviceState {
     int* spec_e = nullptr;
     uint64_t spec_cap = 0, spec_begin = 0, spec_end = 0, spec_lo = 0, spec_hi = 0;
     bool spec_valid = false;
+    bool spec_events_host = false;  // host_counts[10] holds the live batch's simulated events
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     int sm_count = 0, max_smem_optin = 0;
     std::map<uint64_t, PropKernel> kernels;
@@ -125,7 +126,7 @@ DeviceState& device(Model& m) {
         ck(cudaDeviceGetAttribute(&d->sm_count, cudaDevAttrMultiProcessorCount, dev), "attr");
         ck(cudaDeviceGetAttribute(&d->max_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev), "attr");
         d->ctl = dalloc(128);
-        ck(cudaMallocHost((void**)&d->host_counts, 64), "cudaMallocHost");
+        ck(cudaMallocHost((void**)&d->host_counts, 128), "cudaMallocHost");
         ck(cudaEventCreate(&d->e0), "cudaEventCreate");
         ck(cudaEventCreate(&d->e1), "cudaEventCreate");
         m.dev.reset(d.release());
@@ -290,9 +291,11 @@ void read_counts(Model& m, PropKernel& pk, smc_counts* out) {
     if (h.allreduce) {
         if (h.allreduce(m.dev->counters(), 4, h.allreduce_user) != 0) fail(SMC_E_COMM, "allreduce hook failed");
     }
-    ck(cudaMemcpyAsync(m.dev->host_counts, m.dev->counters(), 32, cudaMemcpyDeviceToHost, stream()), "D2H counts");
+    // counters [16, 48) and, in the same copy, the speculative batch's own counters [80, 112)
+    ck(cudaMemcpyAsync(m.dev->host_counts, m.dev->counters(), 96, cudaMemcpyDeviceToHost, stream()), "D2H counts");
     ck(cudaStreamSynchronize(stream()), "cudaStreamSynchronize");
     finish_timing(m, pk);
+    m.dev->spec_events_host = m.dev->spec_valid;   // host_counts[10] = events of the live batch
     out->n_true = m.dev->host_counts[0];
     out->n_false = m.dev->host_counts[1];
     out->events = m.dev->host_counts[2];
@@ -305,10 +308,15 @@ void harvest_spec_events(Model& m, PropKernel& pk) {
     DeviceState& d = *m.dev;
     if (!d.spec_valid) return;
     int64_t ev = 0;
-    ck(cudaMemcpyAsync(&ev, d.spec_scratch() + 2, 8, cudaMemcpyDeviceToHost, stream()), "D2H spec events");
-    ck(cudaStreamSynchronize(stream()), "cudaStreamSynchronize");
+    if (d.spec_events_host) {                       // read with the last round's counts
+        ev = d.host_counts[10];
+    } else {
+        ck(cudaMemcpyAsync(&ev, d.spec_scratch() + 2, 8, cudaMemcpyDeviceToHost, stream()), "D2H spec events");
+        ck(cudaStreamSynchronize(stream()), "cudaStreamSynchronize");
+    }
     pk.info.sim_events += (double)ev;
     d.spec_valid = false;
+    d.spec_events_host = false;
 }
 
 // Prefix-exact speculative round.  The counts of the round
