@@ -565,7 +565,6 @@ std::string generate_source(const Model& m, const Property& p, int variant, cons
         int minb = m.M <= 8 ? 4 : 6;
         if (const char* e = std::getenv("SMC_MINB")) minb = std::atoi(e);
         o << "#define SMC_BLOCK 128\n#define SMC_MINB " << minb << "\n";
-        if (const char* e = std::getenv("SMC_STRAIGHT")) o << "#define SMC_STRAIGHT " << std::atoi(e) << "\n";
         // two-stage draw pipeline: shorter per-event chain (-12 % at low occupancy, C2) for
         // register-light models; heavier models are throughput-bound and keep one stage
         int pipe2 = (m.M <= 8 && m.N <= 8) ? 1 : 0;

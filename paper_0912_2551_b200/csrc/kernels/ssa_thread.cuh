@@ -28,9 +28,6 @@
 //   x += v_j; a_k = law_k(x), k in dep(j); t = t'   step 4
 //   monitor.enter(t, x)               (may decide)
 
-#ifndef SMC_STRAIGHT
-#define SMC_STRAIGHT 0
-#endif
 #ifndef SMC_PIPE2
 #define SMC_PIPE2 0
 #endif
@@ -117,47 +114,6 @@ extern "C" __global__ void __launch_bounds__(SMC_BLOCK, SMC_MINB) smc_ssa_thread
             for (int m = 1; m < SMC_M; ++m) c[m] = __dadd_rn(c[m - 1], a[m]);
             const double A = c[SMC_M - 1];
             const double tn = __dadd_rn(t, smc_tau(e_cur, A));
-#if SMC_STRAIGHT
-            // straight-line (predicated) common path: one basic block from the draw of
-            // step k+1 to the monitor entry, so the scheduler can interleave the two chains
-            const bool okA = (A >= SMC_A_MIN) && (A <= SMC_A_MAX);
-            int v = -1;
-            if (okA) {
-                mon.advance(k, tn);
-                v = mon.verdict();
-                if (v < 0 && SMC_TMAX > 0.0 && tn > SMC_TMAX) { mon.timeout(); v = mon.verdict(); }
-            } else if (A == 0.0) {                        // absorbed (reading R7)
-                mon.absorb();
-                v = mon.verdict();
-            } else {
-                v = 2;                                    // bad propensity (R19)
-            }
-            const bool go = v < 0;
-            const double target = __dmul_rn(u_cur, A);
-            int j = 0;
-#pragma unroll
-            for (int m = 0; m < SMC_M; ++m) j += (c[m] <= target) ? 1 : 0;   // c is non-decreasing
-            if (j == SMC_M) j = smc_last_positive(a);                      // rounding (reading R11)
-            const bool ok = smc_apply(go ? j : -1, x);    // j = -1: no reaction, x unchanged
-            smc_update(j, a, x, H);                       // full recompute (x unchanged -> same a)
-            if (go) {
-                if (!ok) {
-                    v = 2;                                // count overflow
-                } else {
-                    tp = t;
-                    t = tn;
-                    ++k;
-                    e_cur = e_nx;
-                    u_cur = u_nx;
-#if SMC_PIPE2
-                    for (int q = 0; q < 4; ++q) r_nx[q] = r_nx2[q];
-#endif
-                    mon.enter(k, t, tp, x);
-                    v = mon.verdict();
-                    if (v < 0 && k >= cap) v = 2;
-                }
-            }
-#else
             int v = -1;
             if (!(A >= SMC_A_MIN) || A > SMC_A_MAX) {            // A == 0: absorbed; else error (R19)
                 if (A == 0.0) {                           // absorbed (reading R7)
@@ -190,7 +146,6 @@ extern "C" __global__ void __launch_bounds__(SMC_BLOCK, SMC_MINB) smc_ssa_thread
                         u_cur = u_nx;
 #if SMC_PIPE2
                         for (int q = 0; q < 4; ++q) r_nx[q] = r_nx2[q];
-#endif
                         mon.enter(k, t, tp, x);
                         v = mon.verdict();
                         if (v < 0 && k >= cap) v = 2;
