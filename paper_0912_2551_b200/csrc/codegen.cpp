@@ -488,12 +488,23 @@ TileLayout pack_tables(const Model& m) {
     L.off_hill_k = o; o = align16(o + (L.any_hill ? 8 * (size_t)M : 0));
     L.off_hill_n = o; o = align16(o + (L.any_hill ? 4 * (size_t)M : 0));
     L.off_chg = o; o = align16(o + 2 * 4 * (size_t)M);
-    L.off_dep_off = o; o = align16(o + 4 * ((size_t)M + 1));
-    // large networks: 2-byte dependency entries (k only, slot recomputed in the kernel) so
-    // the tables leave room for more resident trajectories
-    L.dep16 = M > 512;
-    if (const char* e = std::getenv("SMC_DEP16")) L.dep16 = std::atoi(e) != 0;
-    L.off_dep = o; o = align16(o + (L.dep16 ? 2 : 4) * nnz);
+    // Large networks, one trajectory per warp: the dependency work of reaction j is the
+    // union of the reader lists of the <= 4 species j changes (species-indexed CSR,
+    // ~1.5 entries per reaction instead of |dep(j)| ~ 19 per reaction: C5 tables 67 -> 28 KiB,
+    // i.e. more resident trajectories; a reaction reading two changed species is simply
+    // recomputed twice).  Otherwise a reaction-indexed CSR of dep(j), 2-byte entries (k
+    // only, slot recomputed) for M > 512, else 4-byte entries k | slot << 16.
+    std::vector<std::vector<int>> readers((size_t)N);
+    for (int k = 0; k < M; ++k)
+        for (int sp : m.law_species(k)) readers[(size_t)sp].push_back(k);
+    size_t nnz_sp = 0;
+    for (auto& r : readers) nnz_sp += r.size();
+    L.depsp = M > 512 && L.tw == 32;
+    if (const char* e = std::getenv("SMC_DEPSP")) L.depsp = std::atoi(e) != 0 && L.tw == 32;
+    L.dep16 = L.depsp || M > 512;
+    if (const char* e = std::getenv("SMC_DEP16")) L.dep16 = L.depsp || std::atoi(e) != 0;
+    L.off_dep_off = o; o = align16(o + 4 * ((size_t)(L.depsp ? N : M) + 1));
+    L.off_dep = o; o = align16(o + (L.dep16 ? 2 : 4) * (L.depsp ? nnz_sp : nnz));
     L.bytes = o;
     L.blob.assign(L.bytes, 0);
     auto* x0 = (int32_t*)(L.blob.data() + L.off_x0);
@@ -533,6 +544,14 @@ TileLayout pack_tables(const Model& m) {
     auto* dep16 = (uint16_t*)(L.blob.data() + L.off_dep);
     if ((size_t)L.gs * L.tw > 65536) fail(SMC_E_MODEL, "tile variant: too many reactions for 16-bit slots");
     size_t pos = 0;
+    if (L.depsp) {
+        for (int sp = 0; sp < N; ++sp) {
+            doff[sp] = (uint32_t)pos;
+            for (int k : readers[(size_t)sp]) dep16[pos++] = (uint16_t)k;
+        }
+        doff[N] = (uint32_t)pos;
+        return L;
+    }
     for (int j = 0; j < M; ++j) {
         doff[j] = (uint32_t)pos;
         for (int k : m.dep[(size_t)j]) {
@@ -583,6 +602,7 @@ std::string generate_source(const Model& m, const Property& p, int variant, cons
         o << "#define SMC_ANY_HILL " << (tl->any_hill ? 1 : 0) << "\n";
         o << "#define SMC_ANY_GENERAL " << (tl->any_general ? 1 : 0) << "\n";
         o << "#define SMC_DEP16 " << (tl->dep16 ? 1 : 0) << "\n";
+        o << "#define SMC_DEPSP " << (tl->depsp ? 1 : 0) << "\n";
         o << "#define SMC_ANY_EXPLICIT " << (tl->any_explicit ? 1 : 0) << "\n";
         if (const char* e = std::getenv("SMC_FLAT")) o << "#define SMC_FLAT " << std::atoi(e) << "\n";
     }

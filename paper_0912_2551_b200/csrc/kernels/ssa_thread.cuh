@@ -146,13 +146,13 @@ extern "C" __global__ void __launch_bounds__(SMC_BLOCK, SMC_MINB) smc_ssa_thread
                         u_cur = u_nx;
 #if SMC_PIPE2
                         for (int q = 0; q < 4; ++q) r_nx[q] = r_nx2[q];
+#endif
                         mon.enter(k, t, tp, x);
                         v = mon.verdict();
                         if (v < 0 && k >= cap) v = 2;
                     }
                 }
             }
-#endif
             if (v >= 0) {
                 if (v == 1) ++c_true;
                 else if (v == 0) ++c_false;

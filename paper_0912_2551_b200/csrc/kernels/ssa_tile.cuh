@@ -27,7 +27,7 @@
 //
 // Generated hooks (codegen.cpp): SMC_N, SMC_M, SMC_TW, SMC_GS, SMC_CH, SMC_NPAD,
 //   SMC_OFF_*, SMC_TAB_BYTES, SMC_TILE_BYTES, SMC_ANY_HILL, SMC_ANY_GENERAL, SMC_DEP16,
-//   SMC_ANY_EXPLICIT (+ smc_explicit),
+//   SMC_ANY_EXPLICIT (+ smc_explicit), SMC_DEPSP,
 //   SMC_TMAX, SmcMon.
 
 __device__ __forceinline__ void smc_mbar_init(unsigned long long* bar, unsigned count) {
@@ -155,7 +155,7 @@ __device__ __forceinline__ double smc_group_sum(const double* at, int l) {
     return __dadd_rn(se, so);
 }
 
-extern "C" __global__ void __launch_bounds__(640, 1) smc_ssa_tile(SmcParams P) {
+extern "C" __global__ void __launch_bounds__(768, 1) smc_ssa_tile(SmcParams P) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ __align__(8) unsigned long long bar;
     const int lane = (int)(threadIdx.x & 31u), warp = (int)(threadIdx.x >> 5);
@@ -340,6 +340,31 @@ extern "C" __global__ void __launch_bounds__(640, 1) smc_ssa_tile(SmcParams P) {
             {
                 const unsigned d0 = go ? T.dep_off[j] : 0u;
                 const unsigned nd = go ? T.dep_off[j + 1] - d0 : 0u;
+#if SMC_DEPSP
+                if (TPW == 1) {                           // union of the reader lists of the changed species
+                    unsigned st[4], pre[4], tot = 0;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const unsigned ce = go ? T.chg[j * 4 + q] : 0xFFFFu;
+                        const unsigned sp = ce >> 4;
+                        st[q] = (ce != 0xFFFFu) ? T.dep_off[sp] : 0u;
+                        const unsigned nq = (ce != 0xFFFFu) ? T.dep_off[sp + 1] - st[q] : 0u;
+                        pre[q] = tot;
+                        tot += nq;
+                    }
+                    for (unsigned b = (unsigned)lane; b < tot; b += 32u) {
+                        const int q = (b >= pre[1]) + (b >= pre[2]) + (b >= pre[3]);
+                        unsigned base = st[0], p0 = 0u;
+#pragma unroll
+                        for (int w = 1; w < 4; ++w)
+                            if (q == w) { base = st[w]; p0 = pre[w]; }
+                        int kk, slot;
+                        smc_dep_entry(T.dep[base + (b - p0)], kk, slot);
+                        at[slot] = smc_law_tab(kk, xs, T);
+                        touched |= 1u << smc_owner(slot);
+                    }
+                } else
+#endif
                 if (TPW == 1 || !SMC_FLAT) {              // each tile walks its own dep(j) with its TW lanes
                     const smc_u32 tb = (TPW == 1) ? 0u : (smc_u32)(tile * TW);
                     for (unsigned b = (unsigned)tl; __any_sync(SMC_FULL, b < nd); b += (unsigned)TW) {

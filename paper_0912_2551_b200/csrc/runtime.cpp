@@ -216,7 +216,9 @@ PropKernel& prepare(Model& m, const Property& p) {
         const size_t max_dyn = (size_t)d.max_smem_optin - fa.sharedSizeBytes;
         ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)max_dyn), "smem attr");
         int best_total = 0, best_w = 0, best_nb = 0;
-        for (int W = 20; W >= 1; --W) {   // <= 640 threads (__launch_bounds__ of smc_ssa_tile)
+        int wmax = 24;                     // <= 768 threads (__launch_bounds__ of smc_ssa_tile)
+        if (const char* e = std::getenv("SMC_TILE_WARPS")) wmax = std::max(1, std::min(24, std::atoi(e)));
+        for (int W = wmax; W >= 1; --W) {
             size_t smem = tl->bytes + (size_t)W * wb;
             if (smem > max_dyn) continue;
             int nb = 0;
