@@ -15,6 +15,15 @@ cudaError_t smc_launch_philox_debug(uint64_t seed, uint64_t traj, uint64_t step0
                                     cudaStream_t stream);
 cudaError_t smc_launch_draw_debug(uint64_t seed, uint64_t traj, uint64_t step0, uint32_t n, double* dev_out,
                                   cudaStream_t stream);
+struct SmcWState {               // aot_kernels.cu (device-resident Fig. 2 rounds)
+    unsigned long long cursor;
+    long long n_tot, yes, events, errors, N;
+    int rounds, status;
+    double p_hat;
+};
+cudaError_t smc_launch_wilson_rounds(const unsigned char* v, const int* e, uint64_t begin, uint64_t end,
+                                     const SmcWState* st, double z, double eps, SmcWState* out,
+                                     cudaStream_t stream);
 cudaError_t smc_launch_count_range(const unsigned char* v, const int* e, uint64_t n, long long* counters,
                                    cudaStream_t stream);
 
@@ -88,6 +97,8 @@ struct DeviceState {
     uint64_t spec_cap = 0, spec_begin = 0, spec_end = 0, spec_lo = 0, spec_hi = 0;
     bool spec_valid = false;
     bool spec_events_host = false;  // host_counts[10] holds the live batch's simulated events
+    SmcWState* wst_dev = nullptr;   // device-resident Fig. 2 loop state
+    SmcWState* wst_host = nullptr;  // pinned
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     int sm_count = 0, max_smem_optin = 0;
     std::map<uint64_t, PropKernel> kernels;
@@ -101,6 +112,8 @@ struct DeviceState {
         if (e0) cudaEventDestroy(e0);
         if (e1) cudaEventDestroy(e1);
         if (host_counts) cudaFreeHost(host_counts);
+        if (wst_host) cudaFreeHost(wst_host);
+        dfree(wst_dev);
         dfree(ctl);
         dfree(spec_v);
         dfree(spec_e);
@@ -321,6 +334,37 @@ void harvest_spec_events(Model& m, PropKernel& pk) {
     d.spec_events_host = false;
 }
 
+// Launch a speculative batch starting at replica `covered`: at least `need` replicas,
+// else as many as all GPUs hold at once, never past the conservative size `limit`.
+void launch_batch(Model& m, PropKernel& pk, uint64_t seed, uint64_t covered, uint64_t need, uint64_t limit) {
+    DeviceState& d = *m.dev;
+    Hooks& h = hooks();
+    const uint64_t cap_all = pk.capacity() * (uint64_t)h.world;
+    const uint64_t room = limit > covered ? limit - covered : 0;
+    const uint64_t S = std::max(need, std::min(cap_all, room));
+    uint64_t lo = covered, hi = covered + S;
+    if (h.world > 1) smc_shard_range(covered, S, h.rank, h.world, &lo, &hi);
+    if (hi - lo > d.spec_cap) {
+        dfree(d.spec_v);
+        dfree(d.spec_e);
+        d.spec_v = nullptr;
+        d.spec_e = nullptr;
+        d.spec_cap = 0;
+        const uint64_t c = hi - lo;
+        d.spec_v = (unsigned char*)dalloc(c);
+        d.spec_e = (int*)dalloc(4 * c);
+        d.spec_cap = c;
+    }
+    harvest_spec_events(m, pk);
+    launch_slice(m, pk, seed, lo, hi, d.spec_v, d.spec_e, true);
+    ck(cudaGetLastError(), "kernel launch");
+    d.spec_begin = covered;
+    d.spec_end = covered + S;
+    d.spec_lo = lo;
+    d.spec_hi = hi;
+    d.spec_valid = true;
+}
+
 // Prefix-exact speculative round.  The counts of the round
 // range [base, base+n) are summed from per-replica results; when the range is not
 // covered by the current batch, a new batch starting at the first uncovered index
@@ -331,7 +375,6 @@ void harvest_spec_events(Model& m, PropKernel& pk) {
 // final N_tot are simulated but never counted.
 void spec_round(Model& m, PropKernel& pk, uint64_t seed, uint64_t base, uint64_t n, uint64_t limit, smc_counts* out) {
     DeviceState& d = *m.dev;
-    Hooks& h = hooks();
     const uint64_t end = base + n;
     ck(cudaMemsetAsync(d.ctl, 0, 64, stream()), "memset counters");
     auto count = [&](uint64_t a, uint64_t b) {       // [a, b) within this rank's slice of the batch
@@ -350,31 +393,7 @@ void spec_round(Model& m, PropKernel& pk, uint64_t seed, uint64_t base, uint64_t
         covered = std::min(end, d.spec_end);
     }
     if (covered < end) {
-        const uint64_t need = end - covered;
-        const uint64_t cap_all = pk.capacity() * (uint64_t)h.world;
-        const uint64_t room = limit > covered ? limit - covered : 0;
-        const uint64_t S = std::max(need, std::min(cap_all, room));
-        uint64_t lo = covered, hi = covered + S;
-        if (h.world > 1) smc_shard_range(covered, S, h.rank, h.world, &lo, &hi);
-        if (hi - lo > d.spec_cap) {
-            dfree(d.spec_v);
-            dfree(d.spec_e);
-            d.spec_v = nullptr;
-            d.spec_e = nullptr;
-            d.spec_cap = 0;
-            const uint64_t c = hi - lo;
-            d.spec_v = (unsigned char*)dalloc(c);
-            d.spec_e = (int*)dalloc(4 * c);
-            d.spec_cap = c;
-        }
-        harvest_spec_events(m, pk);
-        launch_slice(m, pk, seed, lo, hi, d.spec_v, d.spec_e, true);
-        ck(cudaGetLastError(), "kernel launch");
-        d.spec_begin = covered;
-        d.spec_end = covered + S;
-        d.spec_lo = lo;
-        d.spec_hi = hi;
-        d.spec_valid = true;
+        launch_batch(m, pk, seed, covered, end - covered, limit);
         count(covered, end);
     }
     read_counts(m, pk, out);
@@ -397,42 +416,108 @@ int run_round(Model& m, const Property& p, uint64_t seed, uint64_t base, uint64_
 // ------------------------------------------------------------ Fig. 2 ---
 namespace {
 // The Fig. 2 loop over any round runner (global counts).
+// One Fig. 2 step after a round's counts; the device twin is
+// smc_wilson_rounds() in aot_kernels.cu (same operations, same order).
+void wilson_host_step(SmcWState& w, const smc_counts& c, double eps, double z) {
+    w.cursor += (unsigned long long)w.N;
+    w.n_tot += c.n_true + c.n_false;                     // errors excluded from trials
+    w.yes += c.n_true;
+    w.events += c.events;
+    w.errors += c.errors;
+    w.rounds += 1;
+    if ((double)w.errors > 0.01 * (double)w.cursor) { w.status = 2; return; }
+    if (w.n_tot == 0) { w.N = 1; return; }
+    const double p_est = (double)w.yes / (double)w.n_tot;   // "pest = yess" (reading W2)
+    w.p_hat = p_est;
+    const double p_prime = round_estimate(p_est, eps);
+    const int64_t n_new = wilson_sample_size(p_prime, eps, z) - w.n_tot;
+    if (n_new > 0) w.N = n_new;
+    else w.status = 1;
+}
+
+// loop state -> smc_estimate_t; the interval of a finished loop (Eq. 3 at p_hat, N_tot)
+void wilson_state_out(const SmcWState& w, smc_estimate_t* out) {
+    out->events = w.events;
+    out->errors = w.errors;
+    out->rounds = w.rounds;
+    out->n_total = w.n_tot;
+    out->n_true = w.yes;
+    out->p_hat = w.p_hat;
+}
+int wilson_finish(const SmcWState& w, double z, smc_estimate_t* out) {
+    wilson_state_out(w, out);
+    if (w.status == 2) {
+        set_error("more than 1% of replicas ended in error (overflow / event cap / bad propensity)");
+        return SMC_E_ERRRATE;
+    }
+    if (w.status != 1) {
+        set_error("Wilson loop did not terminate");
+        return SMC_E_ARG;
+    }
+    wilson_interval(w.p_hat, (double)w.n_tot, z, &out->lower, &out->upper);
+    return SMC_OK;
+}
+
+// The Fig. 2 loop over any round runner (global counts).
 template <class Runner>
 int wilson_loop(Runner&& run, double confidence, double eps, double start, smc_estimate_t* out) {
     std::memset(out, 0, sizeof *out);
     const double z = normal_quantile(confidence);
     out->z = z;
-    int64_t N = wilson_sample_size(start, eps, z);       // "N = Wilson_Sample(1, epsilon, alpha)"
-    uint64_t cursor = 0;                                 // next trajectory index
-    int64_t n_tot = 0, yes = 0;
-    for (int round = 0; round < 100000; ++round) {
+    SmcWState w{};
+    w.N = wilson_sample_size(start, eps, z);             // "N = Wilson_Sample(1, epsilon, alpha)"
+    while (w.status == 0 && w.rounds < 100000) {
         smc_counts c{};
-        int rc = run(cursor, (uint64_t)N, &c);           // "Perform N experiments"
-        if (rc != SMC_OK) return rc;
-        cursor += (uint64_t)N;
-        n_tot += c.n_true + c.n_false;                   // errors excluded from trials
-        yes += c.n_true;
-        out->events += c.events;
-        out->errors += c.errors;
-        out->rounds = round + 1;
-        out->n_total = n_tot;
-        out->n_true = yes;
-        if ((double)out->errors > 0.01 * (double)cursor) {
-            set_error("more than 1% of replicas ended in error (overflow / event cap / bad propensity)");
-            return SMC_E_ERRRATE;
+        int rc = run(w.cursor, (uint64_t)w.N, &c);       // "Perform N experiments"
+        if (rc != SMC_OK) {
+            wilson_state_out(w, out);                    // partial state
+            return rc;
         }
-        if (n_tot == 0) { N = 1; continue; }
-        const double p_est = (double)yes / (double)n_tot;   // "pest = yess" (reading W2)
-        out->p_hat = p_est;
-        const double p_prime = round_estimate(p_est, eps);
-        const int64_t n_prime = wilson_sample_size(p_prime, eps, z);
-        const int64_t n_new = n_prime - n_tot;
-        if (n_new > 0) { N = n_new; continue; }
-        wilson_interval(p_est, (double)n_tot, z, &out->lower, &out->upper);
-        return SMC_OK;
+        wilson_host_step(w, c, eps, z);
     }
-    set_error("Wilson loop did not terminate");
-    return SMC_E_ARG;
+    return wilson_finish(w, z, out);
+}
+
+// Device-resident Fig. 2 loop (one GPU): after each speculative
+// batch, smc_wilson_rounds consumes every round the batch covers and the host reads the
+// loop state once.  A round only partly covered by the live batch is run on the host
+// (spec_round: counts the covered part, launches the next batch).  Identical results to
+// wilson_loop (test_speculative_rounds_identical).
+int device_estimate(Model& m, PropKernel& pk, uint64_t seed, double confidence, double eps, double start,
+                    uint64_t limit, smc_estimate_t* out) {
+    std::memset(out, 0, sizeof *out);
+    const double z = normal_quantile(confidence);
+    out->z = z;
+    DeviceState& d = *m.dev;
+    if (!d.wst_dev) {
+        d.wst_dev = (SmcWState*)dalloc(sizeof(SmcWState));
+        ck(cudaMallocHost((void**)&d.wst_host, sizeof(SmcWState)), "cudaMallocHost");
+    }
+    SmcWState w{};
+    w.N = wilson_sample_size(start, eps, z);
+    while (w.status == 0 && w.rounds < 100000) {
+        const uint64_t end = w.cursor + (uint64_t)w.N;
+        if (!(d.spec_valid && w.cursor >= d.spec_begin && end <= d.spec_end)) {
+            if (d.spec_valid && w.cursor >= d.spec_begin && w.cursor < d.spec_end) {
+                smc_counts c{};
+                spec_round(m, pk, seed, w.cursor, (uint64_t)w.N, limit, &c);
+                wilson_host_step(w, c, eps, z);
+                continue;
+            }
+            launch_batch(m, pk, seed, w.cursor, (uint64_t)w.N, limit);
+        }
+        ck(smc_launch_wilson_rounds(d.spec_v, d.spec_e, d.spec_begin, d.spec_end, &w, z, eps, d.wst_dev, stream()),
+           "wilson rounds kernel");
+        pk.info.aux_launches += 1;
+        ck(cudaMemcpyAsync(d.wst_host, d.wst_dev, sizeof(SmcWState), cudaMemcpyDeviceToHost, stream()), "D2H state");
+        ck(cudaMemcpyAsync(d.host_counts + 10, d.spec_scratch() + 2, 8, cudaMemcpyDeviceToHost, stream()),
+           "D2H spec events");
+        ck(cudaStreamSynchronize(stream()), "cudaStreamSynchronize");
+        finish_timing(m, pk);
+        d.spec_events_host = true;
+        w = *d.wst_host;
+    }
+    return wilson_finish(w, z, out);
 }
 
 int guard(const std::function<int()>& f) {
@@ -523,6 +608,11 @@ int smc_estimate_ex(smc_model* h, const smc_property* ph, double confidence, dou
         // no Fig. 2 round can reach past the conservative size Eq. 4(0.5) (N' <= Eq. 4(0.5))
         const uint64_t limit = (uint64_t)wilson_sample_size(0.5, half_width, normal_quantile(confidence));
         const bool speculate = m.speculate;
+        if (speculate && hooks().world == 1) {
+            const int rc = device_estimate(m, pk, seed, confidence, half_width, start, limit, out);
+            harvest_spec_events(m, pk);
+            return rc;
+        }
         int rc = wilson_loop(
             [&](uint64_t base, uint64_t n, smc_counts* c) {
                 if (speculate) {
