@@ -256,7 +256,7 @@ def test_c4_full_size_shard_sampled(smc):
     assert abs(v.mean() - 0.54) < 0.03          # fixture estimate 0.5415 (2000 oracle replicas)
 
 
-@pytest.mark.parametrize("name,eps", [("C1", 0.01), ("C2", 0.005), ("C3", 0.02)])
+@pytest.mark.parametrize("name,eps", [("C1", 0.01), ("C2", 0.005), ("C3", 0.02), ("C1", 0.0005), ("C1", 0.0003)])
 def test_speculative_rounds_identical(smc, name, eps):
     """Prefix-exact speculation changes only the schedule: the
     Fig. 2 estimate equals the one from exactly-sized rounds, bit for bit."""
@@ -267,6 +267,8 @@ def test_speculative_rounds_identical(smc, name, eps):
     off = smc.estimate(m, p, 0.99, eps, 17)
     assert on == off
     assert on["rounds"] >= 2
+    # eps = 5e-4 / 3e-4: Eq. 4(0.5) (6.6e6 / 1.8e7) exceeds the resident lanes, so rounds run
+    # over several speculative batches, partly covered ones included
 
 
 def test_c5_first_round_sampled(smc):
