@@ -106,6 +106,7 @@ struct MonGen {
             if (lf.kind == LeafKind::FG || lf.kind == LeafKind::GF) o << "    bool rs" << i << "_set; double rs" << i << ";\n";
             if (lf.kind == LeafKind::GU) o << "    bool w" << i << "; double D" << i << ";\n";
         }
+        o << "    __device__ __forceinline__ void bind(const SmcParams&, smc_u64) {}\n";
         // init
         o << "    __device__ __forceinline__ void init() {\n";
         for (size_t i = 0; i < L; ++i) {
@@ -155,7 +156,7 @@ struct MonGen {
         }
         o << "    }\n";
         // advance
-        o << "    __device__ __forceinline__ void advance(smc_u32 k, double tn) {\n        (void)k;\n";
+        o << "    __device__ __forceinline__ void advance(smc_u32 k, double tn, double tau) {\n        (void)k; (void)tau;\n";
         for (size_t i = 0; i < L; ++i) {
             const Leaf& lf = P.leaves[i];
             std::string s = "s" + std::to_string(i), id = std::to_string(i);
@@ -310,6 +311,40 @@ std::string literal_code(const Property& P) {
         o << "    }\n";
     }
     o << "    return vb[" << P.lroot << "LL * cap];\n}\n";
+    return o.str();
+}
+
+// Recording monitor (tile variant, formulas outside R16; reading R23): the same interface
+// as the template monitors; it buffers (t_k, tau_k, atom mask_k) of the tile's replica and,
+// once the trace passes the horizon or is absorbed, evaluates |= with smc_lit_eval.  All
+// lanes of a tile hold and write identical values.
+std::string recording_monitor(const Property& P) {
+    std::ostringstream o;
+    o << "struct SmcMon {   // recording monitor for: " << P.text << "\n"
+         "    double* tb; double* ub; unsigned* mb; unsigned char* vb; long long cap, last; int res;\n"
+         "    __device__ __forceinline__ void bind(const SmcParams& Q, smc_u64 slot) {\n"
+         "        cap = (long long)Q.lit_cap;\n"
+         "        tb = Q.lit_t + slot * (smc_u64)cap; ub = Q.lit_tau + slot * (smc_u64)cap;\n"
+         "        mb = Q.lit_mask + slot * (smc_u64)cap; vb = Q.lit_val + slot * (smc_u64)cap * SMC_LIT_NODES;\n"
+         "    }\n"
+         "    __device__ __forceinline__ void init() { res = -1; last = 0; }\n"
+         "    template <class XA> __device__ __forceinline__ void enter(smc_u32 k, double t, double tp, const XA& x) {\n"
+         "        (void)tp;\n"
+         "        if (res >= 0) return;\n"
+         "        if ((long long)k >= cap - 1) { res = 2; return; }   // trace buffer full: replica error\n"
+         "        tb[k] = t; mb[k] = smc_lit_mask(x); last = (long long)k;\n"
+         "    }\n"
+         "    __device__ __forceinline__ void advance(smc_u32 k, double tn, double tau) {\n"
+         "        if (res >= 0) return;\n"
+         "        ub[k] = tau;\n"
+         "        if (tn > SMC_LIT_H) res = smc_lit_eval(tb, ub, mb, vb, (long long)k, false, cap) == 1 ? 1 : 0;\n"
+         "    }\n"
+         "    __device__ __forceinline__ void absorb() {\n"
+         "        if (res < 0) res = smc_lit_eval(tb, ub, mb, vb, last, true, cap) == 1 ? 1 : 0;\n"
+         "    }\n"
+         "    __device__ __forceinline__ void timeout() {}\n"
+         "    __device__ __forceinline__ int verdict() const { return res; }\n"
+         "};\n";
     return o.str();
 }
 
@@ -591,6 +626,10 @@ std::string generate_source(const Model& m, const Property& p, int variant, cons
         o << "#define SMC_PIPE2 " << pipe2 << "\n";
         if (const char* e = std::getenv("SMC_UNROLL")) o << "#define SMC_UNROLL " << std::atoi(e) << "\n";
     } else {
+        if (p.literal) {
+            const double H = p.t_max > 0.0 ? p.t_max : p.horizon;
+            o << "#define SMC_LIT_H " << dlit(H) << "\n#define SMC_LIT_NODES " << p.lnodes.size() << "\n";
+        }
         o << "#define SMC_TW " << tl->tw << "\n#define SMC_GS " << tl->gs << "\n#define SMC_CH " << tl->ch
           << "\n#define SMC_NPAD " << tl->n_pad << "\n";
         o << "#define SMC_OFF_X0 " << tl->off_x0 << "\n#define SMC_OFF_LAW " << tl->off_law
@@ -619,7 +658,8 @@ std::string generate_source(const Model& m, const Property& p, int variant, cons
         o << literal_code(p) << "\n" << embedded_source("ssa_literal.cuh") << "\n";
         return o.str();
     }
-    o << MonGen(p).emit() << "\n";
+    if (p.literal) o << literal_code(p) << "\n" << recording_monitor(p) << "\n";   // variant 2 only
+    else o << MonGen(p).emit() << "\n";
     o << embedded_source(variant == 1 ? "ssa_thread.cuh" : "ssa_tile.cuh") << "\n";
     return o.str();
 }

@@ -113,7 +113,8 @@ extern "C" __global__ void __launch_bounds__(SMC_BLOCK, SMC_MINB) smc_ssa_thread
 #pragma unroll
             for (int m = 1; m < SMC_M; ++m) c[m] = __dadd_rn(c[m - 1], a[m]);
             const double A = c[SMC_M - 1];
-            const double tn = __dadd_rn(t, smc_tau(e_cur, A));
+            const double tau = smc_tau(e_cur, A);
+            const double tn = __dadd_rn(t, tau);
             int v = -1;
             if (!(A >= SMC_A_MIN) || A > SMC_A_MAX) {            // A == 0: absorbed; else error (R19)
                 if (A == 0.0) {                           // absorbed (reading R7)
@@ -123,7 +124,7 @@ extern "C" __global__ void __launch_bounds__(SMC_BLOCK, SMC_MINB) smc_ssa_thread
                     v = 2;                                // bad propensity
                 }
             } else {
-                mon.advance(k, tn);
+                mon.advance(k, tn, tau);
                 v = mon.verdict();
                 if (v < 0 && SMC_TMAX > 0.0 && tn > SMC_TMAX) {
                     mon.timeout();

@@ -199,6 +199,7 @@ extern "C" __global__ void __launch_bounds__(768, 1) smc_ssa_tile(SmcParams P) {
     smc_u32 k = 0, kb = 0;
     double Eb = 0.0, Ub = 0.0;          // draw of step kb + tl
     SmcMon mon;
+    mon.bind(P, ((smc_u64)blockIdx.x * (blockDim.x >> 5) + (smc_u64)warp) * TPW + (smc_u64)tile);   // trace slot (R23)
     smc_u32 c_true = 0, c_false = 0, c_err = 0;   // tile leader
     smc_i64 c_ev = 0;
 
@@ -266,14 +267,15 @@ extern "C" __global__ void __launch_bounds__(768, 1) smc_ssa_tile(SmcParams P) {
             const int q = (int)(k - kb) & (TW - 1);
             const double E = __shfl_sync(SMC_FULL, Eb, q, TW);
             const double U = __shfl_sync(SMC_FULL, Ub, q, TW);
-            const double tn = __dadd_rn(t, smc_tau(E, A));
+            const double tau = smc_tau(E, A);
+            const double tn = __dadd_rn(t, tau);
             int v = -1;
             if (act) {
                 if (!(A >= SMC_A_MIN) || A > SMC_A_MAX) {            // A == 0: absorbed; else error (R19)
                     if (A == 0.0) { mon.absorb(); v = mon.verdict(); }     // absorbed (reading R7)
                     else v = 2;                                            // bad propensity
                 } else {
-                    mon.advance(k, tn);
+                    mon.advance(k, tn, tau);
                     v = mon.verdict();
                     if (v < 0 && SMC_TMAX > 0.0 && tn > SMC_TMAX) { mon.timeout(); v = mon.verdict(); }
                 }

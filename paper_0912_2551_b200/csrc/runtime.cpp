@@ -147,6 +147,31 @@ DeviceState& device(Model& m) {
     return *m.dev;
 }
 
+// Trace buffers of the literal |= (reading R23) for `per_cta` replicas per CTA: at most a
+// quarter of the free device memory and 16 GiB per property; every resident replica
+// gets >= 4096 entries (fewer resident CTAs if needed) and no more than the event cap.
+void alloc_traces(Model& m, const Property& p, PropKernel& pk, int per_cta) {
+    size_t free_b = 0, total_b = 0;
+    ck(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+    const size_t budget = std::min<size_t>(free_b / 4, (size_t)16 << 30);
+    const size_t per_entry = 8 + 8 + 4 + p.lnodes.size();
+    const size_t want_cap = (size_t)std::min<uint64_t>(m.event_cap + 2, 1ull << 24);
+    size_t slots = (size_t)pk.grid_max * (size_t)per_cta;
+    const size_t min_cap = std::min<size_t>(want_cap, 4096);
+    if (budget / (slots * per_entry) < min_cap) {
+        const size_t blocks = std::max<size_t>(1, budget / (min_cap * per_entry * (size_t)per_cta));
+        pk.grid_max = (int)std::min<size_t>((size_t)pk.grid_max, blocks);
+        slots = (size_t)pk.grid_max * (size_t)per_cta;
+    }
+    const size_t cap = std::min<size_t>(budget / (slots * per_entry), want_cap);
+    if (cap < 16) fail(SMC_E_CUDA, "literal |=: not enough device memory for trace buffers");
+    pk.lit_cap = cap;
+    pk.lit_t = (double*)dalloc(slots * cap * 8);
+    pk.lit_tau = (double*)dalloc(slots * cap * 8);
+    pk.lit_mask = (unsigned*)dalloc(slots * cap * 4);
+    pk.lit_val = (unsigned char*)dalloc(slots * cap * p.lnodes.size());
+}
+
 PropKernel& prepare(Model& m, const Property& p) {
     DeviceState& d = device(m);
     auto it = d.kernels.find(p.id);
@@ -154,12 +179,9 @@ PropKernel& prepare(Model& m, const Property& p) {
     m.build_deps();
     PropKernel pk;
     pk.variant = m.variant();
-    if (p.literal) {                       // buffered trace + literal |= (thread-owned only)
-        if (m.N > 32 || m.M > 32 || m.variant_forced == 2)
-            fail(SMC_E_UNSUPPORTED, "formula outside the streaming templates needs the thread-owned variant "
-                                    "(N <= 32, M <= 32)");
-        pk.variant = 3;
-    }
+    // buffered trace + literal |= (reading R23): thread-owned models run variant 3, tile
+    // models the tile kernel with the recording monitor
+    if (p.literal && pk.variant == 1) pk.variant = 3;
     const TileLayout* tl = nullptr;
     const int v = pk.variant == 3 ? 1 : pk.variant;      // table set (variant 3 uses variant 1's)
     if (!d.tables_ready[v]) {
@@ -194,28 +216,7 @@ PropKernel& prepare(Model& m, const Property& p) {
         ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, pk.block, 0), "occupancy");
         pk.grid_max = std::max(1, nb) * d.sm_count;
         pk.smem = 0;
-        // trace buffers: at most a quarter of the free device memory and 16 GiB per property;
-        // every resident thread gets >= 4096 entries (fewer resident CTAs if needed), and no
-        // more entries than the event cap allows
-        size_t free_b = 0, total_b = 0;
-        ck(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
-        const size_t budget = std::min<size_t>(free_b / 4, (size_t)16 << 30);
-        const size_t per_entry = 8 + 8 + 4 + p.lnodes.size();
-        const size_t want_cap = (size_t)std::min<uint64_t>(m.event_cap + 2, 1ull << 24);
-        size_t lanes = (size_t)pk.grid_max * (size_t)pk.block;
-        const size_t min_cap = std::min<size_t>(want_cap, 4096);
-        if (budget / (lanes * per_entry) < min_cap) {
-            const size_t blocks = std::max<size_t>(1, budget / (min_cap * per_entry * (size_t)pk.block));
-            pk.grid_max = (int)std::min<size_t>((size_t)pk.grid_max, blocks);
-            lanes = (size_t)pk.grid_max * (size_t)pk.block;
-        }
-        size_t cap = std::min<size_t>(budget / (lanes * per_entry), want_cap);
-        if (cap < 16) fail(SMC_E_CUDA, "literal variant: not enough device memory for trace buffers");
-        pk.lit_cap = cap;
-        pk.lit_t = (double*)dalloc(lanes * cap * 8);
-        pk.lit_tau = (double*)dalloc(lanes * cap * 8);
-        pk.lit_mask = (unsigned*)dalloc(lanes * cap * 4);
-        pk.lit_val = (unsigned char*)dalloc(lanes * cap * p.lnodes.size());
+        alloc_traces(m, p, pk, pk.block);
     } else if (pk.variant == 1) {
         pk.block = 128;
         int nb = 0;
@@ -243,6 +244,7 @@ PropKernel& prepare(Model& m, const Property& p) {
         pk.smem = (int)(tl->bytes + (size_t)best_w * wb);
         pk.grid_max = best_nb * d.sm_count;
         pk.per_warp = 32 / tl->tw;
+        if (p.literal) alloc_traces(m, p, pk, best_w * pk.per_warp);   // one trace per tile
     }
     pk.info.variant = pk.variant;
     pk.info.block_threads = pk.block;
@@ -730,7 +732,8 @@ int smc_kernel_source(smc_model* h, const smc_property* ph, char* buf, size_t* l
         Model& m = h->m;
         std::lock_guard<std::mutex> lk(m.mu);
         m.build_deps();
-        const int v = ph->p->literal ? 3 : m.variant();
+        const int mv = m.variant();
+        const int v = (ph->p->literal && mv == 1) ? 3 : mv;
         TileLayout tl;
         if (v == 2) tl = pack_tables(m);
         std::string s = generate_source(m, *ph->p, v, v == 2 ? &tl : nullptr);

@@ -43,3 +43,8 @@ def test_literal_variant_compiles():
     assert "smc_ssa_literal" in src
     src, _ = _compile(workloads.c2(), 0, "G(E + ES == 100) & F(0,2](G[0.5,1](P > 3))", t_max=10.0)
     assert "smc_ssa_literal" in src
+
+
+def test_tile_recording_monitor_compiles():
+    src, _ = _compile(workloads.c4(), 0, "F[0,0.3](S0 < S1 + 3 & G[0.01,0.04](S0 < S1 + 3))")
+    assert "smc_ssa_tile" in src and "recording monitor" in src

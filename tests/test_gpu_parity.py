@@ -468,3 +468,31 @@ def test_nested_formulas_literal_variant_vs_oracle(smc, case):
     of = O.OracleFormula(f, cfg["species"], t_max)
     oc, ov, oe = O.run(om, of, 5, 0, 2000, mode="literal")
     assert float(((v == ov) & (e == oe)).mean()) >= 0.9995, (f, float((v == ov).mean()), float((e == oe).mean()))
+
+
+@pytest.mark.parametrize("case", range(len(NESTED)))
+def test_nested_formulas_tile_recording_monitor_vs_oracle(smc, case):
+    """NEXT-2 in the tile kernel (recording monitor, reading R23): the NESTED formulas with
+    the models forced to variant 2 equal the oracle's literal mode replica for replica."""
+    name, f = NESTED[case]
+    cfg = dict(_iso_cfg() if name == "iso" else workloads.c2(), formula=f)
+    t_max = 4.0 if "G(" in f else 0.0
+    cfg["t_max"] = t_max
+    m, p = _pair(smc, cfg, variant=2)
+    v, e = m.run_verdicts(p, 0, 1000, 5)
+    v, e = v.cpu().numpy(), e.cpu().numpy().astype(np.int64)
+    assert m.last_launch(p)["variant"] == 2
+    oc, ov, oe = O.run(O.OracleModel(cfg), O.OracleFormula(f, cfg["species"], t_max), 5, 0, 1000, mode="literal")
+    assert float(((v == ov) & (e == oe)).mean()) >= 0.999, (f, float((v == ov).mean()), float((e == oe).mean()))
+
+
+def test_nested_formula_on_c4_tile_vs_oracle(smc):
+    """A formula outside R16 on the 50 x 200 network (tile-only model)."""
+    f = "F[0.01,0.03](X[0,0.0001](S1 > S0 - 40))"
+    cfg = dict(workloads.c4(), formula=f)
+    m, p = _pair(smc, cfg)
+    v, e = m.run_verdicts(p, 0, 40, 4)
+    v, e = v.cpu().numpy(), e.cpu().numpy().astype(np.int64)
+    assert m.last_launch(p)["variant"] == 2
+    oc, ov, oe = O.run(O.OracleModel(cfg), O.OracleFormula(f, cfg["species"]), 4, 0, 40, mode="literal")
+    assert int(((v != ov) | (e != oe)).sum()) == 0
