@@ -501,7 +501,7 @@ TileLayout pack_tables(const Model& m) {
     L.gs = (M + L.tw - 1) / L.tw;
     L.ch = 1;
     while (L.ch * L.tw < L.gs) L.ch *= 2;      // chunk per lane in the in-group selection (power of two)
-    L.n_pad = (N + 3) & ~3;
+    L.n_pad = (N + 1 + 3) & ~3;     // x[0..N) counts, x[N] = 1 (operand of h = x * 1 and h = 1 * 1)
     // per-trajectory slice: a[GS*TW] (fp64) + x[NPAD] (int32), 16-byte aligned; with several
     // tiles per warp the slice is padded to 8*TW mod 128 bytes so that the TPW tiles of a
     // warp cover consecutive bank ranges (minimum wavefronts per warp access)
@@ -544,24 +544,33 @@ TileLayout pack_tables(const Model& m) {
     L.blob.assign(L.bytes, 0);
     auto* x0 = (int32_t*)(L.blob.data() + L.off_x0);
     for (int s = 0; s < N; ++s) x0[s] = m.x0[(size_t)s];
+    x0[N] = 1;
     auto* chg = (uint16_t*)(L.blob.data() + L.off_chg);
     for (int j = 0; j < M; ++j) {
         const Reaction& r = m.R[(size_t)j];
-        // law kind (ssa_tile.cuh smc_law_tab): 0 h=1, 1 x0, 2 x0(x0-1)/2, 3 x0*x1, 4 general
-        uint32_t kind, s0 = 0, s1 = 0;
+        // law kind (ssa_tile.cuh smc_law_tab): h = x[s0] * x[s1] with x[N] = 1 for kinds
+        // 0 (h = 1), 1 (x), 3 (x y); kind 2 (x(x-1)/2) as x * (x-1) with c/2 (exact: halving);
+        // 4 general order 3-4 (int64); 5 explicit rate
+        uint32_t kind, s0 = (uint32_t)N, s1 = (uint32_t)N;
+        double c = r.c;
         if (!r.rate.empty()) kind = 5;                  // explicit rate (generated smc_explicit)
         else if (r.s[0] < 0) kind = 0;
-        else if (r.s[1] < 0) { kind = r.st[0] == 1 ? 1u : 2u; s0 = s1 = (uint32_t)r.s[0]; }
-        else { kind = (r.st[0] == 1 && r.st[1] == 1) ? 3u : 4u; s0 = (uint32_t)r.s[0]; s1 = (uint32_t)r.s[1]; }
+        else if (r.s[1] < 0 && r.st[0] == 1) { kind = 1; s0 = (uint32_t)r.s[0]; }
+        else if (r.s[1] < 0) {
+            kind = 2;
+            s0 = s1 = (uint32_t)r.s[0];
+            if ((c * 0.5) * 2.0 == c && c * 0.5 >= 0x1p-1021) c *= 0.5;   // fold the 1/2 (exact)
+            else { kind = 4; s1 = (uint32_t)N; }                       // subnormal rate: int64 path, x[N] = 1
+        } else { kind = (r.st[0] == 1 && r.st[1] == 1) ? 3u : 4u; s0 = (uint32_t)r.s[0]; s1 = (uint32_t)r.s[1]; }
         uint32_t w0 = s0 | (kind << 16) | ((uint32_t)(r.s[0] >= 0 ? r.st[0] : 1) << 20);
         uint32_t w1 = s1 | ((uint32_t)(r.s[1] >= 0 ? r.st[1] : 1) << 16);
-        if (kind == 4 && r.s[1] < 0) fail(SMC_E_MODEL, "internal: general law with one reactant");
+
         L.any_explicit |= kind == 5;
         if (r.hill) w0 |= 0x80000000u;
         unsigned char* law = L.blob.data() + L.off_law + 16 * (size_t)j;   // {u0, u1, double c}
         std::memcpy(law, &w0, 4);
         std::memcpy(law + 4, &w1, 4);
-        std::memcpy(law + 8, &r.c, 8);
+        std::memcpy(law + 8, &c, 8);
         if (L.any_hill) {
             ((int32_t*)(L.blob.data() + L.off_hill_rep))[j] = r.hill ? r.rep : 0;
             ((double*)(L.blob.data() + L.off_hill_k))[j] = r.hill ? r.K : 1.0;

@@ -82,7 +82,9 @@ struct SmcTabs {
 // a_k(x) (readings R8/R9).  For order <= 2 the combinatorial count h is
 // formed in fp64 from the integer counts: x0, x0*x1 and x0*(x0-1) are single roundings
 // of the exact integer products (counts < 2^31, so the int64 product is exact), and
-// halving is exact, hence h equals (double)(int64 h) bit for bit; a = c * h.
+// halving is exact, hence h equals (double)(int64 h) bit for bit; a = c * h, and for a
+// homodimer (c/2) * fl(x(x-1)) = c * (fl(x(x-1))/2) as real numbers, so the fold of the
+// 1/2 into the table's rate gives the same double (reading R20).
 __device__ __forceinline__ double smc_law_tab(int k, const int* xs, const SmcTabs& T) {
     const SmcLaw L = T.law[k];
     const int kind = (int)((L.u0 >> 16) & 7u);
@@ -101,12 +103,9 @@ __device__ __forceinline__ double smc_law_tab(int k, const int* xs, const SmcTab
     } else
 #endif
     {
-        int xa = v0, xb = v1;
-        if (kind == 2) xb = max(v0 - 1, 0);
-        if (kind <= 1) xb = 1;
-        if (kind == 0) xa = 1;
-        h = __dmul_rn((double)xa, (double)xb);
-        if (kind == 2) h = __dmul_rn(h, 0.5);
+        // x[s0] * x[s1] with x[N] = 1 (kinds 0, 1, 3); kind 2: x * (x-1), the 1/2 folded into c
+        const int xb = (kind == 2) ? max(v0 - 1, 0) : v1;
+        h = __dmul_rn((double)v0, (double)xb);
     }
     double a = __dmul_rn(L.c, h);
 #if SMC_ANY_HILL
@@ -220,7 +219,7 @@ extern "C" __global__ void __launch_bounds__(768, 1) smc_ssa_tile(SmcParams P) {
             const bool init = want && !exhausted;
             if (init) {
                 traj = P.first + rel;
-                for (int s = tl; s < SMC_N; s += TW) xs[s] = T.x0[s];
+                for (int s = tl; s <= SMC_N; s += TW) xs[s] = T.x0[s];   // x[N] = 1
             }
             __syncwarp();
             if (init) {
@@ -284,8 +283,11 @@ extern "C" __global__ void __launch_bounds__(768, 1) smc_ssa_tile(SmcParams P) {
             // ---- two-level selection (Eq. 2b): group g by ballot on the scan ...
             const double target = __dmul_rn(U, A);
             const smc_u32 bg = (__ballot_sync(SMC_FULL, Pp > target) & tbits) >> (tile * TW);
-            const smc_u32 bp = (__ballot_sync(SMC_FULL, S > 0.0) & tbits) >> (tile * TW);
-            const int g = bg ? (__ffs(bg) - 1) : (bp ? 31 - __clz(bp) : 0);
+            int g = __ffs(bg) - 1;
+            if (__any_sync(SMC_FULL, bg == 0u)) {          // rounding: last group with a_j > 0 (R11)
+                const smc_u32 bp = (__ballot_sync(SMC_FULL, S > 0.0) & tbits) >> (tile * TW);
+                if (bg == 0u) g = bp ? 31 - __clz(bp) : 0;
+            }
             double base = __shfl_sync(SMC_FULL, Pp, (g + TW - 1) & (TW - 1), TW);
             if (g == 0) base = 0.0;
             // ... then the member inside group g: lane tl scans its chunk of SMC_CH elements
@@ -305,22 +307,23 @@ extern "C" __global__ void __launch_bounds__(768, 1) smc_ssa_tile(SmcParams P) {
             }
             double acc = __shfl_up_sync(SMC_FULL, ps, 1, TW);
             acc = (tl == 0) ? base : __dadd_rn(base, acc);
-            int hit = -1, lastpos = -1;
+            int hit = -1;
 #pragma unroll
             for (int c = 0; c < SMC_CH; ++c) {
                 acc = __dadd_rn(acc, av[c]);
                 if (hit < 0 && acc > target) hit = c;
-                if (av[c] > 0.0) lastpos = c;
             }
             const smc_u32 bh = (__ballot_sync(SMC_FULL, bg != 0 && hit >= 0) & tbits) >> (tile * TW);
-            const smc_u32 bl = (__ballot_sync(SMC_FULL, lastpos >= 0) & tbits) >> (tile * TW);
-            int jm;
-            if (bh) {
-                const int src = __ffs(bh) - 1;
-                jm = __shfl_sync(SMC_FULL, src * SMC_CH + hit, src, TW);
-            } else {                                     // rounding: last a_j > 0 (reading R11)
+            int jm = __shfl_sync(SMC_FULL, ((__ffs(bh) - 1) & (TW - 1)) * SMC_CH + hit, (__ffs(bh) - 1) & (TW - 1), TW);
+            if (__any_sync(SMC_FULL, bh == 0u)) {          // rounding: last a_j > 0 (reading R11)
+                int lastpos = -1;
+#pragma unroll
+                for (int c = 0; c < SMC_CH; ++c)
+                    if (av[c] > 0.0) lastpos = c;
+                const smc_u32 bl = (__ballot_sync(SMC_FULL, lastpos >= 0) & tbits) >> (tile * TW);
                 const int src = bl ? 31 - __clz(bl) : 0;
-                jm = __shfl_sync(SMC_FULL, src * SMC_CH + lastpos, src, TW);
+                const int jl = __shfl_sync(SMC_FULL, src * SMC_CH + lastpos, src, TW);
+                if (bh == 0u) jm = jl;
             }
             const int j = go ? g * SMC_GS + jm : 0;
 
