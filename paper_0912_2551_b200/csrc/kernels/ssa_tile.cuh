@@ -381,27 +381,30 @@ extern "C" __global__ void __launch_bounds__(768, 1) smc_ssa_tile(SmcParams P) {
                         }
                     }
                 } else {
-                    unsigned pre[TPW], off[TPW], tot = 0;
+                    // item b of the warp's concatenated dep lists belongs to tile u (prefix
+                    // search) and reads entry b + (d0_u - pre_u), fetched from tile u by one shuffle
+                    unsigned pre[TPW], tot = 0, mypre = 0;
 #pragma unroll
                     for (int u = 0; u < TPW; ++u) {
                         pre[u] = tot;
-                        off[u] = __shfl_sync(SMC_FULL, d0, u * TW);
+                        if (u == tile) mypre = tot;
                         tot += __shfl_sync(SMC_FULL, nd, u * TW);
                     }
-                    for (unsigned b = (unsigned)lane; b < tot; b += 32u) {
+                    const unsigned mydelta = d0 - mypre;
+                    for (unsigned b0 = 0; b0 < tot; b0 += 32u) {
+                        const unsigned b = b0 + (unsigned)lane;
                         int u = 0;
 #pragma unroll
                         for (int w = 1; w < TPW; ++w) u += (b >= pre[w]) ? 1 : 0;
-                        unsigned o = off[0], p0 = pre[0];
-#pragma unroll
-                        for (int w = 1; w < TPW; ++w)
-                            if (u == w) { o = off[w]; p0 = pre[w]; }
-                        int kk, slot;
-                        smc_dep_entry(T.dep[o + (b - p0)], kk, slot);
-                        double* at_u = (double*)(warp_base + (size_t)u * SMC_TILE_BYTES);
-                        const int* xs_u = (const int*)(at_u + SMC_GS * TW);
-                        at_u[slot] = smc_law_tab(kk, xs_u, T);
-                        touched |= 1u << (u * TW + smc_owner(slot));
+                        const unsigned delta = __shfl_sync(SMC_FULL, mydelta, u * TW);
+                        if (b < tot) {
+                            int kk, slot;
+                            smc_dep_entry(T.dep[b + delta], kk, slot);
+                            double* at_u = (double*)(warp_base + (size_t)u * SMC_TILE_BYTES);
+                            const int* xs_u = (const int*)(at_u + SMC_GS * TW);
+                            at_u[slot] = smc_law_tab(kk, xs_u, T);
+                            touched |= 1u << (u * TW + smc_owner(slot));
+                        }
                     }
                 }
             }
