@@ -505,7 +505,14 @@ TileLayout pack_tables(const Model& m) {
     // per-trajectory slice: a[GS*TW] (fp64) + x[NPAD] (int32), 16-byte aligned; with several
     // tiles per warp the slice is padded to 8*TW mod 128 bytes so that the TPW tiles of a
     // warp cover consecutive bank ranges (minimum wavefronts per warp access)
-    L.tile_bytes = align16((size_t)L.gs * L.tw * 8 + 4 * (size_t)L.n_pad);
+    // a layout (ssa_tile.cuh smc_slot): row layout (group l contiguous, odd row stride) or
+    // the XOR-swizzled column layout (SMC_ROWLAYOUT = 0)
+    // measured: row layout +2 % on C5 (CH = 1: the in-group read is one contiguous row),
+    // -3 % on C4 (CH = 4: stride-4 reads conflict 2-way); so rows only for CH = 1
+    L.row = L.ch == 1;
+    if (const char* e = std::getenv("SMC_ROWLAYOUT")) L.row = std::atoi(e) != 0;
+    L.gsp = L.row ? (L.gs | 1) : L.gs;
+    L.tile_bytes = align16((size_t)L.gsp * L.tw * 8 + 4 * (size_t)L.n_pad);
     if (L.tw < 16)      // TW lanes x 8 B per access: tiles of a warp cover consecutive bank ranges
         while (L.tile_bytes % 128 != (size_t)(8 * L.tw)) L.tile_bytes += 16;
     for (auto& r : m.R) {
@@ -600,7 +607,7 @@ TileLayout pack_tables(const Model& m) {
         doff[j] = (uint32_t)pos;
         for (int k : m.dep[(size_t)j]) {
             const int l = k / L.gs, mm = k % L.gs;       // owner lane, member (ssa_tile.cuh smc_slot)
-            const uint32_t slot = (uint32_t)(mm * L.tw + (l ^ ((mm / L.ch) % L.tw)));
+            const uint32_t slot = L.row ? (uint32_t)(l * L.gsp + mm) : (uint32_t)(mm * L.tw + (l ^ ((mm / L.ch) % L.tw)));
             if (L.dep16) dep16[pos++] = (uint16_t)k;
             else dep[pos++] = (uint32_t)k | (slot << 16);
         }
@@ -639,6 +646,7 @@ std::string generate_source(const Model& m, const Property& p, int variant, cons
             const double H = p.t_max > 0.0 ? p.t_max : p.horizon;
             o << "#define SMC_LIT_H " << dlit(H) << "\n#define SMC_LIT_NODES " << p.lnodes.size() << "\n";
         }
+        o << "#define SMC_ROWLAYOUT " << (tl->row ? 1 : 0) << "\n#define SMC_GSP " << tl->gsp << "\n";
         o << "#define SMC_TW " << tl->tw << "\n#define SMC_GS " << tl->gs << "\n#define SMC_CH " << tl->ch
           << "\n#define SMC_NPAD " << tl->n_pad << "\n";
         o << "#define SMC_OFF_X0 " << tl->off_x0 << "\n#define SMC_OFF_LAW " << tl->off_law

@@ -124,7 +124,13 @@ __device__ __forceinline__ double smc_law_tab(int k, const int* xs, const SmcTab
 #endif
 
 // smem slot of a(l, m), l = group (owner lane), m = member (SMC_CH is a power of two)
+#if SMC_ROWLAYOUT
+// row layout: group l is a contiguous row of SMC_GSP (odd) doubles, so the lanes of a tile
+// at the same member fall on distinct bank pairs and the group walk is immediate offsets
+__device__ __forceinline__ int smc_slot(int l, int m) { return l * SMC_GSP + m; }
+#else
 __device__ __forceinline__ int smc_slot(int l, int m) { return m * SMC_TW + (l ^ ((m / SMC_CH) % SMC_TW)); }
+#endif
 // dependency entry -> (reaction k, smem slot of a_k)
 __device__ __forceinline__ void smc_dep_entry(unsigned e, int& k, int& slot) {
 #if SMC_DEP16
@@ -137,11 +143,19 @@ __device__ __forceinline__ void smc_dep_entry(unsigned e, int& k, int& slot) {
 #endif
 }
 // owner lane of a slot (inverse of smc_slot)
+#if SMC_ROWLAYOUT
+__device__ __forceinline__ int smc_owner(int slot) { return slot / SMC_GSP; }
+#else
 __device__ __forceinline__ int smc_owner(int slot) { return (slot % SMC_TW) ^ ((slot / SMC_TW / SMC_CH) % SMC_TW); }
+#endif
 
 // Group sum of lane l: two interleaved partial sums (even / odd members, each left to
 // right), then added -- a fixed order (reading R12) with half the dependent-add chain.
 __device__ __forceinline__ double smc_group_sum(const double* at, int l) {
+#if SMC_ROWLAYOUT
+    at += l * SMC_GSP;                        // row of group l: members at immediate offsets
+    l = 0;
+#endif
     double se = at[smc_slot(l, 0)];
     if (SMC_GS == 1) return se;
     double so = at[smc_slot(l, 1)];
@@ -189,7 +203,7 @@ extern "C" __global__ void __launch_bounds__(768, 1) smc_ssa_tile(SmcParams P) {
 #endif
     unsigned char* const warp_base = smem + SMC_TAB_BYTES + (size_t)warp * TPW * SMC_TILE_BYTES;
     double* at = (double*)(warp_base + (size_t)tile * SMC_TILE_BYTES);
-    int* xs = (int*)(at + SMC_GS * TW);
+    int* xs = (int*)(at + SMC_GSP * TW);
 
     // ---- per-tile trajectory state (replicated in the tile's lanes)
     bool act = false, exhausted = false;
@@ -401,7 +415,7 @@ extern "C" __global__ void __launch_bounds__(768, 1) smc_ssa_tile(SmcParams P) {
                             int kk, slot;
                             smc_dep_entry(T.dep[b + delta], kk, slot);
                             double* at_u = (double*)(warp_base + (size_t)u * SMC_TILE_BYTES);
-                            const int* xs_u = (const int*)(at_u + SMC_GS * TW);
+                            const int* xs_u = (const int*)(at_u + SMC_GSP * TW);
                             at_u[slot] = smc_law_tab(kk, xs_u, T);
                             touched |= 1u << (u * TW + smc_owner(slot));
                         }

@@ -144,6 +144,8 @@ std::unique_ptr<Property> compile_property(const Model& m, const std::string& te
 struct TileLayout {               // packed model tables (variant 2), byte offsets
     int tw = 32;                  // lanes per trajectory tile
     int gs = 0;                   // reactions per lane group
+    int gsp = 0;                  // row stride of a group in the row layout (odd), else gs
+    bool row = true;              // row layout of a (ssa_tile.cuh smc_slot)
     int ch = 0;                   // level-2 chunk per lane
     int n_pad = 0;
     size_t tile_bytes = 0;        // smem per trajectory
