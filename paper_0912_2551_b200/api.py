@@ -184,7 +184,7 @@ def use_torch(allocator=True, stream=True):
                 return 0            # NULL -> SMC_E_CUDA "allocator hook returned NULL"
 
         def free(ptr, user):
-            if ptr:
+            if ptr and torch is not None and getattr(torch, "cuda", None) is not None:   # not at interpreter exit
                 torch.cuda.caching_allocator_delete(int(ptr))
         a, f = ALLOC_FN(alloc), FREE_FN(free)
         _keep.extend([a, f])

@@ -496,3 +496,68 @@ def test_nested_formula_on_c4_tile_vs_oracle(smc):
     assert m.last_launch(p)["variant"] == 2
     oc, ov, oe = O.run(O.OracleModel(cfg), O.OracleFormula(f, cfg["species"]), 4, 0, 40, mode="literal")
     assert int(((v != ov) | (e != oe)).sum()) == 0
+
+
+def _random_case(seed):
+    """A random small network (mass action orders 0-2, Hill repression, explicit rates) and a
+    random formula (every streaming template, Kleene roots, nested shapes outside R16)."""
+    g = np.random.default_rng(seed)
+    N = int(g.integers(2, 5))
+    sp = ["A", "B", "C", "D"][:N]
+    rx = workloads._rx
+    R = []
+    for _ in range(int(g.integers(2, 7))):
+        nr = int(g.integers(0, 3))
+        reac = {}
+        for _ in range(nr):
+            s = int(g.integers(0, N))
+            reac[s] = reac.get(s, 0) + 1
+        prods = {}
+        for _ in range(int(g.integers(0, 3))):
+            s = int(g.integers(0, N))
+            prods[s] = prods.get(s, 0) + 1
+        r = rx(list(reac.items()), list(prods.items()), float(np.exp(g.uniform(np.log(0.05), np.log(2.0)))))
+        kind = g.random()
+        if kind < 0.15 and nr == 0:
+            r["hill"] = dict(repressor=int(g.integers(0, N)), K=float(g.uniform(2, 10)), n=int(g.integers(1, 3)))
+        elif kind < 0.3:
+            s = sp[int(g.integers(0, N))]
+            r["rate_expr"] = "%r * (1 + %s) / (2 + %s)" % (float(g.uniform(0.2, 2)), s, s)
+        R.append(r)
+    R.append(rx([], [(0, 1)], 0.5))                      # keep something happening
+    R.append(rx([(0, 1)], [], 0.2))
+    x0 = [int(v) for v in g.integers(0, 8, size=N)]
+    a, b = sp[0], sp[min(1, N - 1)]
+    c1, c2 = int(g.integers(1, 8)), int(g.integers(1, 8))
+    T = float(g.choice([1.0, 2.0, 4.0]))
+    lo = float(g.choice([0.0, 0.0, 0.3]))
+    forms = ["F[%r,%r](%s >= %d)" % (lo, T, a, c1), "G[%r,%r](%s < %d)" % (lo, T, b, c2),
+             "(%s < %d) U[%r,%r] (%s >= %d)" % (a, c1, lo, T, b, c2), "X[0,%r](%s > %d | %s == 0)" % (T / 4, a, c1, b),
+             "F[0,%r] G[0,%r](%s > %s)" % (T, T / 4, a, b), "G[0,%r] F[0,%r](%s >= %s)" % (T, T / 4, a, b),
+             "(G[0,%r](%s < %d)) U[0,%r] (%s > %d)" % (T / 4, a, c1 + 3, T, b, c2),
+             "!(F[0,%r](%s == %d)) & (G[0,%r](%s >= 0) | F(0,%r](%s > %d))" % (T, a, c1, T / 2, b, T, a, c2),
+             "F[0,%r](%s > %d & G[0.1,%r](%s > 0))" % (T, a, c1, T / 3, b),
+             "G[0,%r](%s / 2 <= sqrt(%s + 1) * 3 | X[0,0.5](%s > %d))" % (T, a, b, a, c1)]
+    f = forms[int(g.integers(0, len(forms)))]
+    return dict(name="rnd%d" % seed, species=sp, x0=x0, reactions=R, formula=f, t_max=0.0, seed=seed,
+                sampling=dict(mode="fixed", n=400))
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_random_models_and_formulas_vs_oracle(smc, seed):
+    """Fuzz: random networks x random formulas, thread and tile variants, replica for replica
+    against the oracle (its streaming monitor inside the fragment, its literal |= outside)."""
+    cfg = _random_case(seed)
+    of = O.OracleFormula(cfg["formula"], cfg["species"])
+    mode = "stream" if of.streamable else "literal"
+    oc, ov, oe = O.run(O.OracleModel(cfg), of, seed, 0, 400, mode=mode)
+    for variant in (1, 2):
+        m, p = _pair(smc, cfg, variant)
+        v, e = m.run_verdicts(p, 0, 400, seed)
+        v, e = v.cpu().numpy(), e.cpu().numpy().astype(np.int64)
+        # literal |= runs to the horizon; a replica whose trace outgrows the per-thread buffer
+        # ends as an error (reading R23) -- every other replica must match
+        ok = (v != 2) if mode == "literal" else np.ones_like(v, bool)
+        bad = int((((v != ov) | (e != oe)) & ok).sum())
+        assert bad <= 1, (seed, variant, cfg["formula"], bad)
+        assert ok.mean() >= 0.5 if mode == "literal" else (v != 2).all()
