@@ -182,9 +182,6 @@ struct Kernel {
 std::shared_ptr<Kernel> get_kernel(const std::string& source, const char* entry);
 
 // --------------------------------------------------------------- runtime ---
-struct LaunchRecord {
-    smc_launch_info info{};
-};
 struct Hooks {
     void* (*alloc)(size_t, void*) = nullptr;
     void (*free_)(void*, void*) = nullptr;
@@ -196,9 +193,6 @@ struct Hooks {
 };
 Hooks& hooks();
 
-// counts of one shard slice [lo, hi) (device kernel), no allreduce
-int run_slice(Model& m, const Property& p, uint64_t seed, uint64_t lo, uint64_t hi, smc_counts* local,
-              uint8_t* dev_verdict, int32_t* dev_events);
 // global counts of round range [base, base+n): shard + allreduce
 int run_round(Model& m, const Property& p, uint64_t seed, uint64_t base, uint64_t n, smc_counts* out);
 
