@@ -106,7 +106,7 @@ struct MonGen {
             if (lf.kind == LeafKind::FG || lf.kind == LeafKind::GF) o << "    bool rs" << i << "_set; double rs" << i << ";\n";
             if (lf.kind == LeafKind::GU) o << "    bool w" << i << "; double D" << i << ";\n";
         }
-        o << "    __device__ __forceinline__ void bind(const SmcParams&, smc_u64) {}\n";
+        o << "    __device__ __forceinline__ void bind(const SmcParams&, smc_u64, unsigned, int) {}\n";
         // init
         o << "    __device__ __forceinline__ void init() {\n";
         for (size_t i = 0; i < L; ++i) {
@@ -315,32 +315,42 @@ std::string literal_code(const Property& P) {
 }
 
 // Recording monitor (tile variant, formulas outside R16; reading R23): the same interface
-// as the template monitors; it buffers (t_k, tau_k, atom mask_k) of the tile's replica and,
-// once the trace passes the horizon or is absorbed, evaluates |= with smc_lit_eval.  All
-// lanes of a tile hold and write identical values.
+// as the template monitors; the tile's first lane buffers (t_k, tau_k, atom mask_k) of the
+// tile's replica and, once the trace passes the horizon or is absorbed, evaluates |= with
+// smc_lit_eval; the verdict reaches the other lanes by a shuffle (no shared writes).
 std::string recording_monitor(const Property& P) {
     std::ostringstream o;
     o << "struct SmcMon {   // recording monitor for: " << P.text << "\n"
          "    double* tb; double* ub; unsigned* mb; unsigned char* vb; long long cap, last; int res;\n"
-         "    __device__ __forceinline__ void bind(const SmcParams& Q, smc_u64 slot) {\n"
-         "        cap = (long long)Q.lit_cap;\n"
+         "    unsigned tmask; int leader;   // the tile's lanes; the tile's first lane writes and evaluates\n"
+         "    __device__ __forceinline__ void bind(const SmcParams& Q, smc_u64 slot, unsigned mask, int lead) {\n"
+         "        cap = (long long)Q.lit_cap; tmask = mask; leader = lead;\n"
          "        tb = Q.lit_t + slot * (smc_u64)cap; ub = Q.lit_tau + slot * (smc_u64)cap;\n"
          "        mb = Q.lit_mask + slot * (smc_u64)cap; vb = Q.lit_val + slot * (smc_u64)cap * SMC_LIT_NODES;\n"
+         "    }\n"
+         "    __device__ __forceinline__ bool lead() const { return (int)(threadIdx.x & 31u) == leader; }\n"
+         "    __device__ __forceinline__ int eval(long long n, bool absorbed) {\n"
+         "        int r = 0;\n"
+         "        __syncwarp(tmask);                          // the leader's trace writes are visible\n"
+         "        if (lead()) r = smc_lit_eval(tb, ub, mb, vb, n, absorbed, cap) == 1 ? 1 : 0;\n"
+         "        return __shfl_sync(tmask, r, leader);\n"
          "    }\n"
          "    __device__ __forceinline__ void init() { res = -1; last = 0; }\n"
          "    template <class XA> __device__ __forceinline__ void enter(smc_u32 k, double t, double tp, const XA& x) {\n"
          "        (void)tp;\n"
          "        if (res >= 0) return;\n"
          "        if ((long long)k >= cap - 1) { res = 2; return; }   // trace buffer full: replica error\n"
-         "        tb[k] = t; mb[k] = smc_lit_mask(x); last = (long long)k;\n"
+         "        const unsigned mk = smc_lit_mask(x);\n"
+         "        if (lead()) { tb[k] = t; mb[k] = mk; }\n"
+         "        last = (long long)k;\n"
          "    }\n"
          "    __device__ __forceinline__ void advance(smc_u32 k, double tn, double tau) {\n"
          "        if (res >= 0) return;\n"
-         "        ub[k] = tau;\n"
-         "        if (tn > SMC_LIT_H) res = smc_lit_eval(tb, ub, mb, vb, (long long)k, false, cap) == 1 ? 1 : 0;\n"
+         "        if (lead()) ub[k] = tau;\n"
+         "        if (tn > SMC_LIT_H) res = eval((long long)k, false);\n"
          "    }\n"
          "    __device__ __forceinline__ void absorb() {\n"
-         "        if (res < 0) res = smc_lit_eval(tb, ub, mb, vb, last, true, cap) == 1 ? 1 : 0;\n"
+         "        if (res < 0) res = eval(last, true);\n"
          "    }\n"
          "    __device__ __forceinline__ void timeout() {}\n"
          "    __device__ __forceinline__ int verdict() const { return res; }\n"

@@ -212,7 +212,8 @@ extern "C" __global__ void __launch_bounds__(768, 1) smc_ssa_tile(SmcParams P) {
     smc_u32 k = 0, kb = 0;
     double Eb = 0.0, Ub = 0.0;          // draw of step kb + tl
     SmcMon mon;
-    mon.bind(P, ((smc_u64)blockIdx.x * (blockDim.x >> 5) + (smc_u64)warp) * TPW + (smc_u64)tile);   // trace slot (R23)
+    mon.bind(P, ((smc_u64)blockIdx.x * (blockDim.x >> 5) + (smc_u64)warp) * TPW + (smc_u64)tile, tbits,
+             tile * TW);                                   // trace slot, lanes, leader (R23)
     smc_u32 c_true = 0, c_false = 0, c_err = 0;   // tile leader
     smc_i64 c_ev = 0;
 
