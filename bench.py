@@ -365,7 +365,8 @@ def main():
         torch.cuda.synchronize()
         e2e_ms += (time.perf_counter() - t0) * 1e3
         inf2 = m2.last_launch(p2)
-        h2d = int(inf2["table_bytes"]) + 72 * inf2["launches"]     # tables + kernel parameters
+        # tables + kernel parameters (SmcParams 112 B per SSA launch, <= 96 B per count / Wilson launch)
+        h2d = int(inf2["table_bytes"]) + 112 * inf2["launches"] + 96 * inf2["aux_launches"]
         d2h = 32 * max(1, inf2["launches"])                        # int64[4] counts per round
         del p2, m2
     e2e = {"value": e2e_events / (e2e_ms / 1e3), "unit": "events/s", "h2d_bytes_per_step": h2d,
