@@ -561,3 +561,58 @@ def test_random_models_and_formulas_vs_oracle(smc, seed):
         bad = int((((v != ov) | (e != oe)) & ok).sum())
         assert bad <= 1, (seed, variant, cfg["formula"], bad)
         assert ok.mean() >= 0.5 if mode == "literal" else (v != 2).all()
+
+
+def _random_large_case(seed):
+    """A random tile-only network (N > 32 or M > 32) with every law shape: mass action of
+    order 0-4, Hill repression, explicit rates, null reactions; template formulas."""
+    g = np.random.default_rng(1000 + seed)
+    N = int(g.integers(33, 45))
+    M = int(g.integers(40, 80))
+    sp = ["S%d" % i for i in range(N)]
+    rx = workloads._rx
+    R = []
+    for _ in range(M):
+        reac = {}
+        for _ in range(int(g.integers(0, 3))):
+            s = int(g.integers(0, N))
+            reac[s] = min(2, reac.get(s, 0) + 1)
+        prods = {}
+        for _ in range(int(g.integers(0, 3))):
+            s = int(g.integers(0, N))
+            prods[s] = min(2, prods.get(s, 0) + 1)
+        r = rx(list(reac.items()), list(prods.items()), float(np.exp(g.uniform(np.log(0.01), np.log(1.0)))))
+        u = g.random()
+        if u < 0.1 and not reac:
+            r["hill"] = dict(repressor=int(g.integers(0, N)), K=float(g.uniform(5, 50)), n=int(g.integers(1, 4)))
+        elif u < 0.2:
+            s = sp[int(g.integers(0, N))]
+            r["rate_expr"] = "%r * %s / (10 + %s) + 0.01" % (float(g.uniform(0.1, 2)), s, s)
+        R.append(r)
+    x0 = [int(v) for v in g.integers(0, 40, size=N)]
+    a, b = sp[0], sp[1]
+    forms = ["F[0,3](%s > %s + 5)" % (a, b), "G[0,2](%s <= %s + 30)" % (a, b), "(%s < 50) U[0,3] (%s > 45)" % (a, b),
+             "F[0,3] G[0,0.5](%s > %s)" % (a, b), "(G[0,0.5](%s < 60)) U[0,3] (%s >= 41)" % (a, b),
+             "X[0,0.2](%s != %s) | F[0,1](%s == 0)" % (a, b, b)]
+    return dict(name="big%d" % seed, species=sp, x0=x0, reactions=R, formula=forms[seed % len(forms)], t_max=0.0,
+                seed=seed, sampling=dict(mode="fixed", n=300))
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_large_networks_vs_oracle(smc, seed):
+    """Fuzz of the tile kernel: random tile-only networks (every law shape) x template
+    formulas, every tile width, replica for replica against the oracle's streaming monitor."""
+    cfg = _random_large_case(seed)
+    oc, ov, oe = O.run(O.OracleModel(cfg), O.OracleFormula(cfg["formula"], cfg["species"]), seed, 0, 300)
+    for width in ("8", "32") if seed % 2 else ("4", "16"):
+        os_env = __import__("os").environ
+        os_env["SMC_TILE_WIDTH"] = width
+        try:
+            m, p = _pair(smc, cfg)
+            v, e = m.run_verdicts(p, 0, 300, seed)
+        finally:
+            del os_env["SMC_TILE_WIDTH"]
+        v, e = v.cpu().numpy(), e.cpu().numpy().astype(np.int64)
+        assert m.last_launch(p)["variant"] == 2
+        bad = int(((v != ov) | (e != oe)).sum())
+        assert bad <= 1, (seed, width, cfg["formula"], bad, oc)
