@@ -71,9 +71,9 @@ def model_stats(cfg):
     return [len(d) for d in deps], [len(c) for c in changes], sum(hill) / M
 
 
-def measured_traffic(workload, kernel):
-    """DRAM bytes (read + write) per launch of the SSA kernel from the committed ncu
-    --set full capture summary (profiles/traffic_<round>.json, scripts/ncu_traffic.py)."""
+def measured_profile(workload, kernel):
+    """The committed ncu --set full summary of the SSA kernel (profiles/traffic_<round>.json,
+    scripts/ncu_traffic.py): DRAM bytes per launch, issue and shared-memory pipe utilisation."""
     import glob
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", "traffic_r*.json")))
     if not files:
@@ -81,7 +81,7 @@ def measured_traffic(workload, kernel):
     d = json.load(open(files[-1])).get(workload)
     if not d or d.get("kernel") != kernel:
         return None, None
-    return d["dram_bytes_per_launch"], "%s: %s (%s)" % (os.path.basename(files[-1]), d["capture"], d["note"])
+    return d, "%s: %s (%s)" % (os.path.basename(files[-1]), d["capture"], d["note"])
 
 
 # ------------------------------------------------------------------- clocks
@@ -331,7 +331,8 @@ def main():
     per_gpu_events = events / world
     achieved = sim_events * ipe / 32.0 / (tot_kernel_ms / 1e3) / 1e9
     achieved_counted = per_gpu_events * ipe / 32.0 / (tot_kernel_ms / 1e3) / 1e9
-    traffic, traffic_src = measured_traffic(cfg["name"], "smc_ssa_%s" % ("thread" if info["variant"] == 1 else "tile"))
+    prof, traffic_src = measured_profile(cfg["name"], "smc_ssa_%s" % ("thread" if info["variant"] == 1 else "tile"))
+    traffic = prof["dram_bytes_per_launch"] if prof else None
     roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Gwarp-inst/s", "frac": achieved / peak,
                 "traffic": traffic, "traffic_source": traffic_src,
                 "algorithmic_bytes_per_launch": "tables once per CTA + 64 B control block (no per-event HBM traffic)",
@@ -340,6 +341,11 @@ def main():
                 "simulated_events_per_step": sim_events / args.steps,
                 "counted_events_per_step": per_gpu_events / args.steps,
                 "counted_frac": achieved_counted / peak,
+                # measured co-limits from the committed ncu capture: the tile kernels run the
+                # shared-memory pipe at ~70-75 % of its wavefront peak
+                "ncu_issue_active_pct": prof.get("issue_active_pct") if prof else None,
+                "ncu_smem_wavefront_pct": prof.get("smem_wavefront_pct") if prof else None,
+                "ncu_smem_wavefront_excess": prof.get("smem_wavefront_excess") if prof else None,
                 "kernel_share_of_step": tot_kernel_ms / tot_ms,
                 "peak_source": "148 SM x 4 SMSP x 1 warp-inst/clk x sm_max_mhz (MEASURED_PEAKS.json)"}
 
