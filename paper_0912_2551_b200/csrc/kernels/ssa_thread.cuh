@@ -12,9 +12,13 @@
 //
 // The random draw of step k+1 (Philox + log) does not depend on the state, so
 // it is issued at the top of step k, in the same basic block as the a0 sum,
-// and overlaps the state-dependent chain of step k.
+// and overlaps the state-dependent chain of step k (SMC_PIPE2: the Philox block
+// of step k+2 and the u53 + log of step k+1 as two independent chains).
+// After a reaction all M <= 32 laws are recomputed straight-line: the lanes of a
+// warp fire different reactions, so a masked dependency update would execute
+// (nearly) every law anyway; the values are identical.
 //
-// Generated hooks (codegen.cpp): SMC_N, SMC_M, SMC_BLOCK, SMC_TMAX,
+// Generated hooks (codegen.cpp): SMC_N, SMC_M, SMC_BLOCK, SMC_MINB, SMC_TMAX, SMC_PIPE2,
 //   smc_init_x(x), smc_laws_all(a, x, H), smc_apply(j, x) -> ok,
 //   smc_update(j, a, x, H), smc_last_positive(a), struct SmcMon.
 //   H = P.tables: tabulated Hill propensities (zero-order Hill laws).
@@ -25,7 +29,7 @@
 //   tau = -log(u1)/a0, t' = t + tau   step 3, Eq. 2a
 //   monitor.advance(t')               close windows t' passes (may decide)
 //   j = min{j : sum_{i<=j} a_i > u2 a0}  step 2, Eq. 2b
-//   x += v_j; a_k = law_k(x), k in dep(j); t = t'   step 4
+//   x += v_j; a_k = law_k(x) (all k); t = t'          step 4
 //   monitor.enter(t, x)               (may decide)
 
 #ifndef SMC_PIPE2

@@ -8,10 +8,11 @@
 //   TPW = 32/SMC_TW trajectories in lock step.  x[N] and a[M] live in the tile's
 //   shared-memory slice; lane l of a tile owns the contiguous reaction group
 //   [l*GS, (l+1)*GS) and keeps its group sum S_l in a register.
-//   a(l, m) is stored at m*TW + (l ^ ((m / CH) % TW)): the group walk of the
-//   resum (all lanes at the same m) and the chunked in-group selection (lane c
-//   reads m = c*CH + i) are both bank-conflict free; tile slices are padded so
-//   the TPW tiles of a warp cover consecutive bank ranges.
+//   For CH > 1, a(l, m) is stored at m*TW + (l ^ ((m / CH) % TW)): the group walk
+//   of the resum (all lanes at the same m) and the chunked in-group selection
+//   (lane c reads m = c*CH + i) are both bank-conflict free; for CH = 1 in rows
+//   l*GSP + m (odd GSP: SMC_ROWLAYOUT).  Tile slices are padded so the TPW tiles of
+//   a warp cover consecutive bank ranges; x[N] = 1 is a constant count slot.
 // * Per event: a0 = inclusive tile scan of the TW group sums (fixed order),
 //   two-level selection (group by ballot on the scan, member by chunked scan
 //   inside the group), x += v_j by <= 4 lanes, then the dependency work of ALL
@@ -21,14 +22,17 @@
 // * Propensity laws are evaluated in fp64 on integer-valued doubles; for
 //   reaction order <= 2 this is exactly (double)h with h the int64 combinatorial
 //   count (see smc_law_tab), order 3-4 takes the int64 path.
+// * Formulas outside the streaming templates use a generated recording monitor
+//   (buffered trace + literal |= at the horizon, reading R23) through the same
+//   SmcMon interface (bind / init / enter / advance / absorb / timeout / verdict).
 // * The Philox + log draws of the next SMC_TW steps of every tile are computed
 //   together at the start of each burst of SMC_TW events, one draw per lane
 //   (state-independent, so batching them is exact).
 //
 // Generated hooks (codegen.cpp): SMC_N, SMC_M, SMC_TW, SMC_GS, SMC_CH, SMC_NPAD,
 //   SMC_OFF_*, SMC_TAB_BYTES, SMC_TILE_BYTES, SMC_ANY_HILL, SMC_ANY_GENERAL, SMC_DEP16,
-//   SMC_ANY_EXPLICIT (+ smc_explicit), SMC_DEPSP,
-//   SMC_TMAX, SmcMon.
+//   SMC_ANY_EXPLICIT (+ smc_explicit), SMC_DEPSP, SMC_ROWLAYOUT, SMC_GSP,
+//   SMC_TMAX, SmcMon (+ SMC_LIT_H, SMC_LIT_NODES, smc_lit_* for the recording monitor).
 
 __device__ __forceinline__ void smc_mbar_init(unsigned long long* bar, unsigned count) {
     const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
