@@ -555,14 +555,22 @@ TileLayout pack_tables(const Model& m) {
     if (const char* e = std::getenv("SMC_DEPSP")) L.depsp = std::atoi(e) != 0 && L.tw == 32;
     L.dep16 = L.depsp || M > 512;
     if (const char* e = std::getenv("SMC_DEP16")) L.dep16 = L.depsp || std::atoi(e) != 0;
+    // "fat" 16-byte entries {k | slot << 16, law meta, rate} for the reaction-indexed CSR:
+    // the dependency walk reads contiguous entries instead of random law-table rows (the
+    // law-table gather was 24 % of C4's shared-memory wavefronts, 70 % of them bank-conflict
+    // excess)
+    L.fatdep = !L.dep16 && N <= 4095;
+    if (const char* e = std::getenv("SMC_FATDEP")) L.fatdep = std::atoi(e) != 0 && !L.dep16 && N <= 4095;
     L.off_dep_off = o; o = align16(o + 4 * ((size_t)(L.depsp ? N : M) + 1));
-    L.off_dep = o; o = align16(o + (L.dep16 ? 2 : 4) * (L.depsp ? nnz_sp : nnz));
+    L.off_dep = o; o = align16(o + (L.fatdep ? 16 : (L.dep16 ? 2 : 4)) * (L.depsp ? nnz_sp : nnz));
     L.bytes = o;
     L.blob.assign(L.bytes, 0);
     auto* x0 = (int32_t*)(L.blob.data() + L.off_x0);
     for (int s = 0; s < N; ++s) x0[s] = m.x0[(size_t)s];
     x0[N] = 1;
     auto* chg = (uint16_t*)(L.blob.data() + L.off_chg);
+    std::vector<uint32_t> fat_meta((size_t)M);          // s0 | s1 << 12 | kind << 24 | st0==2 << 27 | st1==2 << 28 | hill << 31
+    std::vector<double> fat_c((size_t)M);
     for (int j = 0; j < M; ++j) {
         const Reaction& r = m.R[(size_t)j];
         // law kind (ssa_tile.cuh smc_law_tab): h = x[s0] * x[s1] with x[N] = 1 for kinds
@@ -584,6 +592,9 @@ TileLayout pack_tables(const Model& m) {
 
         L.any_explicit |= kind == 5;
         if (r.hill) w0 |= 0x80000000u;
+        fat_meta[(size_t)j] = s0 | (s1 << 12) | (kind << 24) | ((uint32_t)(r.s[0] >= 0 && r.st[0] == 2) << 27) |
+                              ((uint32_t)(r.s[1] >= 0 && r.st[1] == 2) << 28) | ((uint32_t)r.hill << 31);
+        fat_c[(size_t)j] = c;
         unsigned char* law = L.blob.data() + L.off_law + 16 * (size_t)j;   // {u0, u1, double c}
         std::memcpy(law, &w0, 4);
         std::memcpy(law + 4, &w1, 4);
@@ -618,7 +629,13 @@ TileLayout pack_tables(const Model& m) {
         for (int k : m.dep[(size_t)j]) {
             const int l = k / L.gs, mm = k % L.gs;       // owner lane, member (ssa_tile.cuh smc_slot)
             const uint32_t slot = L.row ? (uint32_t)(l * L.gsp + mm) : (uint32_t)(mm * L.tw + (l ^ ((mm / L.ch) % L.tw)));
-            if (L.dep16) dep16[pos++] = (uint16_t)k;
+            if (L.fatdep) {
+                unsigned char* fe = L.blob.data() + L.off_dep + 16 * pos++;
+                const uint32_t ks = (uint32_t)k | (slot << 16);
+                std::memcpy(fe, &ks, 4);
+                std::memcpy(fe + 4, &fat_meta[(size_t)k], 4);
+                std::memcpy(fe + 8, &fat_c[(size_t)k], 8);
+            } else if (L.dep16) dep16[pos++] = (uint16_t)k;
             else dep[pos++] = (uint32_t)k | (slot << 16);
         }
     }
@@ -669,6 +686,7 @@ std::string generate_source(const Model& m, const Property& p, int variant, cons
         o << "#define SMC_ANY_GENERAL " << (tl->any_general ? 1 : 0) << "\n";
         o << "#define SMC_DEP16 " << (tl->dep16 ? 1 : 0) << "\n";
         o << "#define SMC_DEPSP " << (tl->depsp ? 1 : 0) << "\n";
+        o << "#define SMC_FATDEP " << (tl->fatdep ? 1 : 0) << "\n";
         o << "#define SMC_ANY_EXPLICIT " << (tl->any_explicit ? 1 : 0) << "\n";
         if (const char* e = std::getenv("SMC_FLAT")) o << "#define SMC_FLAT " << std::atoi(e) << "\n";
     }

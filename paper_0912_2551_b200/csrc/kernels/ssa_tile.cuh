@@ -31,7 +31,7 @@
 //
 // Generated hooks (codegen.cpp): SMC_N, SMC_M, SMC_TW, SMC_GS, SMC_CH, SMC_NPAD,
 //   SMC_OFF_*, SMC_TAB_BYTES, SMC_TILE_BYTES, SMC_ANY_HILL, SMC_ANY_GENERAL, SMC_DEP16,
-//   SMC_ANY_EXPLICIT (+ smc_explicit), SMC_DEPSP, SMC_ROWLAYOUT, SMC_GSP,
+//   SMC_ANY_EXPLICIT (+ smc_explicit), SMC_DEPSP, SMC_FATDEP, SMC_ROWLAYOUT, SMC_GSP,
 //   SMC_TMAX, SmcMon (+ SMC_LIT_H, SMC_LIT_NODES, smc_lit_* for the recording monitor).
 
 __device__ __forceinline__ void smc_mbar_init(unsigned long long* bar, unsigned count) {
@@ -122,6 +122,46 @@ __device__ __forceinline__ double smc_law_tab(int k, const int* xs, const SmcTab
 #endif
     return a;
 }
+
+// a_k(x) from a fat dependency entry: meta = s0 | s1 << 12 | kind << 24 | (st0 == 2) << 27 |
+// (st1 == 2) << 28 | hill << 31, c the (folded) rate -- the same arithmetic as smc_law_tab
+__device__ __forceinline__ double smc_law_meta(unsigned meta, double c, int k, const int* xs, const SmcTabs& T) {
+    const int kind = (int)((meta >> 24) & 7u);
+#if SMC_ANY_EXPLICIT
+    if (kind == 5) return smc_explicit(k, xs);
+#endif
+    const int v0 = xs[meta & 0xFFFu];
+    const int v1 = xs[(meta >> 12) & 0xFFFu];
+    double h;
+#if SMC_ANY_GENERAL
+    if (kind == 4) {
+        const smc_i64 y0 = v0, y1 = v1;
+        const smc_i64 h0 = ((meta >> 27) & 1u) ? (y0 * (y0 - 1)) / 2 : y0;
+        const smc_i64 h1 = ((meta >> 28) & 1u) ? (y1 * (y1 - 1)) / 2 : y1;
+        h = (double)(h0 * h1);
+    } else
+#endif
+    {
+        const int xb = (kind == 2) ? max(v0 - 1, 0) : v1;
+        h = __dmul_rn((double)v0, (double)xb);
+    }
+    double a = __dmul_rn(c, h);
+#if SMC_ANY_HILL
+    if ((int)meta < 0) {
+        const double q = __ddiv_rn((double)xs[T.hill_rep[k]], T.hill_k[k]);
+        double qn = q;
+        for (int i = 1; i < T.hill_n[k]; ++i) qn = __dmul_rn(qn, q);
+        a = __ddiv_rn(a, __dadd_rn(1.0, qn));
+    }
+#endif
+    (void)k;
+    return a;
+}
+struct __align__(16) SmcDepFat {
+    unsigned ks;      // k | slot << 16
+    unsigned meta;
+    double c;
+};
 
 #ifndef SMC_FLAT
 #define SMC_FLAT 1      // dependency work of all tiles of a warp flattened over the 32 lanes
@@ -393,9 +433,15 @@ extern "C" __global__ void __launch_bounds__(768, 1) smc_ssa_tile(SmcParams P) {
                     const smc_u32 tb = (TPW == 1) ? 0u : (smc_u32)(tile * TW);
                     for (unsigned b = (unsigned)tl; __any_sync(SMC_FULL, b < nd); b += (unsigned)TW) {
                         if (b < nd) {
+#if SMC_FATDEP
+                            const SmcDepFat D = ((const SmcDepFat*)T.dep)[d0 + b];
+                            const int slot = (int)(D.ks >> 16);
+                            at[slot] = smc_law_meta(D.meta, D.c, (int)(D.ks & 0xFFFFu), xs, T);
+#else
                             int kk, slot;
                             smc_dep_entry(T.dep[d0 + b], kk, slot);
                             at[slot] = smc_law_tab(kk, xs, T);
+#endif
                             touched |= 1u << (tb + (smc_u32)smc_owner(slot));
                         }
                     }
@@ -417,11 +463,17 @@ extern "C" __global__ void __launch_bounds__(768, 1) smc_ssa_tile(SmcParams P) {
                         for (int w = 1; w < TPW; ++w) u += (b >= pre[w]) ? 1 : 0;
                         const unsigned delta = __shfl_sync(SMC_FULL, mydelta, u * TW);
                         if (b < tot) {
-                            int kk, slot;
-                            smc_dep_entry(T.dep[b + delta], kk, slot);
                             double* at_u = (double*)(warp_base + (size_t)u * SMC_TILE_BYTES);
                             const int* xs_u = (const int*)(at_u + SMC_GSP * TW);
+#if SMC_FATDEP
+                            const SmcDepFat D = ((const SmcDepFat*)T.dep)[b + delta];
+                            const int slot = (int)(D.ks >> 16);
+                            at_u[slot] = smc_law_meta(D.meta, D.c, (int)(D.ks & 0xFFFFu), xs_u, T);
+#else
+                            int kk, slot;
+                            smc_dep_entry(T.dep[b + delta], kk, slot);
                             at_u[slot] = smc_law_tab(kk, xs_u, T);
+#endif
                             touched |= 1u << (u * TW + smc_owner(slot));
                         }
                     }

@@ -155,6 +155,7 @@ struct TileLayout {               // packed model tables (variant 2), byte offse
     bool any_general = false;     // a reaction of order 3-4 (int64 law path)
     bool dep16 = false;           // 2-byte dependency entries (k only)
     bool depsp = false;           // species-indexed reader CSR instead of dep(j) (TW = 32)
+    bool fatdep = false;          // 16-byte dependency entries carrying the law (meta, rate)
     bool any_explicit = false;    // an explicit rate expression (generated smc_explicit)
     int max_dep = 0;
     std::vector<uint8_t> blob;    // host copy
