@@ -331,12 +331,13 @@ def main():
     per_gpu_events = events / world
     achieved = sim_events * ipe / 32.0 / (tot_kernel_ms / 1e3) / 1e9
     achieved_counted = per_gpu_events * ipe / 32.0 / (tot_kernel_ms / 1e3) / 1e9
-    prof, traffic_src = measured_profile(cfg["name"], "smc_ssa_%s" % ("thread" if info["variant"] == 1 else "tile"))
+    kname = "smc_ssa_" + {1: "thread", 2: "tile", 3: "literal", 4: "sweep"}[info["variant"]]
+    prof, traffic_src = measured_profile(cfg["name"], kname)
     traffic = prof["dram_bytes_per_launch"] if prof else None
     roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Gwarp-inst/s", "frac": achieved / peak,
                 "traffic": traffic, "traffic_source": traffic_src,
                 "algorithmic_bytes_per_launch": "tables once per CTA + 64 B control block (no per-event HBM traffic)",
-                "kernel": "smc_ssa_%s" % ("thread" if info["variant"] == 1 else "tile"),
+                "kernel": kname,
                 "inst_per_event": ipe, "kernel_ms_per_step": tot_kernel_ms / args.steps,
                 "simulated_events_per_step": sim_events / args.steps,
                 "counted_events_per_step": per_gpu_events / args.steps,

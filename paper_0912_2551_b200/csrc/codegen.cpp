@@ -470,6 +470,66 @@ std::string model_code_thread(const Model& m) {
     return o.str();
 }
 
+// ------------------------------------------------- variant 4 model code ---
+// Pass 1 of the sweep kernel: every law in index order from register copies of the
+// counts, group sums of SMC_SW_S consecutive laws (left to right) and the prefix chain
+// P_g = P_{g-1} + sum_g (reading R12).  Laws use the same IEEE operations as the law
+// table of pass 2 (ssa_sweep.cuh smc_law_sw): exact int64 h, one rounding to double,
+// a = c * h, Hill as in variant 1 (computed, not tabulated).
+int sweep_group(const Model& m) {
+    int S = 16;
+    if (const char* e = std::getenv("SMC_SW_S")) S = std::max(1, std::atoi(e));
+    return std::min(S, m.M);
+}
+
+std::string model_code_sweep(const Model& m) {
+    std::ostringstream o;
+    const int N = m.N, M = m.M, S = sweep_group(m), G = (M + S - 1) / S;
+    o << "#define SMC_SW_S " << S << "\n#define SMC_SW_G " << G << "\n";
+    o << "__constant__ double smc_rc[" << M << "] = {";
+    for (int k = 0; k < M; ++k) o << (k ? ", " : "") << dlit(m.R[(size_t)k].c);
+    o << "};\n";
+    for (int k = 0; k < M; ++k) {
+        const Reaction& r = m.R[(size_t)k];
+        o << "__device__ __forceinline__ double smc_law" << k << "(const int (&x)[SMC_N]) {\n";
+        if (!r.rate.empty()) {
+            o << explicit_body(r, "x", "    ") << "}\n";
+            continue;
+        }
+        o << "    double a = " << law_expr(r, k) << ";\n";
+        if (r.hill) {
+            o << "    const double q = __ddiv_rn((double)x[" << r.rep << "], " << dlit(r.K) << ");\n";
+            o << "    double qn = q;\n";
+            for (int i = 1; i < r.n; ++i) o << "    qn = __dmul_rn(qn, q);\n";
+            o << "    a = __ddiv_rn(a, __dadd_rn(1.0, qn));\n";
+        }
+        o << "    return a;\n}\n";
+    }
+    bool any_explicit = false;
+    for (auto& r : m.R) any_explicit |= !r.rate.empty();
+    if (any_explicit) {                 // explicit laws of pass 2 (law-table kind 5)
+        o << "__device__ __noinline__ double smc_explicit4(int k, const SmcXCol& xs) {\n    switch (k) {\n";
+        for (int k = 0; k < M; ++k)
+            if (!m.R[(size_t)k].rate.empty())
+                o << "    case " << k << ":\n" << explicit_body(m.R[(size_t)k], "xs", "        ");
+        o << "    }\n    return 0.0;\n}\n";
+    }
+    o << "__device__ __forceinline__ void smc_sweep(const SmcXCol& X, double (&P)[SMC_SW_G]) {\n";
+    o << "    int x[SMC_N];\n#pragma unroll\n    for (int s = 0; s < SMC_N; ++s) x[s] = X[s];\n";
+    o << "    double g;\n";
+    for (int gi = 0; gi < G; ++gi) {
+        for (int k = gi * S; k < std::min(M, gi * S + S); ++k) {
+            if (k == gi * S) o << "    g = smc_law" << k << "(x);\n";
+            else o << "    g = __dadd_rn(g, smc_law" << k << "(x));\n";
+        }
+        if (gi == 0) o << "    P[0] = g;\n";
+        else o << "    P[" << gi << "] = __dadd_rn(P[" << gi - 1 << "], g);\n";
+    }
+    o << "}\n";
+    (void)N;
+    return o.str();
+}
+
 size_t align16(size_t v) { return (v + 15) & ~(size_t)15; }
 
 }  // namespace
@@ -504,7 +564,7 @@ int tile_width(const Model& m) {
     return m.M <= 256 ? 8 : (m.M <= 512 ? 16 : 32);
 }
 
-TileLayout pack_tables(const Model& m) {
+TileLayout pack_tables(const Model& m, bool sweep) {
     TileLayout L;
     const int N = m.N, M = m.M;
     L.tw = tile_width(m);
@@ -532,7 +592,8 @@ TileLayout pack_tables(const Model& m) {
         L.any_general |= order > 2;
     }
     size_t nnz = 0;
-    for (auto& d : m.dep) { nnz += d.size(); L.max_dep = std::max<int>(L.max_dep, (int)d.size()); }
+    if (!sweep)
+        for (auto& d : m.dep) { nnz += d.size(); L.max_dep = std::max<int>(L.max_dep, (int)d.size()); }
     size_t o = 0;
     L.off_x0 = o; o = align16(o + 4 * (size_t)L.n_pad);
     L.off_law = o; o = align16(o + 16 * (size_t)M);
@@ -550,11 +611,13 @@ TileLayout pack_tables(const Model& m) {
     for (int k = 0; k < M; ++k)
         for (int sp : m.law_species(k)) readers[(size_t)sp].push_back(k);
     size_t nnz_sp = 0;
-    for (auto& r : readers) nnz_sp += r.size();
+    if (!sweep)
+        for (auto& r : readers) nnz_sp += r.size();
     L.depsp = M > 512 && L.tw == 32;
     if (const char* e = std::getenv("SMC_DEPSP")) L.depsp = std::atoi(e) != 0 && L.tw == 32;
     L.dep16 = L.depsp || M > 512;
     if (const char* e = std::getenv("SMC_DEP16")) L.dep16 = L.depsp || std::atoi(e) != 0;
+    if (sweep) L.depsp = L.dep16 = false;
     // "fat" 16-byte entries {k | slot << 16, law meta, rate} for the reaction-indexed CSR:
     // the dependency walk reads contiguous entries instead of random law-table rows (the
     // law-table gather was 24 % of C4's shared-memory wavefronts, 70 % of them bank-conflict
@@ -611,10 +674,12 @@ TileLayout pack_tables(const Model& m) {
             chg[4 * j + q] = e;
         }
     }
+    if (sweep) return L;                           // variant 4: no dependency graph
+    if ((size_t)L.gs * L.tw > 65536) fail(SMC_E_MODEL, "tile variant: too many reactions for 16-bit slots");
     auto* doff = (uint32_t*)(L.blob.data() + L.off_dep_off);
     auto* dep = (uint32_t*)(L.blob.data() + L.off_dep);
     auto* dep16 = (uint16_t*)(L.blob.data() + L.off_dep);
-    if ((size_t)L.gs * L.tw > 65536) fail(SMC_E_MODEL, "tile variant: too many reactions for 16-bit slots");
+
     size_t pos = 0;
     if (L.depsp) {
         for (int sp = 0; sp < N; ++sp) {
@@ -668,6 +733,21 @@ std::string generate_source(const Model& m, const Property& p, int variant, cons
         if (const char* e = std::getenv("SMC_PIPE2")) pipe2 = std::atoi(e);
         o << "#define SMC_PIPE2 " << pipe2 << "\n";
         if (const char* e = std::getenv("SMC_UNROLL")) o << "#define SMC_UNROLL " << std::atoi(e) << "\n";
+    } else if (variant == 4) {
+        // 128-thread CTAs; resident CTAs per SM bounded by the counts' shared memory
+        // (tables + 128 columns of N+1 ints) and by registers (pass 1 keeps the counts and
+        // the group prefixes in registers): at most 4 by default (<= 128 registers)
+        const size_t per_cta = tl->bytes + 128 * 4 * (size_t)(m.N + 1) + 64;
+        int minb = (int)std::max<size_t>(1, std::min<size_t>(4, 227 * 1024 / per_cta));
+        if (const char* e = std::getenv("SMC_MINB")) minb = std::atoi(e);
+        o << "#define SMC_SWEEP 1\n#define SMC_BLOCK 128\n#define SMC_MINB " << minb << "\n";
+        o << "#define SMC_OFF_X0 " << tl->off_x0 << "\n#define SMC_OFF_LAW " << tl->off_law
+          << "\n#define SMC_OFF_HREP " << tl->off_hill_rep << "\n#define SMC_OFF_HK " << tl->off_hill_k
+          << "\n#define SMC_OFF_HN " << tl->off_hill_n << "\n#define SMC_OFF_CHG " << tl->off_chg << "\n";
+        o << "#define SMC_TAB_BYTES " << tl->bytes << "\n";
+        o << "#define SMC_ANY_HILL " << (tl->any_hill ? 1 : 0) << "\n";
+        o << "#define SMC_ANY_GENERAL " << (tl->any_general ? 1 : 0) << "\n";
+        o << "#define SMC_ANY_EXPLICIT " << (tl->any_explicit ? 1 : 0) << "\n";
     } else {
         if (p.literal) {
             const double H = p.t_max > 0.0 ? p.t_max : p.horizon;
@@ -692,6 +772,7 @@ std::string generate_source(const Model& m, const Property& p, int variant, cons
     }
     o << embedded_source("ssa_common.cuh") << "\n";
     if (variant == 1 || variant == 3) o << model_code_thread(m) << "\n";
+    if (variant == 4) o << model_code_sweep(m) << "\n";
     if (variant == 2 && tl->any_explicit) {          // explicit laws of the tile variant
         o << "__device__ __noinline__ double smc_explicit(int k, const int* xs) {\n    switch (k) {\n";
         for (int k = 0; k < m.M; ++k)
@@ -705,7 +786,7 @@ std::string generate_source(const Model& m, const Property& p, int variant, cons
     }
     if (p.literal) o << literal_code(p) << "\n" << recording_monitor(p) << "\n";   // variant 2 only
     else o << MonGen(p).emit() << "\n";
-    o << embedded_source(variant == 1 ? "ssa_thread.cuh" : "ssa_tile.cuh") << "\n";
+    o << embedded_source(variant == 1 ? "ssa_thread.cuh" : (variant == 4 ? "ssa_sweep.cuh" : "ssa_tile.cuh")) << "\n";
     return o.str();
 }
 

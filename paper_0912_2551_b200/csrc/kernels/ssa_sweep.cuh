@@ -1,0 +1,256 @@
+// ssa_sweep.cuh -- variant 4: persistent THREAD-OWNED SSA + monitor kernel for
+// networks too large for registers (C4: 50 x 200), with a full propensity SWEEP
+// per event instead of stored propensities.
+//
+// * Each lane owns one trajectory (refill, burst and verdict logic as variant 1).
+//   Its counts live in shared memory as a column: x[s] at s*SMC_BLOCK + tid, so
+//   every access -- uniform s in the sweep, per-lane s in the selection and the
+//   update -- hits bank (tid mod 32): conflict-free whatever the species.
+//   x[N] = 1 is a constant column (operand of h = x * 1 in the law table).
+// * Model tables (law table, change lists, Hill parameters) are staged once per CTA
+//   by a TMA bulk copy (cp.async.bulk + mbarrier), as in the tile variant.
+// * Per event, pass 1 (generated straight-line code, smc_sweep): every law a_k(x)
+//   in index order, summed per group of SMC_SW_S consecutive reactions, and the
+//   group prefix P_g = P_{g-1} + (group g sum) kept in registers; a0 = P_{G-1}
+//   (reading R12: a fixed order).  All lanes of a warp run the same law at the
+//   same time: rates come from the constant bank, species loads are uniform
+//   offsets.  The propensities are not stored: a dependency-driven update would
+//   touch, over the 32 lanes' different reactions, nearly every law anyway (the
+//   argument of variant 1), and not storing a[M] frees the 1.6 KB per trajectory
+//   that would cap residency.
+// * Selection (Eq. 2b), pass 2: the group g = #{P_i <= u2 a0} by integer compares
+//   of the non-negative doubles' bit patterns, then the member inside g by a
+//   running sum from P_{g-1} over the group's laws read from the smem law table
+//   (per-lane group: a short divergent loop of <= SMC_SW_S laws).
+// * x += v_j from the change table; the monitor reads its atoms from the column.
+//
+// Generated hooks (codegen.cpp): SMC_N, SMC_M, SMC_BLOCK, SMC_MINB, SMC_SW_S, SMC_SW_G,
+//   SMC_OFF_X0/LAW/HREP/HK/HN/CHG, SMC_TAB_BYTES, SMC_ANY_HILL, SMC_ANY_GENERAL,
+//   SMC_ANY_EXPLICIT (+ smc_explicit4), smc_sweep(X, P), SMC_TMAX, SmcMon.
+
+#ifndef SMC_BURST
+#define SMC_BURST 8
+#endif
+
+struct SmcSwTabs {
+    const int* x0;
+    const SmcLaw* law;
+    const int* hill_rep;
+    const double* hill_k;
+    const int* hill_n;
+    const unsigned short* chg;       // [M][4]: species << 4 | (delta + 8), 0xFFFF = none
+};
+
+// a_k(x) from the law table (readings R8/R9/R20) -- the same IEEE
+// operations as the generated pass-1 law, so both passes see identical values:
+// order <= 2: h = fl(x0 * x1) (x[N] = 1 for the missing operand), kind 2 as
+// fl(x (x-1)) with the 1/2 folded into c; order 3-4: exact int64 binomials.
+__device__ __forceinline__ double smc_law_sw(int k, const SmcXCol& X, const SmcSwTabs& T) {
+    const SmcLaw L = T.law[k];
+    const int kind = (int)((L.u0 >> 16) & 7u);
+#if SMC_ANY_EXPLICIT
+    if (kind == 5) return smc_explicit4(k, X);
+#endif
+    const int v0 = X[(int)(L.u0 & 0xFFFFu)];
+    const int v1 = X[(int)(L.u1 & 0xFFFFu)];
+    double h;
+#if SMC_ANY_GENERAL
+    if (kind == 4) {
+        const smc_i64 y0 = v0, y1 = v1;
+        const smc_i64 h0 = ((L.u0 >> 20) & 3u) == 1u ? y0 : (y0 * (y0 - 1)) / 2;
+        const smc_i64 h1 = ((L.u1 >> 16) & 3u) == 1u ? y1 : (y1 * (y1 - 1)) / 2;
+        h = (double)(h0 * h1);
+    } else
+#endif
+    {
+        const int xb = (kind == 2) ? max(v0 - 1, 0) : v1;
+        h = (double)((smc_i64)v0 * (smc_i64)xb);          // exact product, one rounding
+    }
+    double a = __dmul_rn(L.c, h);
+#if SMC_ANY_HILL
+    if ((int)L.u0 < 0) {
+        const double q = __ddiv_rn((double)X[T.hill_rep[k]], T.hill_k[k]);
+        double qn = q;
+        for (int i = 1; i < T.hill_n[k]; ++i) qn = __dmul_rn(qn, q);
+        a = __ddiv_rn(a, __dadd_rn(1.0, qn));
+    }
+#endif
+    return a;
+}
+
+// non-negative doubles (and -0) order like their bit patterns as signed int64
+__device__ __forceinline__ smc_i64 smc_ord(double v) { return __double_as_longlong(v); }
+
+// member of group gi: first j with base + a_{j0} + ... + a_j > target (left to right);
+// rounding: the last a_j > 0 of the group, which exists since P_gi > P_{gi-1} (R11)
+__device__ __forceinline__ int smc_pick(int gi, double base, double target, const SmcXCol& X, const SmcSwTabs& T) {
+    const int j0 = gi * SMC_SW_S;
+    const int j1 = min(j0 + SMC_SW_S, SMC_M);
+    const smc_i64 tb = smc_ord(target);
+    double acc = base;
+    int last = j0;
+    for (int j = j0; j < j1; ++j) {
+        const double a = smc_law_sw(j, X, T);
+        acc = __dadd_rn(acc, a);
+        if (smc_ord(a) > 0) last = j;
+        if (smc_ord(acc) > tb) return j;
+    }
+    return last;
+}
+
+// rounding with u2 a0 >= every prefix: the last reaction with a_j > 0 (reading R11)
+__device__ __noinline__ int smc_last_positive_sw(const SmcXCol& X, const SmcSwTabs& T) {
+    for (int j = SMC_M - 1; j > 0; --j)
+        if (smc_law_sw(j, X, T) > 0.0) return j;
+    return 0;
+}
+
+extern "C" __global__ void __launch_bounds__(SMC_BLOCK, SMC_MINB) smc_ssa_sweep(SmcParams P) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ __align__(8) unsigned long long bar;
+    const smc_u32 lane = threadIdx.x & 31u;
+
+    // ---- stage the model tables: one TMA bulk copy per 32 KB chunk
+    if (threadIdx.x == 0) smc_mbar_init(&bar, 1);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        smc_mbar_expect_tx(&bar, (unsigned)SMC_TAB_BYTES);
+        for (unsigned off = 0; off < (unsigned)SMC_TAB_BYTES; off += 32768u) {
+            const unsigned n = ((unsigned)SMC_TAB_BYTES - off) < 32768u ? ((unsigned)SMC_TAB_BYTES - off) : 32768u;
+            smc_bulk_g2s(smem + off, (const unsigned char*)P.tables + off, n, &bar);
+        }
+    }
+    smc_mbar_wait(&bar, 0);
+    SmcSwTabs T;
+    T.x0 = (const int*)(smem + SMC_OFF_X0);
+    T.law = (const SmcLaw*)(smem + SMC_OFF_LAW);
+    T.hill_rep = (const int*)(smem + SMC_OFF_HREP);
+    T.hill_k = (const double*)(smem + SMC_OFF_HK);
+    T.hill_n = (const int*)(smem + SMC_OFF_HN);
+    T.chg = (const unsigned short*)(smem + SMC_OFF_CHG);
+    int* const xcol = (int*)(smem + SMC_TAB_BYTES) + threadIdx.x;
+    const SmcXCol X{xcol};
+    xcol[SMC_N * SMC_BLOCK] = 1;                        // x[N] = 1
+
+    const smc_u32 cap = (smc_u32)(P.event_cap < 0xFFFFFFFFull ? P.event_cap : 0xFFFFFFFFull);
+    double t = 0.0, tp = 0.0;
+    double e_cur = 0.0, u_cur = 0.0;      // draw of the current step k
+    smc_u32 k = 0;
+    smc_u64 rel = 0, traj = 0;
+    SmcMon mon;
+    bool busy = false, exhausted = false;
+    smc_u32 c_true = 0, c_false = 0, c_err = 0;
+    smc_i64 c_ev = 0;
+
+    for (;;) {
+        // ---- refill: compact the idle lanes onto fresh trajectory indices
+        for (;;) {
+            const bool want = !busy && !exhausted;
+            const smc_u32 wm = __ballot_sync(SMC_FULL, want);
+            if (wm == 0u) break;
+            const int leader = __ffs(wm) - 1;
+            smc_u64 base = 0;
+            if ((int)lane == leader) base = atomicAdd(P.cursor, (smc_u64)__popc(wm));
+            base = __shfl_sync(SMC_FULL, base, leader);
+            if (want) {
+                rel = base + (smc_u64)__popc(wm & ((1u << lane) - 1u));
+                if (rel >= P.count) {
+                    exhausted = true;
+                } else {
+                    traj = P.first + rel;
+                    for (int s = 0; s < SMC_N; ++s) xcol[s * SMC_BLOCK] = T.x0[s];
+                    t = 0.0;
+                    tp = 0.0;
+                    k = 0;
+                    mon.init();
+                    mon.enter(0u, 0.0, 0.0, X);          // sigma_buff = {(s0, t0)}
+                    const int v = mon.verdict();
+                    if (v >= 0) {
+                        if (v == 1) ++c_true; else ++c_false;
+                        if (P.verdicts) { P.verdicts[rel] = (unsigned char)v; P.events_out[rel] = 0; }
+                    } else {
+                        busy = true;
+                        smc_draw(P.seed, traj, 0ull, e_cur, u_cur);
+                    }
+                }
+            }
+        }
+        if (!__any_sync(SMC_FULL, busy)) break;
+
+#pragma unroll 1
+        for (int burst = 0; burst < SMC_BURST; ++burst) {
+            if (!busy) continue;
+            double e_nx, u_nx;                            // step k+1's draw, off the critical path
+            smc_draw(P.seed, traj, (smc_u64)k + 1ull, e_nx, u_nx);
+            double Pg[SMC_SW_G];
+            smc_sweep(X, Pg);                             // pass 1: a0 and the group prefixes
+            const double A = Pg[SMC_SW_G - 1];
+            const double tau = smc_tau(e_cur, A);
+            const double tn = __dadd_rn(t, tau);
+            int v = -1;
+            if (!(A >= SMC_A_MIN) || A > SMC_A_MAX) {      // A == 0: absorbed; else error (R19)
+                if (A == 0.0) {                           // absorbed (reading R7)
+                    mon.absorb();
+                    v = mon.verdict();
+                } else {
+                    v = 2;                                // bad propensity
+                }
+            } else {
+                mon.advance(k, tn, tau);
+                v = mon.verdict();
+                if (v < 0 && SMC_TMAX > 0.0 && tn > SMC_TMAX) {
+                    mon.timeout();
+                    v = mon.verdict();
+                }
+                if (v < 0) {
+                    // ---- selection (Eq. 2b): group by the prefixes, member by pass 2
+                    const double target = __dmul_rn(u_cur, A);
+                    const smc_i64 tb = smc_ord(target);
+                    int gi = 0;
+                    double base = 0.0;
+#pragma unroll
+                    for (int i = 0; i < SMC_SW_G; ++i) {
+                        const bool le = smc_ord(Pg[i]) <= tb;
+                        gi += le ? 1 : 0;
+                        base = le ? Pg[i] : base;
+                    }
+                    const int j = (gi < SMC_SW_G) ? smc_pick(gi, base, target, X, T) : smc_last_positive_sw(X, T);
+                    // ---- x += v_j (wrapping add; a negative result is a count overflow, R17)
+                    const uint2 ce = *(const uint2*)(T.chg + 4 * j);
+                    bool ovf = false;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const unsigned e = ((q < 2 ? ce.x : ce.y) >> (16 * (q & 1))) & 0xFFFFu;
+                        if (e != 0xFFFFu) {
+                            int* xp = xcol + (int)(e >> 4) * SMC_BLOCK;
+                            const int nv = (int)((unsigned)*xp + (unsigned)((int)(e & 15u) - 8));
+                            ovf |= nv < 0;
+                            *xp = nv;
+                        }
+                    }
+                    if (ovf) {
+                        v = 2;
+                    } else {
+                        tp = t;
+                        t = tn;
+                        ++k;
+                        e_cur = e_nx;
+                        u_cur = u_nx;
+                        mon.enter(k, t, tp, X);
+                        v = mon.verdict();
+                        if (v < 0 && k >= cap) v = 2;
+                    }
+                }
+            }
+            if (v >= 0) {
+                if (v == 1) ++c_true;
+                else if (v == 0) ++c_false;
+                else ++c_err;
+                c_ev += k;
+                if (P.verdicts) { P.verdicts[rel] = (unsigned char)v; P.events_out[rel] = (int)k; }
+                busy = false;
+            }
+        }
+    }
+    smc_flush_counts(c_true, c_false, c_ev, c_err, P.counters);
+}

@@ -34,40 +34,6 @@
 //   SMC_ANY_EXPLICIT (+ smc_explicit), SMC_DEPSP, SMC_FATDEP, SMC_ROWLAYOUT, SMC_GSP,
 //   SMC_TMAX, SmcMon (+ SMC_LIT_H, SMC_LIT_NODES, smc_lit_* for the recording monitor).
 
-__device__ __forceinline__ void smc_mbar_init(unsigned long long* bar, unsigned count) {
-    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void smc_mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
-    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void smc_bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
-    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                 ::"r"(d), "l"(src), "r"(bytes), "r"(b) : "memory");
-}
-__device__ __forceinline__ void smc_mbar_wait(unsigned long long* bar, unsigned parity) {
-    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
-    unsigned done = 0;
-    while (!done) {
-        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
-                     : "=r"(done) : "r"(a), "r"(parity) : "memory");
-    }
-}
-
-// Law table entry, one 16-byte load:
-//   u0 = s0 | kind << 16 | hill << 31, u1 = s1 (both species indices are valid:
-//   unused slots repeat s0), c = rate.  kind: 0 h = 1, 1 h = x0, 2 h = x0(x0-1)/2,
-//   3 h = x0 x1, 4 general (order 3-4: C(x0,st0) C(x1,st1) in int64; st in u1 >> 16).
-struct __align__(16) SmcLaw {
-    unsigned u0;
-    unsigned u1;
-    double c;
-};
-
 struct SmcTabs {
     const int* x0;
     const SmcLaw* law;

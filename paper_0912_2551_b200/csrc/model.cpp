@@ -1,5 +1,6 @@
 // model.cpp -- model packer: validation, reactant merging, change vectors and
 // the reaction dependency graph.
+#include <cstdlib>
 #include <algorithm>
 #include <cmath>
 #include <set>
@@ -45,9 +46,17 @@ void Model::build_deps() {
     deps_built = true;
 }
 
+// variant 4 (sweep) holds the counts of 128 trajectories per CTA in shared memory
+bool Model::sweep_fits() const { return N <= 4095 && 128 * 4 * (size_t)(N + 1) + 24 * (size_t)M + 4096 <= 200 * 1024; }
+
 int Model::variant() const {
     if (variant_forced) return variant_forced;
-    return (N <= 32 && M <= 32) ? 1 : 2;
+    if (N <= 32 && M <= 32) return 1;
+    // sweep for mid-size networks (pass 1 is straight-line code over all M laws with the
+    // counts in registers); SMC_SWEEP=0/1 forces the automatic choice off / on
+    bool sweep = N <= 64 && M <= 512;
+    if (const char* e = std::getenv("SMC_SWEEP")) sweep = std::atoi(e) != 0;
+    return (sweep && sweep_fits()) ? 4 : 2;
 }
 
 }  // namespace smc
@@ -164,8 +173,15 @@ int smc_model_set_rate_expr(smc_model* h, int32_t reaction, const char* expr, co
 }
 
 int smc_model_set_variant(smc_model* h, int32_t variant) {
-    if (!h || variant < 0 || variant > 2) { set_error("smc_model_set_variant: variant in 0..2"); return SMC_E_ARG; }
+    if (!h || variant < 0 || variant > 4 || variant == 3) {
+        set_error("smc_model_set_variant: variant 0 (automatic), 1, 2 or 4");
+        return SMC_E_ARG;
+    }
     Model& m = h->m;
+    if (variant == 4 && !m.sweep_fits()) {
+        set_error("smc_model_set_variant: sweep variant needs the counts of 128 trajectories in shared memory");
+        return SMC_E_ARG;
+    }
     if (variant == 1 && (m.N > 32 || m.M > 32)) {
         set_error("smc_model_set_variant: thread-owned variant needs N <= 32 and M <= 32");
         return SMC_E_ARG;

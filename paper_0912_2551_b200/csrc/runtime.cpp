@@ -84,10 +84,11 @@ struct PropKernel {
 };
 
 struct DeviceState {
-    void* tables[3] = {nullptr, nullptr, nullptr};   // per variant: [1] Hill tables, [2] tile tables
-    size_t table_bytes[3] = {0, 0, 0};
-    bool tables_ready[3] = {false, false, false};
-    TileLayout layout;
+    void* tables[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};   // per variant: [1] Hill, [2] tile, [4] sweep
+    size_t table_bytes[5] = {0, 0, 0, 0, 0};
+    bool tables_ready[5] = {false, false, false, false, false};
+    TileLayout layout;              // variant 2
+    TileLayout sw_layout;           // variant 4
     void* ctl = nullptr;            // [0..8) cursor, [16..48) counters, [64..72) spec cursor, [80..112) spec scratch
     int64_t* host_counts = nullptr; // pinned
     // speculative batch of smc_estimate (prefix-exact rounds): this rank's slice [lo, hi)
@@ -182,6 +183,7 @@ PropKernel& prepare(Model& m, const Property& p) {
     // buffered trace + literal |= (reading R23): thread-owned models run variant 3, tile
     // models the tile kernel with the recording monitor
     if (p.literal && pk.variant == 1) pk.variant = 3;
+    if (p.literal && pk.variant == 4) pk.variant = 2;    // the recording monitor lives in the tile kernel
     const TileLayout* tl = nullptr;
     const int v = pk.variant == 3 ? 1 : pk.variant;      // table set (variant 3 uses variant 1's)
     if (!d.tables_ready[v]) {
@@ -192,6 +194,10 @@ PropKernel& prepare(Model& m, const Property& p) {
             d.layout = pack_tables(m);
             src = d.layout.blob.data();
             bytes = d.layout.bytes;
+        } else if (v == 4) {
+            d.sw_layout = pack_tables(m, true);
+            src = d.sw_layout.blob.data();
+            bytes = d.sw_layout.bytes;
         } else {
             ht = pack_hill_tables(m);
             src = ht.values.data();
@@ -206,9 +212,11 @@ PropKernel& prepare(Model& m, const Property& p) {
         d.tables_ready[v] = true;
     }
     if (v == 2) tl = &d.layout;
+    if (v == 4) tl = &d.sw_layout;
     pk.tables = d.tables[v];
     pk.source = generate_source(m, p, pk.variant, tl);
-    pk.k = get_kernel(pk.source, pk.variant == 1 ? "smc_ssa_thread" : (pk.variant == 2 ? "smc_ssa_tile" : "smc_ssa_literal"));
+    pk.k = get_kernel(pk.source, pk.variant == 1 ? "smc_ssa_thread"
+                                 : (pk.variant == 2 ? "smc_ssa_tile" : (pk.variant == 4 ? "smc_ssa_sweep" : "smc_ssa_literal")));
     const void* fn = (const void*)pk.k->kernel;
     if (pk.variant == 3) {
         pk.block = 128;
@@ -217,6 +225,18 @@ PropKernel& prepare(Model& m, const Property& p) {
         pk.grid_max = std::max(1, nb) * d.sm_count;
         pk.smem = 0;
         alloc_traces(m, p, pk, pk.block);
+    } else if (pk.variant == 4) {
+        pk.block = 128;
+        pk.smem = (int)(tl->bytes + (size_t)pk.block * 4 * (size_t)(m.N + 1));
+        cudaFuncAttributes fa;
+        ck(cudaFuncGetAttributes(&fa, fn), "cudaFuncGetAttributes");
+        if ((size_t)pk.smem + fa.sharedSizeBytes > (size_t)d.max_smem_optin)
+            fail(SMC_E_CUDA, "sweep kernel: counts and tables do not fit in shared memory");
+        ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, pk.smem), "smem attr");
+        int nb = 0;
+        ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, pk.block, (size_t)pk.smem), "occupancy");
+        if (nb < 1) fail(SMC_E_CUDA, "sweep kernel: no resident CTA");
+        pk.grid_max = nb * d.sm_count;
     } else if (pk.variant == 1) {
         pk.block = 128;
         int nb = 0;
@@ -735,8 +755,9 @@ int smc_kernel_source(smc_model* h, const smc_property* ph, char* buf, size_t* l
         const int mv = m.variant();
         const int v = (ph->p->literal && mv == 1) ? 3 : mv;
         TileLayout tl;
-        if (v == 2) tl = pack_tables(m);
-        std::string s = generate_source(m, *ph->p, v, v == 2 ? &tl : nullptr);
+        const int vv = (ph->p->literal && v == 4) ? 2 : v;
+        if (vv == 2 || vv == 4) tl = pack_tables(m, vv == 4);
+        std::string s = generate_source(m, *ph->p, vv, (vv == 2 || vv == 4) ? &tl : nullptr);
         size_t need = s.size() + 1;
         if (buf) std::memcpy(buf, s.c_str(), std::min(*len, need));
         *len = need;

@@ -66,7 +66,8 @@ struct Model {
     std::mutex mu;
     void build_deps();
     std::vector<int> law_species(int k) const;   // species read by a_k
-    int variant() const;                          // 1 thread-owned, 2 tile
+    int variant() const;                          // 1 thread-owned, 2 tile, 4 sweep
+    bool sweep_fits() const;
 };
 
 // -------------------------------------------------------------- property ---
@@ -160,7 +161,7 @@ struct TileLayout {               // packed model tables (variant 2), byte offse
     int max_dep = 0;
     std::vector<uint8_t> blob;    // host copy
 };
-TileLayout pack_tables(const Model& m);
+TileLayout pack_tables(const Model& m, bool sweep = false);   // sweep: law/change tables only (variant 4)
 // variant 1: zero-order Hill propensities a_k(x_r), x_r < size, tabulated on the host with
 // the same IEEE operations as the law (one __ldg instead of two divisions per update)
 struct HillTables {

@@ -3,7 +3,7 @@ options jit.cpp uses on the GPU box, so the cubin is the binary that runs) on a
 machine without a GPU: catches codegen errors and reports registers / spills /
 static SASS size.  Writes build/gen/<cfg>_v<variant>.cu and .cubin.
 
-  python scripts/check_codegen.py [C1 C2 ...]       (SMC_TILE_WIDTH honoured)
+  python scripts/check_codegen.py [C1 C2 ...]       (SMC_TILE_WIDTH, SMC_SW_S honoured)
 """
 import ctypes
 import os
@@ -45,7 +45,8 @@ def main(names):
     os.makedirs(out, exist_ok=True)
     for name in names:
         cfg = workloads.get(name)
-        for variant in ([1, 2] if len(cfg["species"]) <= 32 and len(cfg["reactions"]) <= 32 else [2]):
+        small = len(cfg["species"]) <= 32 and len(cfg["reactions"]) <= 32
+        for variant in ([1, 2, 4] if small else [2, 4]):
             m = smc.Model.from_config(cfg)
             m.set_variant(variant)
             p = smc.Property(m, cfg["formula"], t_max=cfg.get("t_max", 0.0))

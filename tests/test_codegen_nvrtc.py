@@ -1,6 +1,6 @@
 """Every generated kernel compiles for sm_100a with the same NVRTC library and options
 the GPU box uses (scripts/check_codegen.py), without a GPU: thread, tile (every tile
-width) and literal variants for the benchmark configs and the feature workloads."""
+width), sweep and literal variants for the benchmark configs and the feature workloads."""
 import os
 import sys
 
@@ -12,8 +12,8 @@ import paper_0912_2551_b200 as smc
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scripts"))
 from check_codegen import nvrtc_cubin  # noqa: E402
 
-CASES = [("C1", 1), ("C2", 1), ("C2", 2), ("C3", 1), ("C3", 2), ("C4", 2), ("C5", 2), ("EXPL", 1), ("EXPL", 2),
-         ("CC", 1), ("CC", 2)]
+CASES = [("C1", 1), ("C1", 4), ("C2", 1), ("C2", 2), ("C2", 4), ("C3", 1), ("C3", 2), ("C3", 4), ("C4", 2), ("C4", 4),
+         ("C5", 2), ("C5", 4), ("EXPL", 1), ("EXPL", 2), ("EXPL", 4), ("CC", 1), ("CC", 2), ("CC", 4)]
 
 
 def _compile(cfg, variant, formula=None, t_max=0.0):

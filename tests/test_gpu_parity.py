@@ -59,7 +59,7 @@ def test_philox_stream_bit_exact(smc):
             assert b == O.philox(seed, traj, step0 + q)
 
 
-@pytest.mark.parametrize("variant", [1, 2])
+@pytest.mark.parametrize("variant", [1, 2, 4])
 def test_c1_all_replicas(smc, variant):
     cfg = workloads.c1()
     a, ae, v, e, ov, oe = _compare(smc, cfg, cfg["seed"], 0, 10_000, variant)
@@ -71,7 +71,7 @@ def test_c1_all_replicas(smc, variant):
     assert lo <= exact <= hi
 
 
-@pytest.mark.parametrize("variant", [1, 2])
+@pytest.mark.parametrize("variant", [1, 2, 4])
 def test_c2_replicas(smc, variant):
     cfg = workloads.c2()
     a, ae, *_ = _compare(smc, cfg, cfg["seed"], 0, 3000, variant)
@@ -100,7 +100,7 @@ def test_c2_wilson_estimate(smc):
     del om, of
 
 
-@pytest.mark.parametrize("variant", [1, 2])
+@pytest.mark.parametrize("variant", [1, 2, 4])
 def test_c3_replicas(smc, variant):
     cfg = workloads.c3()
     a, ae, *_ = _compare(smc, cfg, cfg["seed"], 0, 400, variant)
@@ -176,7 +176,7 @@ def test_edge_cases(smc):
     "(A == 10) | F[0,0.1](A < 9)"])
 def test_templates_vs_oracle(smc, formula):
     cfg = dict(workloads.c1(), formula=formula)
-    for variant in (1, 2):
+    for variant in (1, 2, 4):
         a, ae, *_ = _compare(smc, cfg, 4, 0, 5000, variant)
         assert a >= AGREE and ae >= AGREE, (formula, variant, a, ae)
 
@@ -198,22 +198,22 @@ def test_shard_invariance(smc):
         assert tot == whole
 
 
-@pytest.mark.parametrize("name", ["C4", "C5"])
-def test_large_networks_vs_oracle_fixture(smc, name):
-    """Tile variant (smem/TMA-staged tables) vs the oracle's per-replica verdicts and event
-    counts (tests/golden/<cfg>_oracle.json, written by scripts/make_fixtures.py from oracle/ only)."""
+@pytest.mark.parametrize("name,variant", [("C4", 2), ("C4", 4), ("C5", 2), ("C5", 4)])
+def test_large_networks_vs_oracle_fixture(smc, name, variant):
+    """Tile and sweep variants (smem/TMA-staged tables) vs the oracle's per-replica verdicts and
+    event counts (tests/golden/<cfg>_oracle.json, written by scripts/make_fixtures.py from oracle/ only)."""
     import json
     import os
     fx = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "%s_oracle.json" % name.lower())))
     cfg = workloads.get(name)
     assert fx["formula"] == cfg["formula"] and fx["seed"] == cfg["seed"]
-    m, p = _pair(smc, cfg)
+    m, p = _pair(smc, cfg, variant)
     v, e = m.run_verdicts(p, fx["first"], fx["n"], fx["seed"])
     v, e = v.cpu().numpy(), e.cpu().numpy()
     ov, oe = np.array(fx["verdicts"]), np.array(fx["events"])
     mism = int(((v != ov) | (e != oe)).sum())
-    assert mism <= 1, (name, mism)           # ulp-level flips only (readings R12/S11)
-    assert m.last_launch(p)["variant"] == 2
+    assert mism <= 1, (name, variant, mism)  # ulp-level flips only (readings R12/S11)
+    assert m.last_launch(p)["variant"] == variant
 
 
 @pytest.mark.parametrize("width", ["4", "8", "16", "32"])
@@ -224,7 +224,7 @@ def test_tile_widths_vs_fixture(smc, width, monkeypatch):
     monkeypatch.setenv("SMC_TILE_WIDTH", width)
     fx = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "c4_oracle.json")))
     cfg = workloads.c4()
-    m, p = _pair(smc, cfg)
+    m, p = _pair(smc, cfg, variant=2)
     n = 600
     v, e = m.run_verdicts(p, 0, n, fx["seed"])
     v, e = v.cpu().numpy(), e.cpu().numpy()
@@ -304,7 +304,7 @@ def _law_kinds_cfg():
                 formula="F[0,5](C > 8)", t_max=0.0, seed=11, sampling=dict(mode="fixed", n=2000))
 
 
-@pytest.mark.parametrize("variant", [1, 2])
+@pytest.mark.parametrize("variant", [1, 2, 4])
 def test_all_law_kinds_vs_oracle(smc, variant):
     """The tile kernel forms h in fp64 for order <= 2 and in int64 for order 3-4; the thread
     kernel always in int64.  Both must reproduce the oracle's replicas exactly."""
@@ -354,7 +354,7 @@ def test_fig3_modes_vs_oracle(smc, p):
         assert smc.estimate(m, prop, 0.99, 0.025, 1)["n_total"] == 304
 
 
-@pytest.mark.parametrize("variant", [1, 2])
+@pytest.mark.parametrize("variant", [1, 2, 4])
 def test_explicit_rates_vs_oracle(smc, variant):
     """NEXT-3: explicit propensities (repressed production, Michaelis-Menten conversion,
     explicit decay) mixed with mass-action laws, thread and tile variants, replica by
@@ -392,7 +392,7 @@ def test_cell_cycle_rows_vs_oracle(smc, row):
     assert ae >= AGREE, (row, a, ae)
 
 
-@pytest.mark.parametrize("variant", [1, 2])
+@pytest.mark.parametrize("variant", [1, 2, 4])
 def test_general_val_atoms_vs_oracle(smc, variant):
     """NEXT-2: general val atoms -- non-linear int64 products, '/', Real constants,
     sqrt / abs / min / max / pow -- in the GPU monitors, replica by replica against the
@@ -551,7 +551,7 @@ def test_random_models_and_formulas_vs_oracle(smc, seed):
     of = O.OracleFormula(cfg["formula"], cfg["species"])
     mode = "stream" if of.streamable else "literal"
     oc, ov, oe = O.run(O.OracleModel(cfg), of, seed, 0, 400, mode=mode)
-    for variant in (1, 2):
+    for variant in (1, 2, 4):
         m, p = _pair(smc, cfg, variant)
         v, e = m.run_verdicts(p, 0, 400, seed)
         v, e = v.cpu().numpy(), e.cpu().numpy().astype(np.int64)
@@ -600,19 +600,21 @@ def _random_large_case(seed):
 
 @pytest.mark.parametrize("seed", range(12))
 def test_random_large_networks_vs_oracle(smc, seed):
-    """Fuzz of the tile kernel: random tile-only networks (every law shape) x template
-    formulas, every tile width, replica for replica against the oracle's streaming monitor."""
+    """Fuzz of the tile and sweep kernels: random tile-only networks (every law shape) x
+    template formulas, every tile width and the sweep variant, replica for replica against
+    the oracle's streaming monitor."""
     cfg = _random_large_case(seed)
     oc, ov, oe = O.run(O.OracleModel(cfg), O.OracleFormula(cfg["formula"], cfg["species"]), seed, 0, 300)
-    for width in ("8", "32") if seed % 2 else ("4", "16"):
+    for width in ("8", "32", "sweep") if seed % 2 else ("4", "16", "sweep"):
         os_env = __import__("os").environ
-        os_env["SMC_TILE_WIDTH"] = width
+        if width != "sweep":
+            os_env["SMC_TILE_WIDTH"] = width
         try:
-            m, p = _pair(smc, cfg)
+            m, p = _pair(smc, cfg, 4 if width == "sweep" else 2)
             v, e = m.run_verdicts(p, 0, 300, seed)
         finally:
-            del os_env["SMC_TILE_WIDTH"]
+            os_env.pop("SMC_TILE_WIDTH", None)
         v, e = v.cpu().numpy(), e.cpu().numpy().astype(np.int64)
-        assert m.last_launch(p)["variant"] == 2
+        assert m.last_launch(p)["variant"] == (4 if width == "sweep" else 2)
         bad = int(((v != ov) | (e != oe)).sum())
         assert bad <= 1, (seed, width, cfg["formula"], bad, oc)

@@ -116,6 +116,28 @@ def test_codegen_source(name):
     src = m.kernel_source(p)
     assert "struct SmcMon" in src
     assert ("smc_ssa_thread" in src) == (len(cfg["reactions"]) <= 32)
+    assert ("smc_ssa_sweep" in src) == (name == "C4")          # automatic choice: sweep for C4
+
+
+def test_variant_selection_and_errors():
+    cfg = workloads.c4()
+    m = smc.Model.from_config(cfg)
+    p = smc.Property(m, cfg["formula"])
+    for v, entry in ((2, "smc_ssa_tile"), (4, "smc_ssa_sweep"), (0, "smc_ssa_sweep")):
+        m.set_variant(v)
+        assert entry in m.kernel_source(p)
+    for bad in (3, 5, -1, 1):            # 3 is the literal variant (chosen by the formula), 1 needs N, M <= 32
+        with pytest.raises(smc.SmcError):
+            m.set_variant(bad)
+    # a literal (nested) formula on a sweep model runs the tile kernel's recording monitor
+    m.set_variant(4)
+    lp = smc.Property(m, "F[0,1](G[0.5,1](S0 > S1))")
+    assert "smc_ssa_tile" in m.kernel_source(lp)
+    # the counts of 128 trajectories must fit in shared memory
+    big = dict(cfg, species=["S%d" % i for i in range(500)], x0=[1] * 500)
+    mb = smc.Model.from_config(big)
+    with pytest.raises(smc.SmcError):
+        mb.set_variant(4)
 
 
 def _oracle_runner(cfg, seed, stats):
