@@ -477,7 +477,7 @@ std::string model_code_thread(const Model& m) {
 // table of pass 2 (ssa_sweep.cuh smc_law_sw): exact int64 h, one rounding to double,
 // a = c * h, Hill as in variant 1 (computed, not tabulated).
 int sweep_group(const Model& m) {
-    int S = 16;
+    int S = 12;     // C4 (M = 200): S = 8 8.6e9, 12 1.14e10, 16 1.07e10, 20 1.08e10 events/s
     if (const char* e = std::getenv("SMC_SW_S")) S = std::max(1, std::atoi(e));
     return std::min(S, m.M);
 }
@@ -514,19 +514,66 @@ std::string model_code_sweep(const Model& m) {
                 o << "    case " << k << ":\n" << explicit_body(m.R[(size_t)k], "xs", "        ");
         o << "    }\n    return 0.0;\n}\n";
     }
+    // fast laws, valid while every count is < 2^26: each mass-action count product h is
+    // < 2^52, so (double)h is formed exactly on the FP64 pipe as (2^52 + h) - 2^52 from
+    // the bit pattern 0x43300000:h (no int64 -> fp64 conversion on the XU pipe); the
+    // values are identical to the general laws'
+    std::vector<bool> used((size_t)N, false);
+    for (int k = 0; k < M; ++k) {
+        const Reaction& r = m.R[(size_t)k];
+        for (int sp : m.law_species(k)) used[(size_t)sp] = true;
+        o << "__device__ __forceinline__ double smc_lawf" << k << "(const int (&x)[SMC_N]) {\n";
+        int order = 0;
+        for (int q = 0; q < 2; ++q) order += r.s[q] >= 0 ? r.st[q] : 0;
+        if (!r.rate.empty() || order > 2) {           // explicit rate / order 3-4: the general law
+            o << "    return smc_law" << k << "(x);\n}\n";
+            continue;
+        }
+        std::string h;
+        if (order == 0) h = "";
+        else if (r.s[1] < 0 && r.st[0] == 1) h = "smc_u2d((smc_u64)(unsigned)x[" + std::to_string(r.s[0]) + "])";
+        else if (r.s[1] < 0) {
+            const std::string xs = "(smc_u64)(unsigned)x[" + std::to_string(r.s[0]) + "]";
+            h = "smc_u2d((" + xs + " * (" + xs + " - 1ull)) >> 1)";     // x >= 1 whenever it matters; x = 0 -> 0
+        } else {
+            h = "smc_u2d((smc_u64)(unsigned)x[" + std::to_string(r.s[0]) + "] * (smc_u64)(unsigned)x[" +
+                std::to_string(r.s[1]) + "])";
+        }
+        o << "    (void)x;\n";
+        o << "    double a = " << (h.empty() ? "__dmul_rn(smc_rc[" + std::to_string(k) + "], 1.0)"
+                                        : "__dmul_rn(smc_rc[" + std::to_string(k) + "], " + h + ")") << ";\n";
+        if (r.hill) {
+            o << "    const double q = __ddiv_rn(smc_u2d((smc_u64)(unsigned)x[" << r.rep << "]), " << dlit(r.K) << ");\n";
+            o << "    double qn = q;\n";
+            for (int i = 1; i < r.n; ++i) o << "    qn = __dmul_rn(qn, q);\n";
+            o << "    a = __ddiv_rn(a, __dadd_rn(1.0, qn));\n";
+        }
+        o << "    return a;\n}\n";
+    }
+    auto body = [&](const char* law, const char* indent) {
+        for (int gi = 0; gi < G; ++gi) {
+            for (int k = gi * S; k < std::min(M, gi * S + S); ++k) {
+                const std::string call = std::string(law) + std::to_string(k) + "(x)";
+                if (k == gi * S) o << indent << "g = " << call << ";\n";
+                else o << indent << "g = __dadd_rn(g, " << call << ");\n";
+            }
+            if (gi == 0) o << indent << "P[0] = g;\n";
+            else o << indent << "P[" << gi << "] = __dadd_rn(P[" << gi - 1 << "], g);\n";
+        }
+    };
     o << "__device__ __forceinline__ void smc_sweep(const SmcXCol& X, double (&P)[SMC_SW_G]) {\n";
     o << "    int x[SMC_N];\n#pragma unroll\n    for (int s = 0; s < SMC_N; ++s) x[s] = X[s];\n";
+    o << "    unsigned big = 0u;\n";
+    for (int sp = 0; sp < N; ++sp)
+        if (used[(size_t)sp]) o << "    big |= (unsigned)x[" << sp << "];\n";
     o << "    double g;\n";
-    for (int gi = 0; gi < G; ++gi) {
-        for (int k = gi * S; k < std::min(M, gi * S + S); ++k) {
-            if (k == gi * S) o << "    g = smc_law" << k << "(x);\n";
-            else o << "    g = __dadd_rn(g, smc_law" << k << "(x));\n";
-        }
-        if (gi == 0) o << "    P[0] = g;\n";
-        else o << "    P[" << gi << "] = __dadd_rn(P[" << gi - 1 << "], g);\n";
-    }
-    o << "}\n";
-    (void)N;
+    bool fast = true;
+    if (const char* e = std::getenv("SMC_SW_FAST")) fast = std::atoi(e) != 0;
+    o << "    if (" << (fast ? "" : "false && ") << "(big >> 26) == 0u) {\n";
+    body("smc_lawf", "        ");
+    o << "    } else {\n";
+    body("smc_law", "        ");
+    o << "    }\n}\n";
     return o.str();
 }
 
@@ -736,11 +783,13 @@ std::string generate_source(const Model& m, const Property& p, int variant, cons
     } else if (variant == 4) {
         // 128-thread CTAs; resident CTAs per SM bounded by the counts' shared memory
         // (tables + 128 columns of N+1 ints) and by registers (pass 1 keeps the counts and
-        // the group prefixes in registers): at most 4 by default (<= 128 registers)
+        // the group prefixes in registers): 3 by default (<= 168 registers; C4: 3 -> 1.19e10,
+        // 4 -> 1.14e10, 5 -> 8.8e9 events/s: the sweep's ILP needs the registers)
         const size_t per_cta = tl->bytes + 128 * 4 * (size_t)(m.N + 1) + 64;
-        int minb = (int)std::max<size_t>(1, std::min<size_t>(4, 227 * 1024 / per_cta));
+        int minb = (int)std::max<size_t>(1, std::min<size_t>(3, 227 * 1024 / per_cta));
         if (const char* e = std::getenv("SMC_MINB")) minb = std::atoi(e);
         o << "#define SMC_SWEEP 1\n#define SMC_BLOCK 128\n#define SMC_MINB " << minb << "\n";
+        if (const char* e = std::getenv("SMC_SW_C")) o << "#define SMC_SW_C " << std::max(1, std::atoi(e)) << "\n";
         o << "#define SMC_OFF_X0 " << tl->off_x0 << "\n#define SMC_OFF_LAW " << tl->off_law
           << "\n#define SMC_OFF_HREP " << tl->off_hill_rep << "\n#define SMC_OFF_HK " << tl->off_hill_k
           << "\n#define SMC_OFF_HN " << tl->off_hill_n << "\n#define SMC_OFF_CHG " << tl->off_chg << "\n";

@@ -207,6 +207,10 @@ struct __align__(16) SmcLaw {
 };
 
 #ifdef SMC_SWEEP
+// (double)h for 0 <= h < 2^52, exact: the bit pattern 0x43300000:h is 2^52 + h
+__device__ __forceinline__ double smc_u2d(smc_u64 h) {
+    return __dadd_rn(__longlong_as_double((long long)(h | 0x4330000000000000ull)), -0x1p52);
+}
 // x[s] of this thread's trajectory in the sweep variant: a shared-memory column with
 // stride SMC_BLOCK, so lane l always hits bank l mod 32 (conflict-free for any s)
 struct SmcXCol {

@@ -21,7 +21,7 @@
 // * Selection (Eq. 2b), pass 2: the group g = #{P_i <= u2 a0} by integer compares
 //   of the non-negative doubles' bit patterns, then the member inside g by a
 //   running sum from P_{g-1} over the group's laws read from the smem law table
-//   (per-lane group: a short divergent loop of <= SMC_SW_S laws).
+//   (per-lane group, in chunks of independent law reads; one dependent add chain).
 // * x += v_j from the change table; the monitor reads its atoms from the column.
 //
 // Generated hooks (codegen.cpp): SMC_N, SMC_M, SMC_BLOCK, SMC_MINB, SMC_SW_S, SMC_SW_G,
@@ -82,18 +82,34 @@ __device__ __forceinline__ double smc_law_sw(int k, const SmcXCol& X, const SmcS
 __device__ __forceinline__ smc_i64 smc_ord(double v) { return __double_as_longlong(v); }
 
 // member of group gi: first j with base + a_{j0} + ... + a_j > target (left to right);
-// rounding: the last a_j > 0 of the group, which exists since P_gi > P_{gi-1} (R11)
+// rounding: the last a_j > 0 of the group, which exists since P_gi > P_{gi-1} (R11).
+// Chunks of SMC_SW_C laws: the reads of a chunk are independent (one load latency per
+// chunk), the running sum is the only chain.
+#ifndef SMC_SW_C
+#define SMC_SW_C 4
+#endif
 __device__ __forceinline__ int smc_pick(int gi, double base, double target, const SmcXCol& X, const SmcSwTabs& T) {
     const int j0 = gi * SMC_SW_S;
     const int j1 = min(j0 + SMC_SW_S, SMC_M);
     const smc_i64 tb = smc_ord(target);
     double acc = base;
     int last = j0;
-    for (int j = j0; j < j1; ++j) {
-        const double a = smc_law_sw(j, X, T);
-        acc = __dadd_rn(acc, a);
-        if (smc_ord(a) > 0) last = j;
-        if (smc_ord(acc) > tb) return j;
+    for (int c0 = j0; c0 < j1; c0 += SMC_SW_C) {
+        double av[SMC_SW_C];
+#pragma unroll
+        for (int m = 0; m < SMC_SW_C; ++m) {
+            const int j = c0 + m;
+            const double a = smc_law_sw(min(j, j1 - 1), X, T);
+            av[m] = (j < j1) ? a : 0.0;
+        }
+        int hit = -1;
+#pragma unroll
+        for (int m = 0; m < SMC_SW_C; ++m) {
+            acc = __dadd_rn(acc, av[m]);
+            if (smc_ord(av[m]) > 0) last = c0 + m;
+            if (hit < 0 && smc_ord(acc) > tb) hit = c0 + m;
+        }
+        if (hit >= 0) return hit;
     }
     return last;
 }
