@@ -482,10 +482,102 @@ int sweep_group(const Model& m) {
     return std::min(S, m.M);
 }
 
-std::string model_code_sweep(const Model& m) {
+std::string sweep_code_xd(const Model& m, int S, int G) {
+    std::ostringstream o;
+    const int N = m.N, M = m.M;
+    std::vector<double> cs((size_t)M);
+    std::vector<int> form((size_t)M);     // 0 c, 1 c x, 2 (c/2) x (x-1), 3 c x y, 4 general
+    for (int k = 0; k < M; ++k) {
+        const Reaction& r = m.R[(size_t)k];
+        double c = r.c;
+        int order = 0;
+        for (int q = 0; q < 2; ++q) order += r.s[q] >= 0 ? r.st[q] : 0;
+        int f = 4;
+        if (!r.rate.empty() || order > 2) f = 4;
+        else if (r.s[0] < 0) f = 0;
+        else if (r.s[1] < 0 && r.st[0] == 1) f = 1;
+        else if (r.s[1] < 0) {
+            if ((c * 0.5) * 2.0 == c && c * 0.5 >= 0x1p-1021) { f = 2; c *= 0.5; }   // exact fold
+        } else if (r.st[0] == 1 && r.st[1] == 1) f = 3;
+        form[(size_t)k] = f;
+        cs[(size_t)k] = c;
+    }
+    o << "__constant__ double smc_rc[" << M << "] = {";
+    for (int k = 0; k < M; ++k) o << (k ? ", " : "") << dlit(cs[(size_t)k]);
+    o << "};\n";
+    for (int k = 0; k < M; ++k) {
+        const Reaction& r = m.R[(size_t)k];
+        const std::string K = std::to_string(k);
+        o << "__device__ __forceinline__ double smc_law" << k << "(const double (&x)[SMC_N]) {\n";
+        if (!r.rate.empty()) {
+            o << explicit_body(r, "x", "    ") << "}\n";
+            continue;
+        }
+        const std::string a = std::to_string(r.s[0]), b = std::to_string(r.s[1]);
+        switch (form[(size_t)k]) {
+            case 0: o << "    double v = smc_rc[" << K << "];\n"; break;
+            case 1: o << "    double v = __dmul_rn(smc_rc[" << K << "], x[" << a << "]);\n"; break;
+            case 2: o << "    double v = __dmul_rn(smc_rc[" << K << "], __dmul_rn(x[" << a << "], __dadd_rn(x[" << a
+                      << "], -1.0)));\n"; break;
+            case 3: o << "    double v = __dmul_rn(smc_rc[" << K << "], __dmul_rn(x[" << a << "], x[" << b << "]));\n"; break;
+            default: {                                   // order 3-4 / unfoldable homodimer: exact int64 h
+                std::vector<std::string> terms;
+                for (int q = 0; q < 2; ++q) {
+                    if (r.s[q] < 0) continue;
+                    std::string xs = "(smc_i64)x[" + std::to_string(r.s[q]) + "]";
+                    terms.push_back(r.st[q] == 1 ? xs : "((" + xs + " * (" + xs + " - 1LL)) / 2LL)");
+                }
+                std::string h = terms.size() == 1 ? terms[0] : "(" + terms[0] + " * " + terms[1] + ")";
+                o << "    double v = __dmul_rn(smc_rc[" << K << "], (double)(" << h << "));\n";
+            }
+        }
+        if (r.hill) {
+            o << "    const double q = __ddiv_rn(x[" << r.rep << "], " << dlit(r.K) << ");\n";
+            o << "    double qn = q;\n";
+            for (int i = 1; i < r.n; ++i) o << "    qn = __dmul_rn(qn, q);\n";
+            o << "    v = __ddiv_rn(v, __dadd_rn(1.0, qn));\n";
+        }
+        o << "    return v;\n}\n";
+    }
+    bool any_explicit = false;
+    for (auto& r : m.R) any_explicit |= !r.rate.empty();
+    if (any_explicit) {
+        o << "__device__ __noinline__ double smc_explicit4(int k, const SmcXCol& xs) {\n    switch (k) {\n";
+        for (int k = 0; k < M; ++k)
+            if (!m.R[(size_t)k].rate.empty())
+                o << "    case " << k << ":\n" << explicit_body(m.R[(size_t)k], "xs", "        ");
+        o << "    }\n    return 0.0;\n}\n";
+    }
+    o << "__device__ __forceinline__ void smc_sweep(const SmcXCol& X, double (&P)[SMC_SW_G]) {\n";
+    o << "    double x[SMC_N];\n#pragma unroll\n    for (int s = 0; s < SMC_N; ++s) x[s] = X[s];\n    double g;\n";
+    for (int gi = 0; gi < G; ++gi) {
+        for (int k = gi * S; k < std::min(M, gi * S + S); ++k) {
+            if (k == gi * S) o << "    g = smc_law" << k << "(x);\n";
+            else o << "    g = __dadd_rn(g, smc_law" << k << "(x));\n";
+        }
+        if (gi == 0) o << "    P[0] = g;\n";
+        else o << "    P[" << gi << "] = __dadd_rn(P[" << gi - 1 << "], g);\n";
+    }
+    o << "}\n";
+    (void)N;
+    return o.str();
+}
+
+// Counts as binary64 columns (SMC_SW_XD): the laws are plain fp64 products of the
+// counts (exact integers, < 2^31), identical to the int64 forms: fl(x0 x1) is the
+// rounding of the exact product either way, and x (x - 1) with the 1/2 folded into
+// c (reading R20); no conversion per law.
+bool sweep_xd_impl(const Model& m, size_t table_bytes) {
+    bool xd = table_bytes + 128 * 8 * (size_t)(m.N + 1) <= 72 * 1024;     // 3 CTAs per SM
+    if (const char* e = std::getenv("SMC_SW_XD")) xd = std::atoi(e) != 0;
+    return xd;
+}
+
+std::string model_code_sweep(const Model& m, bool xd) {
     std::ostringstream o;
     const int N = m.N, M = m.M, S = sweep_group(m), G = (M + S - 1) / S;
     o << "#define SMC_SW_S " << S << "\n#define SMC_SW_G " << G << "\n";
+    if (xd) return o.str() + sweep_code_xd(m, S, G);
     o << "__constant__ double smc_rc[" << M << "] = {";
     for (int k = 0; k < M; ++k) o << (k ? ", " : "") << dlit(m.R[(size_t)k].c);
     o << "};\n";
@@ -580,6 +672,8 @@ std::string model_code_sweep(const Model& m) {
 size_t align16(size_t v) { return (v + 15) & ~(size_t)15; }
 
 }  // namespace
+
+bool sweep_xd(const Model& m, size_t table_bytes) { return sweep_xd_impl(m, table_bytes); }
 
 // --------------------------------------------------- variant 1 tables ---
 HillTables pack_hill_tables(const Model& m) {
@@ -785,10 +879,11 @@ std::string generate_source(const Model& m, const Property& p, int variant, cons
         // (tables + 128 columns of N+1 ints) and by registers (pass 1 keeps the counts and
         // the group prefixes in registers): 3 by default (<= 168 registers; C4: 3 -> 1.19e10,
         // 4 -> 1.14e10, 5 -> 8.8e9 events/s: the sweep's ILP needs the registers)
-        const size_t per_cta = tl->bytes + 128 * 4 * (size_t)(m.N + 1) + 64;
+        const size_t per_cta = tl->bytes + 128 * (sweep_xd_impl(m, tl->bytes) ? 8 : 4) * (size_t)(m.N + 1) + 64;
         int minb = (int)std::max<size_t>(1, std::min<size_t>(3, 227 * 1024 / per_cta));
         if (const char* e = std::getenv("SMC_MINB")) minb = std::atoi(e);
         o << "#define SMC_SWEEP 1\n#define SMC_BLOCK 128\n#define SMC_MINB " << minb << "\n";
+        o << "#define SMC_SW_XD " << (sweep_xd_impl(m, tl->bytes) ? 1 : 0) << "\n";
         if (const char* e = std::getenv("SMC_SW_C")) o << "#define SMC_SW_C " << std::max(1, std::atoi(e)) << "\n";
         o << "#define SMC_OFF_X0 " << tl->off_x0 << "\n#define SMC_OFF_LAW " << tl->off_law
           << "\n#define SMC_OFF_HREP " << tl->off_hill_rep << "\n#define SMC_OFF_HK " << tl->off_hill_k
@@ -821,7 +916,7 @@ std::string generate_source(const Model& m, const Property& p, int variant, cons
     }
     o << embedded_source("ssa_common.cuh") << "\n";
     if (variant == 1 || variant == 3) o << model_code_thread(m) << "\n";
-    if (variant == 4) o << model_code_sweep(m) << "\n";
+    if (variant == 4) o << model_code_sweep(m, sweep_xd_impl(m, tl->bytes)) << "\n";
     if (variant == 2 && tl->any_explicit) {          // explicit laws of the tile variant
         o << "__device__ __noinline__ double smc_explicit(int k, const int* xs) {\n    switch (k) {\n";
         for (int k = 0; k < m.M; ++k)

@@ -212,9 +212,14 @@ __device__ __forceinline__ double smc_u2d(smc_u64 h) {
     return __dadd_rn(__longlong_as_double((long long)(h | 0x4330000000000000ull)), -0x1p52);
 }
 // x[s] of this thread's trajectory in the sweep variant: a shared-memory column with
-// stride SMC_BLOCK, so lane l always hits bank l mod 32 (conflict-free for any s)
+// stride SMC_BLOCK, so lane l always hits bank(s) l mod 32 (conflict-free for any s)
+#if SMC_SW_XD
+typedef double smc_xt;          // counts as binary64 (exact integers < 2^31)
+#else
+typedef int smc_xt;
+#endif
 struct SmcXCol {
-    int* p;
-    __device__ __forceinline__ int operator[](int s) const { return p[s * SMC_BLOCK]; }
+    smc_xt* p;
+    __device__ __forceinline__ smc_xt operator[](int s) const { return p[s * SMC_BLOCK]; }
 };
 #endif

@@ -7,6 +7,9 @@
 //   every access -- uniform s in the sweep, per-lane s in the selection and the
 //   update -- hits bank (tid mod 32): conflict-free whatever the species.
 //   x[N] = 1 is a constant column (operand of h = x * 1 in the law table).
+//   SMC_SW_XD: the counts are stored as binary64 (exact integers < 2^31; the
+//   count-overflow test of R17 is x > 2^31 - 1), so the laws are fp64 products
+//   with no int -> fp64 conversion; otherwise int32 columns.
 // * Model tables (law table, change lists, Hill parameters) are staged once per CTA
 //   by a TMA bulk copy (cp.async.bulk + mbarrier), as in the tile variant.
 // * Per event, pass 1 (generated straight-line code, smc_sweep): every law a_k(x)
@@ -51,20 +54,32 @@ __device__ __forceinline__ double smc_law_sw(int k, const SmcXCol& X, const SmcS
 #if SMC_ANY_EXPLICIT
     if (kind == 5) return smc_explicit4(k, X);
 #endif
+#if SMC_SW_XD
+    const double v0 = X[(int)(L.u0 & 0xFFFFu)];
+    const double v1 = X[(int)(L.u1 & 0xFFFFu)];
+#else
     const int v0 = X[(int)(L.u0 & 0xFFFFu)];
     const int v1 = X[(int)(L.u1 & 0xFFFFu)];
+#endif
     double h;
 #if SMC_ANY_GENERAL
     if (kind == 4) {
-        const smc_i64 y0 = v0, y1 = v1;
+        const smc_i64 y0 = (smc_i64)v0, y1 = (smc_i64)v1;
         const smc_i64 h0 = ((L.u0 >> 20) & 3u) == 1u ? y0 : (y0 * (y0 - 1)) / 2;
         const smc_i64 h1 = ((L.u1 >> 16) & 3u) == 1u ? y1 : (y1 * (y1 - 1)) / 2;
         h = (double)(h0 * h1);
     } else
 #endif
     {
+#if SMC_SW_XD
+        // fl(x0 x1) = the rounding of the exact product; kind 2: x (x - 1), -0 for x = 0
+        // exactly as the generated pass-1 law
+        const double xb = (kind == 2) ? __dadd_rn(v0, -1.0) : v1;
+        h = __dmul_rn(v0, xb);
+#else
         const int xb = (kind == 2) ? max(v0 - 1, 0) : v1;
         h = (double)((smc_i64)v0 * (smc_i64)xb);          // exact product, one rounding
+#endif
     }
     double a = __dmul_rn(L.c, h);
 #if SMC_ANY_HILL
@@ -144,9 +159,9 @@ extern "C" __global__ void __launch_bounds__(SMC_BLOCK, SMC_MINB) smc_ssa_sweep(
     T.hill_k = (const double*)(smem + SMC_OFF_HK);
     T.hill_n = (const int*)(smem + SMC_OFF_HN);
     T.chg = (const unsigned short*)(smem + SMC_OFF_CHG);
-    int* const xcol = (int*)(smem + SMC_TAB_BYTES) + threadIdx.x;
+    smc_xt* const xcol = (smc_xt*)(smem + SMC_TAB_BYTES) + threadIdx.x;
     const SmcXCol X{xcol};
-    xcol[SMC_N * SMC_BLOCK] = 1;                        // x[N] = 1
+    xcol[SMC_N * SMC_BLOCK] = (smc_xt)1;                // x[N] = 1
 
     const smc_u32 cap = (smc_u32)(P.event_cap < 0xFFFFFFFFull ? P.event_cap : 0xFFFFFFFFull);
     double t = 0.0, tp = 0.0;
@@ -174,7 +189,7 @@ extern "C" __global__ void __launch_bounds__(SMC_BLOCK, SMC_MINB) smc_ssa_sweep(
                     exhausted = true;
                 } else {
                     traj = P.first + rel;
-                    for (int s = 0; s < SMC_N; ++s) xcol[s * SMC_BLOCK] = T.x0[s];
+                    for (int s = 0; s < SMC_N; ++s) xcol[s * SMC_BLOCK] = (smc_xt)T.x0[s];
                     t = 0.0;
                     tp = 0.0;
                     k = 0;
@@ -238,9 +253,14 @@ extern "C" __global__ void __launch_bounds__(SMC_BLOCK, SMC_MINB) smc_ssa_sweep(
                     for (int q = 0; q < 4; ++q) {
                         const unsigned e = ((q < 2 ? ce.x : ce.y) >> (16 * (q & 1))) & 0xFFFFu;
                         if (e != 0xFFFFu) {
-                            int* xp = xcol + (int)(e >> 4) * SMC_BLOCK;
+                            smc_xt* xp = xcol + (int)(e >> 4) * SMC_BLOCK;
+#if SMC_SW_XD
+                            const double nv = __dadd_rn(*xp, (double)((int)(e & 15u) - 8));   // exact
+                            ovf |= nv > 2147483647.0;
+#else
                             const int nv = (int)((unsigned)*xp + (unsigned)((int)(e & 15u) - 8));
                             ovf |= nv < 0;
+#endif
                             *xp = nv;
                         }
                     }

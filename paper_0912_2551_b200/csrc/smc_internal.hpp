@@ -171,6 +171,7 @@ struct HillTables {
 };
 HillTables pack_hill_tables(const Model& m);
 std::string generate_source(const Model& m, const Property& p, int variant, const TileLayout* tl);
+bool sweep_xd(const Model& m, size_t table_bytes);   // variant 4: counts as binary64 columns
 std::string embedded_source(const char* name);   // kernels/*.cuh embedded at build time
 
 // -------------------------------------------------------------------- jit ---
