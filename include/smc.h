@@ -67,8 +67,9 @@ typedef struct smc_model smc_model;
  *   P:141-143 and reading R8).  A species listed twice as reactant is merged
  *   (A + A == 2A); merged stoichiometry must be <= 2.
  * Null reactions (v_j = 0) are allowed and fire as events (reading G3).
- * The kernel variant (register-resident thread-owned vs warp-owned tile) is
- * chosen from (N, M); see smc_model_set_variant.
+ * The kernel variant (register-resident thread-owned, thread-owned sweep with
+ * the counts in shared memory, or warp-owned tile) is chosen from (N, M); see
+ * smc_model_set_variant.
  * Errors: SMC_E_ARG (NULL / sizes), SMC_E_MODEL (validation, all violations). */
 int smc_model_create(int32_t n_species, const int32_t* init_counts,
                      int32_t n_reactions,
@@ -92,10 +93,15 @@ int smc_model_set_hill(smc_model* m, int32_t reaction, int32_t repressor, double
  * position) / SMC_E_ARG otherwise. */
 int smc_model_set_rate_expr(smc_model* m, int32_t reaction, const char* expr, const char* const* species_names);
 
-/* Force a kernel variant: 0 = automatic, 1 = thread-owned (registers;
- * requires N <= 32 and M <= 32), 2 = warp-owned tile (shared memory).
- * Variant 1 and 2 compute the same replicas; they differ only in where the
- * state lives.  SMC_E_ARG if the variant cannot hold the model. */
+/* Force a kernel variant: 0 = automatic (1 for N, M <= 32; 4 for N <= 64,
+ * M <= 512; else 2), 1 = thread-owned (registers; requires N <= 32 and
+ * M <= 32), 2 = warp-owned tile (propensities and counts in shared memory,
+ * dependency graph), 4 = thread-owned sweep (counts in a shared-memory column,
+ * every law re-evaluated per event; requires the counts of 128 trajectories to
+ * fit in shared memory).  3 (buffered trace + literal |=) is not selectable: it
+ * is chosen by the formula.  All variants compute the same replicas up to the
+ * ulp-level summation orders of reading R12.  SMC_E_ARG if the
+ * variant cannot hold the model. */
 int smc_model_set_variant(smc_model* m, int32_t variant);
 
 /* Per-replica event cap (default 2^31 - 1): a replica reaching it undecided is
@@ -245,7 +251,7 @@ int smc_philox_blocks(uint64_t seed, uint64_t trajectory, uint64_t step0, uint32
 int smc_draw_blocks(uint64_t seed, uint64_t trajectory, uint64_t step0, uint32_t n, double* host_out);
 
 typedef struct {
-    int32_t variant;          /* 1 thread-owned, 2 warp-owned tile                 */
+    int32_t variant;          /* 1 thread-owned, 2 tile, 3 literal, 4 sweep        */
     int32_t block_threads;    /* threads per CTA                                    */
     int32_t grid_blocks;      /* persistent CTAs                                    */
     int32_t smem_bytes;       /* dynamic shared memory per CTA                      */
