@@ -673,7 +673,6 @@ size_t align16(size_t v) { return (v + 15) & ~(size_t)15; }
 
 }  // namespace
 
-bool sweep_xd(const Model& m, size_t table_bytes) { return sweep_xd_impl(m, table_bytes); }
 
 // --------------------------------------------------- variant 1 tables ---
 HillTables pack_hill_tables(const Model& m) {
@@ -795,6 +794,7 @@ TileLayout pack_tables(const Model& m, bool sweep) {
         uint32_t w1 = s1 | ((uint32_t)(r.s[1] >= 0 ? r.st[1] : 1) << 16);
 
         L.any_explicit |= kind == 5;
+        L.any_general |= kind == 4;                     // incl. a homodimer with a subnormal rate
         if (r.hill) w0 |= 0x80000000u;
         fat_meta[(size_t)j] = s0 | (s1 << 12) | (kind << 24) | ((uint32_t)(r.s[0] >= 0 && r.st[0] == 2) << 27) |
                               ((uint32_t)(r.s[1] >= 0 && r.st[1] == 2) << 28) | ((uint32_t)r.hill << 31);
@@ -815,7 +815,47 @@ TileLayout pack_tables(const Model& m, bool sweep) {
             chg[4 * j + q] = e;
         }
     }
-    if (sweep) return L;                           // variant 4: no dependency graph
+    if (sweep) {                                   // variant 4: no dependency graph
+        // sweep law table: {u0 = column byte offset of s0 | flags, u1 = offset of s1, c},
+        // padded with zero-rate entries to G*S so that every group has S members.
+        // flags: bit 0 homodimer (h = x (x - 1), c halved as above), bit 1 general law
+        // (order 3-4, explicit, Hill: the kernel takes the law-table path)
+        L.sw_s = sweep_group(m);
+        L.sw_c = 1;
+        for (int c : {4, 3, 2})
+            if (L.sw_s % c == 0) { L.sw_c = c; break; }
+        if (const char* e = std::getenv("SMC_SW_C")) {
+            const int c = std::atoi(e);
+            if (c >= 1 && L.sw_s % c == 0) L.sw_c = c;
+        }
+        const int G = (M + L.sw_s - 1) / L.sw_s;
+        L.off_swlaw = align16(L.bytes);
+        const size_t nb = L.off_swlaw + 16 * (size_t)G * L.sw_s;
+        L.sw_xd = sweep_xd_impl(m, nb);
+        const uint32_t col = 128u * (L.sw_xd ? 8u : 4u);
+        L.blob.resize(nb, 0);
+        L.bytes = nb;
+        for (int j = 0; j < G * L.sw_s; ++j) {
+            uint32_t u0 = (uint32_t)N * col, u1 = (uint32_t)N * col;
+            double c = 0.0;
+            if (j < M) {
+                uint32_t w0, w1;
+                std::memcpy(&w0, L.blob.data() + L.off_law + 16 * (size_t)j, 4);
+                std::memcpy(&w1, L.blob.data() + L.off_law + 16 * (size_t)j + 4, 4);
+                std::memcpy(&c, L.blob.data() + L.off_law + 16 * (size_t)j + 8, 8);
+                const uint32_t kind = (w0 >> 16) & 7u;
+                u0 = (w0 & 0xFFFFu) * col;
+                u1 = (w1 & 0xFFFFu) * col;
+                if (kind == 2) u0 |= 1u;
+                if (kind >= 4 || (w0 & 0x80000000u)) u0 |= 2u;
+            }
+            unsigned char* e = L.blob.data() + L.off_swlaw + 16 * (size_t)j;
+            std::memcpy(e, &u0, 4);
+            std::memcpy(e + 4, &u1, 4);
+            std::memcpy(e + 8, &c, 8);
+        }
+        return L;
+    }
     if ((size_t)L.gs * L.tw > 65536) fail(SMC_E_MODEL, "tile variant: too many reactions for 16-bit slots");
     auto* doff = (uint32_t*)(L.blob.data() + L.off_dep_off);
     auto* dep = (uint32_t*)(L.blob.data() + L.off_dep);
@@ -879,12 +919,13 @@ std::string generate_source(const Model& m, const Property& p, int variant, cons
         // (tables + 128 columns of N+1 ints) and by registers (pass 1 keeps the counts and
         // the group prefixes in registers): 3 by default (<= 168 registers; C4: 3 -> 1.19e10,
         // 4 -> 1.14e10, 5 -> 8.8e9 events/s: the sweep's ILP needs the registers)
-        const size_t per_cta = tl->bytes + 128 * (sweep_xd_impl(m, tl->bytes) ? 8 : 4) * (size_t)(m.N + 1) + 64;
+        const size_t per_cta = tl->bytes + 128 * (tl->sw_xd ? 8 : 4) * (size_t)(m.N + 1) + 64;
         int minb = (int)std::max<size_t>(1, std::min<size_t>(3, 227 * 1024 / per_cta));
         if (const char* e = std::getenv("SMC_MINB")) minb = std::atoi(e);
         o << "#define SMC_SWEEP 1\n#define SMC_BLOCK 128\n#define SMC_MINB " << minb << "\n";
-        o << "#define SMC_SW_XD " << (sweep_xd_impl(m, tl->bytes) ? 1 : 0) << "\n";
-        if (const char* e = std::getenv("SMC_SW_C")) o << "#define SMC_SW_C " << std::max(1, std::atoi(e)) << "\n";
+        o << "#define SMC_SW_XD " << (tl->sw_xd ? 1 : 0) << "\n#define SMC_OFF_SWLAW " << tl->off_swlaw
+          << "\n#define SMC_SW_C " << tl->sw_c << "\n";
+        o << "#define SMC_SW_ANYGEN " << ((tl->any_hill || tl->any_general || tl->any_explicit) ? 1 : 0) << "\n";
         o << "#define SMC_OFF_X0 " << tl->off_x0 << "\n#define SMC_OFF_LAW " << tl->off_law
           << "\n#define SMC_OFF_HREP " << tl->off_hill_rep << "\n#define SMC_OFF_HK " << tl->off_hill_k
           << "\n#define SMC_OFF_HN " << tl->off_hill_n << "\n#define SMC_OFF_CHG " << tl->off_chg << "\n";
@@ -916,7 +957,7 @@ std::string generate_source(const Model& m, const Property& p, int variant, cons
     }
     o << embedded_source("ssa_common.cuh") << "\n";
     if (variant == 1 || variant == 3) o << model_code_thread(m) << "\n";
-    if (variant == 4) o << model_code_sweep(m, sweep_xd_impl(m, tl->bytes)) << "\n";
+    if (variant == 4) o << model_code_sweep(m, tl->sw_xd) << "\n";
     if (variant == 2 && tl->any_explicit) {          // explicit laws of the tile variant
         o << "__device__ __noinline__ double smc_explicit(int k, const int* xs) {\n    switch (k) {\n";
         for (int k = 0; k < m.M; ++k)

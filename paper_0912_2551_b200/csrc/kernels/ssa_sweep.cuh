@@ -37,7 +37,8 @@
 
 struct SmcSwTabs {
     const int* x0;
-    const SmcLaw* law;
+    const SmcLaw* law;               // tile-format law table (general laws)
+    const SmcLaw* swlaw;             // sweep-format law table, G*S entries
     const int* hill_rep;
     const double* hill_k;
     const int* hill_n;
@@ -48,7 +49,8 @@ struct SmcSwTabs {
 // operations as the generated pass-1 law, so both passes see identical values:
 // order <= 2: h = fl(x0 * x1) (x[N] = 1 for the missing operand), kind 2 as
 // fl(x (x-1)) with the 1/2 folded into c; order 3-4: exact int64 binomials.
-__device__ __forceinline__ double smc_law_sw(int k, const SmcXCol& X, const SmcSwTabs& T) {
+// General path (order 3-4, explicit rates, Hill): the tile-format law table.
+__device__ __noinline__ double smc_law_gen(int k, const SmcXCol& X, const SmcSwTabs& T) {
     const SmcLaw L = T.law[k];
     const int kind = (int)((L.u0 >> 16) & 7u);
 #if SMC_ANY_EXPLICIT
@@ -62,23 +64,18 @@ __device__ __forceinline__ double smc_law_sw(int k, const SmcXCol& X, const SmcS
     const int v1 = X[(int)(L.u1 & 0xFFFFu)];
 #endif
     double h;
-#if SMC_ANY_GENERAL
     if (kind == 4) {
         const smc_i64 y0 = (smc_i64)v0, y1 = (smc_i64)v1;
         const smc_i64 h0 = ((L.u0 >> 20) & 3u) == 1u ? y0 : (y0 * (y0 - 1)) / 2;
         const smc_i64 h1 = ((L.u1 >> 16) & 3u) == 1u ? y1 : (y1 * (y1 - 1)) / 2;
         h = (double)(h0 * h1);
-    } else
-#endif
-    {
+    } else {
 #if SMC_SW_XD
-        // fl(x0 x1) = the rounding of the exact product; kind 2: x (x - 1), -0 for x = 0
-        // exactly as the generated pass-1 law
         const double xb = (kind == 2) ? __dadd_rn(v0, -1.0) : v1;
         h = __dmul_rn(v0, xb);
 #else
         const int xb = (kind == 2) ? max(v0 - 1, 0) : v1;
-        h = (double)((smc_i64)v0 * (smc_i64)xb);          // exact product, one rounding
+        h = (double)((smc_i64)v0 * (smc_i64)xb);
 #endif
     }
     double a = __dmul_rn(L.c, h);
@@ -93,40 +90,57 @@ __device__ __forceinline__ double smc_law_sw(int k, const SmcXCol& X, const SmcS
     return a;
 }
 
+// Sweep-format entry: u0 = byte offset of the column of s0 | flags (bit 0 homodimer,
+// bit 1 general law), u1 = byte offset of the column of s1, c = rate (halved for a
+// homodimer); entries past M are zero-rate padding (a = 0).
+__device__ __forceinline__ double smc_law_sw(int k, const SmcXCol& X, const SmcSwTabs& T) {
+    const SmcLaw L = T.swlaw[k];
+#if SMC_SW_ANYGEN
+    if (L.u0 & 2u) return smc_law_gen(k, X, T);
+#endif
+    const char* xb = (const char*)X.p;
+    const smc_xt v0 = *(const smc_xt*)(xb + (L.u0 & ~511u));
+    const smc_xt v1 = *(const smc_xt*)(xb + L.u1);
+#if SMC_SW_XD
+    const double h = __dmul_rn(v0, __dadd_rn(v1, (L.u0 & 1u) ? -1.0 : 0.0));   // exact shift by 0 / -1
+#else
+    const double h = (double)((smc_i64)v0 * (smc_i64)(v1 - (int)(L.u0 & 1u)));
+#endif
+    return __dmul_rn(L.c, h);
+}
+
 // non-negative doubles (and -0) order like their bit patterns as signed int64
 __device__ __forceinline__ smc_i64 smc_ord(double v) { return __double_as_longlong(v); }
 
-// member of group gi: first j with base + a_{j0} + ... + a_j > target (left to right);
-// rounding: the last a_j > 0 of the group, which exists since P_gi > P_{gi-1} (R11).
+// member of group gi: first j with base + a_{j0} + ... + a_j > target (left to right).
 // Chunks of SMC_SW_C laws: the reads of a chunk are independent (one load latency per
-// chunk), the running sum is the only chain.
-#ifndef SMC_SW_C
-#define SMC_SW_C 4
+// chunk), the running sum is the only chain; inside a chunk the member is the count of
+// prefixes <= target (the prefixes are non-decreasing).  Rounding (no prefix exceeds the
+// target although P_gi does): the last a_j > 0 of the group (R11), re-evaluated.
+#if SMC_SW_S % SMC_SW_C != 0
+#error "SMC_SW_C must divide SMC_SW_S"
 #endif
 __device__ __forceinline__ int smc_pick(int gi, double base, double target, const SmcXCol& X, const SmcSwTabs& T) {
     const int j0 = gi * SMC_SW_S;
-    const int j1 = min(j0 + SMC_SW_S, SMC_M);
     const smc_i64 tb = smc_ord(target);
     double acc = base;
-    int last = j0;
-    for (int c0 = j0; c0 < j1; c0 += SMC_SW_C) {
+#pragma unroll 1
+    for (int c0 = j0; c0 < j0 + SMC_SW_S; c0 += SMC_SW_C) {
         double av[SMC_SW_C];
 #pragma unroll
-        for (int m = 0; m < SMC_SW_C; ++m) {
-            const int j = c0 + m;
-            const double a = smc_law_sw(min(j, j1 - 1), X, T);
-            av[m] = (j < j1) ? a : 0.0;
-        }
-        int hit = -1;
+        for (int m = 0; m < SMC_SW_C; ++m) av[m] = smc_law_sw(c0 + m, X, T);
+        int cnt = 0;
 #pragma unroll
         for (int m = 0; m < SMC_SW_C; ++m) {
             acc = __dadd_rn(acc, av[m]);
-            if (smc_ord(av[m]) > 0) last = c0 + m;
-            if (hit < 0 && smc_ord(acc) > tb) hit = c0 + m;
+            cnt += (smc_ord(acc) <= tb) ? 1 : 0;
         }
-        if (hit >= 0) return hit;
+        if (cnt < SMC_SW_C) return c0 + cnt;
     }
-    return last;
+#pragma unroll 1
+    for (int j = j0 + SMC_SW_S - 1; j > j0; --j)
+        if (smc_law_sw(j, X, T) > 0.0) return j;
+    return j0;
 }
 
 // rounding with u2 a0 >= every prefix: the last reaction with a_j > 0 (reading R11)
@@ -155,6 +169,7 @@ extern "C" __global__ void __launch_bounds__(SMC_BLOCK, SMC_MINB) smc_ssa_sweep(
     SmcSwTabs T;
     T.x0 = (const int*)(smem + SMC_OFF_X0);
     T.law = (const SmcLaw*)(smem + SMC_OFF_LAW);
+    T.swlaw = (const SmcLaw*)(smem + SMC_OFF_SWLAW);
     T.hill_rep = (const int*)(smem + SMC_OFF_HREP);
     T.hill_k = (const double*)(smem + SMC_OFF_HK);
     T.hill_n = (const int*)(smem + SMC_OFF_HN);

@@ -227,7 +227,7 @@ PropKernel& prepare(Model& m, const Property& p) {
         alloc_traces(m, p, pk, pk.block);
     } else if (pk.variant == 4) {
         pk.block = 128;
-        pk.smem = (int)(tl->bytes + (size_t)pk.block * (sweep_xd(m, tl->bytes) ? 8 : 4) * (size_t)(m.N + 1));
+        pk.smem = (int)(tl->bytes + (size_t)pk.block * (tl->sw_xd ? 8 : 4) * (size_t)(m.N + 1));
         cudaFuncAttributes fa;
         ck(cudaFuncGetAttributes(&fa, fn), "cudaFuncGetAttributes");
         if ((size_t)pk.smem + fa.sharedSizeBytes > (size_t)d.max_smem_optin)

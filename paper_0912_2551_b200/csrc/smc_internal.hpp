@@ -158,6 +158,10 @@ struct TileLayout {               // packed model tables (variant 2), byte offse
     bool depsp = false;           // species-indexed reader CSR instead of dep(j) (TW = 32)
     bool fatdep = false;          // 16-byte dependency entries carrying the law (meta, rate)
     bool any_explicit = false;    // an explicit rate expression (generated smc_explicit)
+    // variant 4 (sweep): law table in the sweep format, padded to G*S entries
+    size_t off_swlaw = 0;
+    int sw_s = 0, sw_c = 0;       // laws per group, independent law reads per chunk
+    bool sw_xd = false;           // counts as binary64 columns
     int max_dep = 0;
     std::vector<uint8_t> blob;    // host copy
 };
@@ -171,7 +175,6 @@ struct HillTables {
 };
 HillTables pack_hill_tables(const Model& m);
 std::string generate_source(const Model& m, const Property& p, int variant, const TileLayout* tl);
-bool sweep_xd(const Model& m, size_t table_bytes);   // variant 4: counts as binary64 columns
 std::string embedded_source(const char* name);   // kernels/*.cuh embedded at build time
 
 // -------------------------------------------------------------------- jit ---

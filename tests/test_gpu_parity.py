@@ -170,6 +170,37 @@ def test_edge_cases(smc):
     assert a >= AGREE and ae >= AGREE
 
 
+@pytest.mark.parametrize("variant,xd", [(1, None), (2, None), (4, "1"), (4, "0")])
+def test_edge_cases_every_variant(smc, variant, xd, monkeypatch):
+    """Edge cases on every kernel family (sweep with binary64 and int32 count columns):
+    absorbing start, event cap, count overflow (R17), and counts >= 2^26 whose products
+    exceed 2^53 (int64 -> double rounding; the sweep's int32 columns take their general
+    conversion path) replica for replica against the oracle."""
+    if xd is not None:
+        monkeypatch.setenv("SMC_SW_XD", xd)
+    z = dict(workloads.c1(), x0=[0])
+    m0, p0 = _pair(smc, z, variant)
+    assert m0.run(p0, 1000, 3) == dict(n_true=1000, n_false=0, events=0, errors=0)
+    assert m0.last_launch(p0)["variant"] == variant
+    m2, p2 = _pair(smc, workloads.c2(), variant)
+    m2.set_event_cap(5)
+    c = m2.run(p2, 100, 2)
+    assert c["errors"] == 100 and c["events"] == 500
+    big = dict(species=["A"], x0=[2147483640], reactions=[dict(reactants=[], products=[[0, 2]], rate=1.0, hill=None)],
+               formula="F[0,100](A < 0)")
+    m3, p3 = _pair(smc, big, variant)
+    c = m3.run(p3, 50, 1)
+    assert c["errors"] == 50 and c["events"] == 50 * 3
+    rx = workloads._rx
+    huge = dict(name="huge", species=["A", "B", "C"], x0=[200000000, 100000000, 0],
+                reactions=[rx([(0, 1), (1, 1)], [(2, 1)], 3e-16), rx([(0, 2)], [(1, 1)], 1e-16),
+                           rx([(2, 1)], [], 0.5), rx([], [(0, 1)], 2.0)],
+                formula="F[0,3](C >= 12)", t_max=0.0, seed=8, sampling=dict(mode="fixed", n=400))
+    a, ae, v, e, ov, oe = _compare(smc, huge, 8, 0, 400, variant)
+    assert ae >= 399 / 400, (variant, xd, a, ae)
+    assert 0.05 < v.mean() < 0.95 and e.mean() > 10
+
+
 @pytest.mark.parametrize("formula", [
     "G[0,1](A >= 8)", "(A >= 7) U[0.2,1.5] (A <= 5)", "X[0,0.3](A == 9)", "F[0,1] G[0,0.5](A <= 6)",
     "G[0,1.5] F[0,0.3](A >= 5)", "(G[0,0.5](A > 3)) U[0,2] (A <= 6)", "F(0.5,2](A == 7) & !G[0,0.2](A == 10)",
