@@ -477,7 +477,11 @@ std::string model_code_thread(const Model& m) {
 // table of pass 2 (ssa_sweep.cuh smc_law_sw): exact int64 h, one rounding to double,
 // a = c * h, Hill as in variant 1 (computed, not tabulated).
 int sweep_group(const Model& m) {
-    int S = 12;     // C4 (M = 200): S = 8 8.6e9, 12 1.14e10, 16 1.07e10, 20 1.08e10 events/s
+    // small groups keep the in-group selection one chunk of independent law reads; the
+    // G = M/S prefixes live in registers, so S grows with M beyond ~29 groups.  C4 (M = 200,
+    // events/s): S:C = 7:7 1.63e10, 5:5 1.61e10, 6:6 1.60e10, 10:5 1.60e10, 12:4 1.50e10,
+    // 16:4 1.22e10
+    int S = std::max(7, (m.M + 28) / 29);
     if (const char* e = std::getenv("SMC_SW_S")) S = std::max(1, std::atoi(e));
     return std::min(S, m.M);
 }
@@ -549,12 +553,19 @@ std::string sweep_code_xd(const Model& m, int S, int G) {
         o << "    }\n    return 0.0;\n}\n";
     }
     o << "__device__ __forceinline__ void smc_sweep(const SmcXCol& X, double (&P)[SMC_SW_G]) {\n";
-    o << "    double x[SMC_N];\n#pragma unroll\n    for (int s = 0; s < SMC_N; ++s) x[s] = X[s];\n    double g;\n";
+    o << "    double x[SMC_N];\n#pragma unroll\n    for (int s = 0; s < SMC_N; ++s) x[s] = X[s];\n    double g, h;\n";
+    // a group sum is SPLIT interleaved partial sums (members m = r mod SPLIT, each left
+    // to right) added in order -- a fixed order (reading R12) with a shorter add chain
+    int split = 1;
+    if (const char* e = std::getenv("SMC_SW_SPLIT")) split = std::max(1, std::min(2, std::atoi(e)));
     for (int gi = 0; gi < G; ++gi) {
-        for (int k = gi * S; k < std::min(M, gi * S + S); ++k) {
-            if (k == gi * S) o << "    g = smc_law" << k << "(x);\n";
-            else o << "    g = __dadd_rn(g, smc_law" << k << "(x));\n";
+        const int k0 = gi * S, k1 = std::min(M, gi * S + S);
+        for (int k = k0; k < k1; ++k) {
+            const char* acc = (split == 2 && ((k - k0) & 1)) ? "h" : "g";
+            if (k - k0 < split) o << "    " << acc << " = smc_law" << k << "(x);\n";
+            else o << "    " << acc << " = __dadd_rn(" << acc << ", smc_law" << k << "(x));\n";
         }
+        if (split == 2 && k1 - k0 > 1) o << "    g = __dadd_rn(g, h);\n";
         if (gi == 0) o << "    P[0] = g;\n";
         else o << "    P[" << gi << "] = __dadd_rn(P[" << gi - 1 << "], g);\n";
     }
@@ -822,8 +833,10 @@ TileLayout pack_tables(const Model& m, bool sweep) {
         // (order 3-4, explicit, Hill: the kernel takes the law-table path)
         L.sw_s = sweep_group(m);
         L.sw_c = 1;
-        for (int c : {4, 3, 2})
-            if (L.sw_s % c == 0) { L.sw_c = c; break; }
+        if (L.sw_s <= 8) L.sw_c = L.sw_s;
+        else
+            for (int c : {5, 4, 3, 2})
+                if (L.sw_s % c == 0) { L.sw_c = c; break; }
         if (const char* e = std::getenv("SMC_SW_C")) {
             const int c = std::atoi(e);
             if (c >= 1 && L.sw_s % c == 0) L.sw_c = c;
@@ -925,6 +938,7 @@ std::string generate_source(const Model& m, const Property& p, int variant, cons
         o << "#define SMC_SWEEP 1\n#define SMC_BLOCK 128\n#define SMC_MINB " << minb << "\n";
         o << "#define SMC_SW_XD " << (tl->sw_xd ? 1 : 0) << "\n#define SMC_OFF_SWLAW " << tl->off_swlaw
           << "\n#define SMC_SW_C " << tl->sw_c << "\n";
+        if (const char* e = std::getenv("SMC_BURST")) o << "#define SMC_BURST " << std::max(1, std::atoi(e)) << "\n";
         o << "#define SMC_SW_ANYGEN " << ((tl->any_hill || tl->any_general || tl->any_explicit) ? 1 : 0) << "\n";
         o << "#define SMC_OFF_X0 " << tl->off_x0 << "\n#define SMC_OFF_LAW " << tl->off_law
           << "\n#define SMC_OFF_HREP " << tl->off_hill_rep << "\n#define SMC_OFF_HK " << tl->off_hill_k
