@@ -271,7 +271,8 @@ extern "C" __global__ void __launch_bounds__(SMC_BLOCK, SMC_MINB) smc_ssa_sweep(
                             smc_xt* xp = xcol + (int)(e >> 4) * SMC_BLOCK;
 #if SMC_SW_XD
                             const double nv = __dadd_rn(*xp, (double)((int)(e & 15u) - 8));   // exact
-                            ovf |= nv > 2147483647.0;
+                            // nv > 2^31 - 1 for an integer nv >= 0 <=> its high word >= that of 2^31
+                            ovf |= __double2hiint(nv) >= 0x41E00000;
 #else
                             const int nv = (int)((unsigned)*xp + (unsigned)((int)(e & 15u) - 8));
                             ovf |= nv < 0;
