@@ -402,9 +402,62 @@ std::string law_expr(const Reaction& r, int k) {
     return "__dmul_rn(smc_rc[" + std::to_string(k) + "], (double)(" + h + "))";   // c_k from the constant bank
 }
 
+void xd_forms(const Model& m, std::vector<int>& form, std::vector<double>& cs);
+std::string xd_law_body(const Model& m, int k, int f, const char* rc, const HillTables* ht);
+
+// Variant 1 with the counts as binary64 registers (exact integers < 2^31): the laws are
+// fp64 products with no int64 -> fp64 conversion on the per-event chain (R20); the
+// count-overflow test of R17 is a high-word compare.
+std::string model_code_thread_xd(const Model& m) {
+    std::ostringstream o;
+    const int N = m.N, M = m.M;
+    std::vector<double> cs;
+    std::vector<int> form;
+    xd_forms(m, form, cs);
+    o << "typedef double smc_x1t;\n";
+    o << "__constant__ double smc_rc[" << M << "] = {";
+    for (int k = 0; k < M; ++k) o << (k ? ", " : "") << dlit(cs[(size_t)k]);
+    o << "};\n";
+    o << "__device__ __forceinline__ void smc_init_x(smc_x1t (&x)[SMC_N]) {\n";
+    for (int s = 0; s < N; ++s) o << "    x[" << s << "] = " << m.x0[(size_t)s] << ".0;\n";
+    o << "}\n";
+    const HillTables ht = pack_hill_tables(m);
+    for (int k = 0; k < M; ++k) {
+        o << "__device__ __forceinline__ double smc_law" << k << "(const smc_x1t (&x)[SMC_N], const double* __restrict__ H) {\n";
+        o << "    (void)H;\n" << xd_law_body(m, k, form[(size_t)k], "smc_rc", &ht) << "}\n";
+    }
+    o << "__device__ __forceinline__ void smc_laws_all(double (&a)[SMC_M], const smc_x1t (&x)[SMC_N], const double* __restrict__ H) {\n";
+    for (int k = 0; k < M; ++k) o << "    a[" << k << "] = smc_law" << k << "(x, H);\n";
+    o << "}\n";
+    o << "__device__ __forceinline__ bool smc_apply(int j, smc_x1t (&x)[SMC_N]) {\n    bool ovf = false;\n";
+    for (int s = 0; s < N; ++s) {
+        std::vector<std::pair<int, int>> ds;
+        bool pos = false;
+        for (int j = 0; j < M; ++j)
+            for (auto& ch : m.R[(size_t)j].change)
+                if (ch.first == s) { ds.push_back({j, ch.second}); pos |= ch.second > 0; }
+        if (ds.empty()) continue;
+        std::string sel = "0";
+        for (auto it = ds.rbegin(); it != ds.rend(); ++it)
+            sel = "(j == " + std::to_string(it->first) + " ? " + std::to_string(it->second) + " : " + sel + ")";
+        o << "    x[" << s << "] = __dadd_rn(x[" << s << "], (double)" << sel << ");\n";
+        if (pos) o << "    ovf |= __double2hiint(x[" << s << "]) >= 0x41E00000;\n";   // x >= 2^31
+    }
+    o << "    return !ovf;\n}\n";
+    o << "__device__ __forceinline__ void smc_update(int j, double (&a)[SMC_M], const smc_x1t (&x)[SMC_N], const double* __restrict__ H) {\n";
+    o << "    (void)j;\n";
+    for (int k = 0; k < M; ++k) o << "    a[" << k << "] = smc_law" << k << "(x, H);\n";
+    o << "}\n";
+    o << "__device__ __forceinline__ int smc_last_positive(const double (&a)[SMC_M]) {\n    return ";
+    for (int k = M - 1; k >= 1; --k) o << "a[" << k << "] > 0.0 ? " << k << " : ";
+    o << "0;\n}\n";
+    return o.str();
+}
+
 std::string model_code_thread(const Model& m) {
     std::ostringstream o;
     const int N = m.N, M = m.M;
+    o << "typedef int smc_x1t;\n";
     // rate constants in the constant bank (DMUL reads c[][] operands; no per-event
     // materialisation of 64-bit immediates)
     o << "__constant__ double smc_rc[" << M << "] = {";
@@ -486,11 +539,13 @@ int sweep_group(const Model& m) {
     return std::min(S, m.M);
 }
 
-std::string sweep_code_xd(const Model& m, int S, int G) {
-    std::ostringstream o;
-    const int N = m.N, M = m.M;
-    std::vector<double> cs((size_t)M);
-    std::vector<int> form((size_t)M);     // 0 c, 1 c x, 2 (c/2) x (x-1), 3 c x y, 4 general
+// Laws over binary64 counts (sweep SMC_SW_XD, variant 1 with binary64 registers): plain
+// fp64 products of the counts, identical to the int64 forms (R20).  form: 0 c, 1 c x,
+// 2 (c/2) x (x-1) (exact fold), 3 c x y, 4 general (explicit, order 3-4, unfoldable).
+void xd_forms(const Model& m, std::vector<int>& form, std::vector<double>& cs) {
+    const int M = m.M;
+    form.assign((size_t)M, 4);
+    cs.assign((size_t)M, 0.0);
     for (int k = 0; k < M; ++k) {
         const Reaction& r = m.R[(size_t)k];
         double c = r.c;
@@ -506,42 +561,57 @@ std::string sweep_code_xd(const Model& m, int S, int G) {
         form[(size_t)k] = f;
         cs[(size_t)k] = c;
     }
+}
+
+// statements of law k over double x[] with rates in constant array `rc`; zero-order Hill
+// laws read the host table H (variant 1) when ht is given
+std::string xd_law_body(const Model& m, int k, int f, const char* rc, const HillTables* ht) {
+    std::ostringstream o;
+    const Reaction& r = m.R[(size_t)k];
+    const std::string K = std::to_string(k);
+    if (!r.rate.empty()) return explicit_body(r, "x", "    ");
+    if (ht && ht->offset[(size_t)k] >= 0)
+        o << "    if (x[" << r.rep << "] < " << ht->size << ".0) return __ldg(H + " << ht->offset[(size_t)k]
+          << " + (int)x[" << r.rep << "]);\n";
+    const std::string a = std::to_string(r.s[0]), b = std::to_string(r.s[1]), C = std::string(rc) + "[" + K + "]";
+    switch (f) {
+        case 0: o << "    double v = " << C << ";\n"; break;
+        case 1: o << "    double v = __dmul_rn(" << C << ", x[" << a << "]);\n"; break;
+        case 2: o << "    double v = __dmul_rn(" << C << ", __dmul_rn(x[" << a << "], __dadd_rn(x[" << a << "], -1.0)));\n"; break;
+        case 3: o << "    double v = __dmul_rn(" << C << ", __dmul_rn(x[" << a << "], x[" << b << "]));\n"; break;
+        default: {                                   // order 3-4 / unfoldable homodimer: exact int64 h
+            std::vector<std::string> terms;
+            for (int q = 0; q < 2; ++q) {
+                if (r.s[q] < 0) continue;
+                std::string xs = "(smc_i64)x[" + std::to_string(r.s[q]) + "]";
+                terms.push_back(r.st[q] == 1 ? xs : "((" + xs + " * (" + xs + " - 1LL)) / 2LL)");
+            }
+            std::string h = terms.empty() ? "1LL" : (terms.size() == 1 ? terms[0] : "(" + terms[0] + " * " + terms[1] + ")");
+            o << "    double v = __dmul_rn(" << C << ", (double)(" << h << "));\n";
+        }
+    }
+    if (r.hill) {
+        o << "    const double q = __ddiv_rn(x[" << r.rep << "], " << dlit(r.K) << ");\n";
+        o << "    double qn = q;\n";
+        for (int i = 1; i < r.n; ++i) o << "    qn = __dmul_rn(qn, q);\n";
+        o << "    v = __ddiv_rn(v, __dadd_rn(1.0, qn));\n";
+    }
+    o << "    return v;\n";
+    return o.str();
+}
+
+std::string sweep_code_xd(const Model& m, int S, int G) {
+    std::ostringstream o;
+    const int N = m.N, M = m.M;
+    std::vector<double> cs;
+    std::vector<int> form;
+    xd_forms(m, form, cs);
     o << "__constant__ double smc_rc[" << M << "] = {";
     for (int k = 0; k < M; ++k) o << (k ? ", " : "") << dlit(cs[(size_t)k]);
     o << "};\n";
     for (int k = 0; k < M; ++k) {
-        const Reaction& r = m.R[(size_t)k];
-        const std::string K = std::to_string(k);
         o << "__device__ __forceinline__ double smc_law" << k << "(const double (&x)[SMC_N]) {\n";
-        if (!r.rate.empty()) {
-            o << explicit_body(r, "x", "    ") << "}\n";
-            continue;
-        }
-        const std::string a = std::to_string(r.s[0]), b = std::to_string(r.s[1]);
-        switch (form[(size_t)k]) {
-            case 0: o << "    double v = smc_rc[" << K << "];\n"; break;
-            case 1: o << "    double v = __dmul_rn(smc_rc[" << K << "], x[" << a << "]);\n"; break;
-            case 2: o << "    double v = __dmul_rn(smc_rc[" << K << "], __dmul_rn(x[" << a << "], __dadd_rn(x[" << a
-                      << "], -1.0)));\n"; break;
-            case 3: o << "    double v = __dmul_rn(smc_rc[" << K << "], __dmul_rn(x[" << a << "], x[" << b << "]));\n"; break;
-            default: {                                   // order 3-4 / unfoldable homodimer: exact int64 h
-                std::vector<std::string> terms;
-                for (int q = 0; q < 2; ++q) {
-                    if (r.s[q] < 0) continue;
-                    std::string xs = "(smc_i64)x[" + std::to_string(r.s[q]) + "]";
-                    terms.push_back(r.st[q] == 1 ? xs : "((" + xs + " * (" + xs + " - 1LL)) / 2LL)");
-                }
-                std::string h = terms.size() == 1 ? terms[0] : "(" + terms[0] + " * " + terms[1] + ")";
-                o << "    double v = __dmul_rn(smc_rc[" << K << "], (double)(" << h << "));\n";
-            }
-        }
-        if (r.hill) {
-            o << "    const double q = __ddiv_rn(x[" << r.rep << "], " << dlit(r.K) << ");\n";
-            o << "    double qn = q;\n";
-            for (int i = 1; i < r.n; ++i) o << "    qn = __dmul_rn(qn, q);\n";
-            o << "    v = __ddiv_rn(v, __dadd_rn(1.0, qn));\n";
-        }
-        o << "    return v;\n}\n";
+        o << xd_law_body(m, k, form[(size_t)k], "smc_rc", nullptr) << "}\n";
     }
     bool any_explicit = false;
     for (auto& r : m.R) any_explicit |= !r.rate.empty();
@@ -970,7 +1040,14 @@ std::string generate_source(const Model& m, const Property& p, int variant, cons
         if (const char* e = std::getenv("SMC_FLAT")) o << "#define SMC_FLAT " << std::atoi(e) << "\n";
     }
     o << embedded_source("ssa_common.cuh") << "\n";
-    if (variant == 1 || variant == 3) o << model_code_thread(m) << "\n";
+    if (variant == 1) {
+        // binary64 count registers for the latency-bound small models (C2: 0.389 -> 0.381
+        // us per event on the chain); larger ones keep int32 (C3: more spills, -6 %)
+        bool xd = m.M <= 8 && m.N <= 8;
+        if (const char* e = std::getenv("SMC_V1_XD")) xd = std::atoi(e) != 0;
+        o << (xd ? model_code_thread_xd(m) : model_code_thread(m)) << "\n";
+    }
+    if (variant == 3) o << model_code_thread(m) << "\n";
     if (variant == 4) o << model_code_sweep(m, tl->sw_xd) << "\n";
     if (variant == 2 && tl->any_explicit) {          // explicit laws of the tile variant
         o << "__device__ __noinline__ double smc_explicit(int k, const int* xs) {\n    switch (k) {\n";

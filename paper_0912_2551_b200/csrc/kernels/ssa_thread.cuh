@@ -46,7 +46,7 @@ extern "C" __global__ void __launch_bounds__(SMC_BLOCK, SMC_MINB) smc_ssa_thread
     const smc_u32 lane = threadIdx.x & 31u;
     const double* __restrict__ H = (const double*)P.tables;
     const smc_u32 cap = (smc_u32)(P.event_cap < 0xFFFFFFFFull ? P.event_cap : 0xFFFFFFFFull);
-    int x[SMC_N];
+    smc_x1t x[SMC_N];                     // int32, or binary64 (codegen SMC_V1_XD)
     double a[SMC_M];
     double t = 0.0, tp = 0.0;
     double e_cur = 0.0, u_cur = 0.0;      // draw of the current step k
