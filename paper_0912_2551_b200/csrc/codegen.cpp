@@ -437,10 +437,10 @@ std::string model_code_thread_xd(const Model& m) {
             for (auto& ch : m.R[(size_t)j].change)
                 if (ch.first == s) { ds.push_back({j, ch.second}); pos |= ch.second > 0; }
         if (ds.empty()) continue;
-        std::string sel = "0";
+        std::string sel = "0.0";           // binary64 deltas: no int -> fp64 conversion on the chain
         for (auto it = ds.rbegin(); it != ds.rend(); ++it)
-            sel = "(j == " + std::to_string(it->first) + " ? " + std::to_string(it->second) + " : " + sel + ")";
-        o << "    x[" << s << "] = __dadd_rn(x[" << s << "], (double)" << sel << ");\n";
+            sel = "(j == " + std::to_string(it->first) + " ? " + std::to_string(it->second) + ".0 : " + sel + ")";
+        o << "    x[" << s << "] = __dadd_rn(x[" << s << "], " << sel << ");\n";
         if (pos) o << "    ovf |= __double2hiint(x[" << s << "]) >= 0x41E00000;\n";   // x >= 2^31
     }
     o << "    return !ovf;\n}\n";
