@@ -755,6 +755,15 @@ size_t align16(size_t v) { return (v + 15) & ~(size_t)15; }
 }  // namespace
 
 
+// CTA size of variant 1: a Fig. 2 batch smaller than the resident capacity is spread over
+// the SMs in whole CTAs, so smaller CTAs even out the per-SM load (the most loaded SM sets
+// the latency-bound round time)
+int thread_block() {
+    int b = 128;
+    if (const char* e = std::getenv("SMC_V1_BLOCK")) b = std::atoi(e);
+    return (b == 32 || b == 64 || b == 128 || b == 256) ? b : 128;
+}
+
 // --------------------------------------------------- variant 1 tables ---
 HillTables pack_hill_tables(const Model& m) {
     HillTables h;
@@ -990,7 +999,8 @@ std::string generate_source(const Model& m, const Property& p, int variant, cons
         // registers for ILP (minb 4); larger ones are throughput-bound (minb 6: C3 +4 %)
         int minb = m.M <= 8 ? 4 : 6;
         if (const char* e = std::getenv("SMC_MINB")) minb = std::atoi(e);
-        o << "#define SMC_BLOCK 128\n#define SMC_MINB " << minb << "\n";
+        const int blk = thread_block();     // the same resident threads with smaller CTAs
+        o << "#define SMC_BLOCK " << blk << "\n#define SMC_MINB " << std::max(1, minb * 128 / blk) << "\n";
         // two-stage draw pipeline: shorter per-event chain (-12 % at low occupancy, C2) for
         // register-light models; heavier models are throughput-bound and keep one stage
         int pipe2 = (m.M <= 8 && m.N <= 8) ? 1 : 0;
