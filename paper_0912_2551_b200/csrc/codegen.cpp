@@ -688,9 +688,16 @@ std::string model_code_sweep(const Model& m, bool xd) {
         o << "    }\n    return 0.0;\n}\n";
     }
     // fast laws, valid while every count is < 2^26: each mass-action count product h is
-    // < 2^52, so (double)h is formed exactly on the FP64 pipe as (2^52 + h) - 2^52 from
-    // the bit pattern 0x43300000:h (no int64 -> fp64 conversion on the XU pipe); the
-    // values are identical to the general laws'
+    // < 2^52, so the bit pattern 0x43300000:h is the double 2^52 + h exactly, and
+    //   a = fma(c, 2^52 + h, -c 2^52) = round(c (2^52 + h) - c 2^52) = round(c h)
+    // (one rounding of the exact value, -c 2^52 is an exact constant): the same double as
+    // c * (double)h with one FP64 instruction and no int64 -> fp64 conversion (SMC_SW_FMA;
+    // 0: (2^52 + h) - 2^52 then the product, two FP64 instructions)
+    bool fma = true;
+    if (const char* e = std::getenv("SMC_SW_FMA")) fma = std::atoi(e) != 0;
+    o << "__constant__ double smc_rcn[" << M << "] = {";
+    for (int k = 0; k < M; ++k) o << (k ? ", " : "") << dlit(-std::ldexp(m.R[(size_t)k].c, 52));
+    o << "};\n";
     std::vector<bool> used((size_t)N, false);
     for (int k = 0; k < M; ++k) {
         const Reaction& r = m.R[(size_t)k];
@@ -713,8 +720,14 @@ std::string model_code_sweep(const Model& m, bool xd) {
                 std::to_string(r.s[1]) + "])";
         }
         o << "    (void)x;\n";
-        o << "    double a = " << (h.empty() ? "__dmul_rn(smc_rc[" + std::to_string(k) + "], 1.0)"
-                                        : "__dmul_rn(smc_rc[" + std::to_string(k) + "], " + h + ")") << ";\n";
+        const std::string K = std::to_string(k);
+        if (fma && !h.empty()) {                       // smc_u2d(v) -> the biased pattern of v
+            const std::string hb = "__longlong_as_double((long long)(" + h.substr(8, h.size() - 9) + " | 0x4330000000000000ull))";
+            o << "    double a = __fma_rn(smc_rc[" << K << "], " << hb << ", smc_rcn[" << K << "]);\n";
+        } else {
+            o << "    double a = " << (h.empty() ? "__dmul_rn(smc_rc[" + K + "], 1.0)" : "__dmul_rn(smc_rc[" + K + "], " + h + ")")
+              << ";\n";
+        }
         if (r.hill) {
             o << "    const double q = __ddiv_rn(smc_u2d((smc_u64)(unsigned)x[" << r.rep << "]), " << dlit(r.K) << ");\n";
             o << "    double qn = q;\n";
