@@ -649,7 +649,7 @@ std::string sweep_code_xd(const Model& m, int S, int G) {
 // rounding of the exact product either way, and x (x - 1) with the 1/2 folded into
 // c (reading R20); no conversion per law.
 bool sweep_xd_impl(const Model& m, size_t table_bytes) {
-    bool xd = table_bytes + 128 * 8 * (size_t)(m.N + 1) <= 72 * 1024;     // 3 CTAs per SM
+    bool xd = table_bytes + (size_t)sweep_block() * 8 * (size_t)(m.N + 1) <= (size_t)sweep_block() * 576;   // 3 CTAs of 128 per SM
     if (const char* e = std::getenv("SMC_SW_XD")) xd = std::atoi(e) != 0;
     return xd;
 }
@@ -771,6 +771,13 @@ size_t align16(size_t v) { return (v + 15) & ~(size_t)15; }
 // CTA size of variant 1: a Fig. 2 batch smaller than the resident capacity is spread over
 // the SMs in whole CTAs, so smaller CTAs even out the per-SM load (the most loaded SM sets
 // the latency-bound round time)
+// CTA size of the sweep variant (the stride of the count columns)
+int sweep_block() {
+    int b = 128;
+    if (const char* e = std::getenv("SMC_SW_BLOCK")) b = std::atoi(e);
+    return (b >= 32 && b <= 256 && b % 32 == 0) ? b : 128;
+}
+
 int thread_block() {
     int b = 128;
     if (const char* e = std::getenv("SMC_V1_BLOCK")) b = std::atoi(e);
@@ -937,7 +944,7 @@ TileLayout pack_tables(const Model& m, bool sweep) {
         L.off_swlaw = align16(L.bytes);
         const size_t nb = L.off_swlaw + 16 * (size_t)G * L.sw_s;
         L.sw_xd = sweep_xd_impl(m, nb);
-        const uint32_t col = 128u * (L.sw_xd ? 8u : 4u);
+        const uint32_t col = (uint32_t)sweep_block() * (L.sw_xd ? 8u : 4u);
         L.blob.resize(nb, 0);
         L.bytes = nb;
         for (int j = 0; j < G * L.sw_s; ++j) {
@@ -1025,10 +1032,11 @@ std::string generate_source(const Model& m, const Property& p, int variant, cons
         // (tables + 128 columns of N+1 ints) and by registers (pass 1 keeps the counts and
         // the group prefixes in registers): 3 by default (<= 168 registers; C4: 3 -> 1.19e10,
         // 4 -> 1.14e10, 5 -> 8.8e9 events/s: the sweep's ILP needs the registers)
-        const size_t per_cta = tl->bytes + 128 * (tl->sw_xd ? 8 : 4) * (size_t)(m.N + 1) + 64;
-        int minb = (int)std::max<size_t>(1, std::min<size_t>(3, 227 * 1024 / per_cta));
+        const int blk = sweep_block();
+        const size_t per_cta = tl->bytes + (size_t)blk * (tl->sw_xd ? 8 : 4) * (size_t)(m.N + 1) + 1024 + 64;
+        int minb = (int)std::max<size_t>(1, std::min<size_t>(8, 233472 / per_cta));   // smem-bound CTAs per SM
         if (const char* e = std::getenv("SMC_MINB")) minb = std::atoi(e);
-        o << "#define SMC_SWEEP 1\n#define SMC_BLOCK 128\n#define SMC_MINB " << minb << "\n";
+        o << "#define SMC_SWEEP 1\n#define SMC_BLOCK " << blk << "\n#define SMC_MINB " << std::max(1, minb) << "\n";
         o << "#define SMC_SW_XD " << (tl->sw_xd ? 1 : 0) << "\n#define SMC_OFF_SWLAW " << tl->off_swlaw
           << "\n#define SMC_SW_C " << tl->sw_c << "\n";
         if (const char* e = std::getenv("SMC_BURST")) o << "#define SMC_BURST " << std::max(1, std::atoi(e)) << "\n";

@@ -90,7 +90,7 @@ __device__ __noinline__ double smc_law_gen(int k, const SmcXCol& X, const SmcSwT
     return a;
 }
 
-// Sweep-format entry: u0 = byte offset of the column of s0 | flags (bit 0 homodimer,
+// Sweep-format entry: u0 = byte offset of the column of s0 (a multiple of 4) | flags (bit 0 homodimer,
 // bit 1 general law), u1 = byte offset of the column of s1, c = rate (halved for a
 // homodimer); entries past M are zero-rate padding (a = 0).
 __device__ __forceinline__ double smc_law_sw(int k, const SmcXCol& X, const SmcSwTabs& T) {
@@ -99,7 +99,7 @@ __device__ __forceinline__ double smc_law_sw(int k, const SmcXCol& X, const SmcS
     if (L.u0 & 2u) return smc_law_gen(k, X, T);
 #endif
     const char* xb = (const char*)X.p;
-    const smc_xt v0 = *(const smc_xt*)(xb + (L.u0 & ~511u));
+    const smc_xt v0 = *(const smc_xt*)(xb + (L.u0 & ~3u));
     const smc_xt v1 = *(const smc_xt*)(xb + L.u1);
 #if SMC_SW_XD
     const double h = __dmul_rn(v0, __dadd_rn(v1, (L.u0 & 1u) ? -1.0 : 0.0));   // exact shift by 0 / -1
