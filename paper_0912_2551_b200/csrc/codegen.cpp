@@ -648,10 +648,20 @@ std::string sweep_code_xd(const Model& m, int S, int G) {
 // counts (exact integers, < 2^31), identical to the int64 forms: fl(x0 x1) is the
 // rounding of the exact product either way, and x (x - 1) with the 1/2 folded into
 // c (reading R20); no conversion per law.
-bool sweep_xd_impl(const Model& m, size_t table_bytes) {
-    bool xd = table_bytes + (size_t)sweep_block() * 8 * (size_t)(m.N + 1) <= (size_t)sweep_block() * 576;   // 3 CTAs of 128 per SM
+// Count columns and CTA size of the sweep variant, from the packed table size: one CTA of
+// up to 384 threads per SM (12 warps at 168 registers fill the register file; one CTA
+// per SM measured +10 % over three CTAs of 128 on C4), binary64 columns when they fit,
+// else int32 columns; SMC_SW_XD / SMC_SW_BLOCK override.
+void sweep_shape(const Model& m, size_t table_bytes, bool& xd, int& blk) {
+    const size_t avail = 233472 - 2048 - std::min<size_t>(table_bytes, 200000);
+    auto fit = [&](size_t esz) { return (int)std::min<size_t>(384, avail / (esz * (size_t)(m.N + 1)) / 32 * 32); };
+    xd = fit(8) >= 128;
     if (const char* e = std::getenv("SMC_SW_XD")) xd = std::atoi(e) != 0;
-    return xd;
+    blk = std::max(32, fit(xd ? 8 : 4));
+    if (const char* e = std::getenv("SMC_SW_BLOCK")) {
+        const int b = std::atoi(e);
+        if (b >= 32 && b <= 512 && b % 32 == 0) blk = b;
+    }
 }
 
 std::string model_code_sweep(const Model& m, bool xd) {
@@ -771,13 +781,6 @@ size_t align16(size_t v) { return (v + 15) & ~(size_t)15; }
 // CTA size of variant 1: a Fig. 2 batch smaller than the resident capacity is spread over
 // the SMs in whole CTAs, so smaller CTAs even out the per-SM load (the most loaded SM sets
 // the latency-bound round time)
-// CTA size of the sweep variant (the stride of the count columns)
-int sweep_block() {
-    int b = 128;
-    if (const char* e = std::getenv("SMC_SW_BLOCK")) b = std::atoi(e);
-    return (b >= 32 && b <= 256 && b % 32 == 0) ? b : 128;
-}
-
 int thread_block() {
     int b = 128;
     if (const char* e = std::getenv("SMC_V1_BLOCK")) b = std::atoi(e);
@@ -943,8 +946,8 @@ TileLayout pack_tables(const Model& m, bool sweep) {
         const int G = (M + L.sw_s - 1) / L.sw_s;
         L.off_swlaw = align16(L.bytes);
         const size_t nb = L.off_swlaw + 16 * (size_t)G * L.sw_s;
-        L.sw_xd = sweep_xd_impl(m, nb);
-        const uint32_t col = (uint32_t)sweep_block() * (L.sw_xd ? 8u : 4u);
+        sweep_shape(m, nb, L.sw_xd, L.sw_blk);
+        const uint32_t col = (uint32_t)L.sw_blk * (L.sw_xd ? 8u : 4u);
         L.blob.resize(nb, 0);
         L.bytes = nb;
         for (int j = 0; j < G * L.sw_s; ++j) {
@@ -1032,7 +1035,7 @@ std::string generate_source(const Model& m, const Property& p, int variant, cons
         // (tables + 128 columns of N+1 ints) and by registers (pass 1 keeps the counts and
         // the group prefixes in registers): 3 by default (<= 168 registers; C4: 3 -> 1.19e10,
         // 4 -> 1.14e10, 5 -> 8.8e9 events/s: the sweep's ILP needs the registers)
-        const int blk = sweep_block();
+        const int blk = tl->sw_blk;
         const size_t per_cta = tl->bytes + (size_t)blk * (tl->sw_xd ? 8 : 4) * (size_t)(m.N + 1) + 1024 + 64;
         int minb = (int)std::max<size_t>(1, std::min<size_t>(8, 233472 / per_cta));   // smem-bound CTAs per SM
         if (const char* e = std::getenv("SMC_MINB")) minb = std::atoi(e);

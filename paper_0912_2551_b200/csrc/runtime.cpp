@@ -226,7 +226,7 @@ PropKernel& prepare(Model& m, const Property& p) {
         pk.smem = 0;
         alloc_traces(m, p, pk, pk.block);
     } else if (pk.variant == 4) {
-        pk.block = sweep_block();
+        pk.block = tl->sw_blk;
         pk.smem = (int)(tl->bytes + (size_t)pk.block * (tl->sw_xd ? 8 : 4) * (size_t)(m.N + 1));
         cudaFuncAttributes fa;
         ck(cudaFuncGetAttributes(&fa, fn), "cudaFuncGetAttributes");

@@ -162,12 +162,12 @@ struct TileLayout {               // packed model tables (variant 2), byte offse
     size_t off_swlaw = 0;
     int sw_s = 0, sw_c = 0;       // laws per group, independent law reads per chunk
     bool sw_xd = false;           // counts as binary64 columns
+    int sw_blk = 128;             // CTA size = stride of the count columns
     int max_dep = 0;
     std::vector<uint8_t> blob;    // host copy
 };
-TileLayout pack_tables(const Model& m, bool sweep = false);
+TileLayout pack_tables(const Model& m, bool sweep = false);   // sweep: law/change tables only (variant 4)
 int thread_block();                 // CTA size of variant 1 (codegen.cpp)
-int sweep_block();                  // CTA size of variant 4 (stride of the count columns)   // sweep: law/change tables only (variant 4)
 // variant 1: zero-order Hill propensities a_k(x_r), x_r < size, tabulated on the host with
 // the same IEEE operations as the law (one __ldg instead of two divisions per update)
 struct HillTables {
