@@ -778,13 +778,23 @@ size_t align16(size_t v) { return (v + 15) & ~(size_t)15; }
 }  // namespace
 
 
-// CTA size of variant 1: a Fig. 2 batch smaller than the resident capacity is spread over
-// the SMs in whole CTAs, so smaller CTAs even out the per-SM load (the most loaded SM sets
-// the latency-bound round time)
-int thread_block() {
-    int b = 128;
+// resident 128-thread units per SM of variant 1 (register cap 65536 / (128 minb)): the small
+// models (M <= 8: C1, C2) run latency-bound Wilson rounds below full occupancy and keep
+// registers for ILP (4); larger ones are throughput-bound (6: C3 +4 %)
+int thread_minb(const Model& m) {
+    int minb = m.M <= 8 ? 4 : 6;
+    if (const char* e = std::getenv("SMC_MINB")) minb = std::atoi(e);
+    return std::max(1, minb);
+}
+
+// CTA size of variant 1 (SMC_V1_BLOCK overrides)
+int thread_block(const Model& m) {
+    // one CTA per SM holding all the resident threads of the register budget (minb x 128):
+    // measured C2 0.688 -> 0.645 us per event on a 66 k batch (6.04e10 -> 6.35e10 events/s),
+    // C3 7.69e10 -> 7.86e10, against 128-thread CTAs
+    int b = thread_minb(m) * 128;
     if (const char* e = std::getenv("SMC_V1_BLOCK")) b = std::atoi(e);
-    return (b == 32 || b == 64 || b == 128 || b == 256) ? b : 128;
+    return (b >= 32 && b <= 1024 && b % 32 == 0) ? b : 128;
 }
 
 // --------------------------------------------------- variant 1 tables ---
@@ -1020,9 +1030,8 @@ std::string generate_source(const Model& m, const Property& p, int variant, cons
         // resident 128-thread CTAs per SM (register cap 65536 / (128 minb)): the small models
         // (M <= 8: C1, C2) run latency-bound Wilson rounds below full occupancy and keep
         // registers for ILP (minb 4); larger ones are throughput-bound (minb 6: C3 +4 %)
-        int minb = m.M <= 8 ? 4 : 6;
-        if (const char* e = std::getenv("SMC_MINB")) minb = std::atoi(e);
-        const int blk = thread_block();     // the same resident threads with smaller CTAs
+        const int minb = thread_minb(m);
+        const int blk = thread_block(m);    // the same resident threads in fewer, larger CTAs
         o << "#define SMC_BLOCK " << blk << "\n#define SMC_MINB " << std::max(1, minb * 128 / blk) << "\n";
         // two-stage draw pipeline: shorter per-event chain (-12 % at low occupancy, C2) for
         // register-light models; heavier models are throughput-bound and keep one stage

@@ -238,7 +238,7 @@ PropKernel& prepare(Model& m, const Property& p) {
         if (nb < 1) fail(SMC_E_CUDA, "sweep kernel: no resident CTA");
         pk.grid_max = nb * d.sm_count;
     } else if (pk.variant == 1) {
-        pk.block = thread_block();
+        pk.block = thread_block(m);
         int nb = 0;
         ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, pk.block, 0), "occupancy");
         pk.grid_max = std::max(1, nb) * d.sm_count;

@@ -167,7 +167,8 @@ struct TileLayout {               // packed model tables (variant 2), byte offse
     std::vector<uint8_t> blob;    // host copy
 };
 TileLayout pack_tables(const Model& m, bool sweep = false);   // sweep: law/change tables only (variant 4)
-int thread_block();                 // CTA size of variant 1 (codegen.cpp)
+int thread_minb(const Model& m);    // resident 128-thread units per SM of variant 1 (codegen.cpp)
+int thread_block(const Model& m);   // CTA size of variant 1
 // variant 1: zero-order Hill propensities a_k(x_r), x_r < size, tabulated on the host with
 // the same IEEE operations as the law (one __ldg instead of two divisions per update)
 struct HillTables {
