@@ -247,6 +247,28 @@ def test_large_networks_vs_oracle_fixture(smc, name, variant):
     assert m.last_launch(p)["variant"] == variant
 
 
+@pytest.mark.parametrize("xd,block", [("0", None), ("1", "96"), ("0", "224")])
+def test_sweep_shapes_vs_fixture(smc, xd, block, monkeypatch):
+    """The sweep variant with int32 count columns (exact fma laws, I2F in the selection) and
+    other CTA sizes (the column stride and the pre-scaled law offsets follow it) gives the
+    oracle's C4 replicas."""
+    import json
+    import os
+    monkeypatch.setenv("SMC_SW_XD", xd)
+    if block:
+        monkeypatch.setenv("SMC_SW_BLOCK", block)
+    fx = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "c4_oracle.json")))
+    cfg = workloads.c4()
+    m, p = _pair(smc, cfg, variant=4)
+    n = 600
+    v, e = m.run_verdicts(p, 0, n, fx["seed"])
+    v, e = v.cpu().numpy(), e.cpu().numpy()
+    mism = int(((v != np.array(fx["verdicts"][:n])) | (e != np.array(fx["events"][:n]))).sum())
+    assert mism <= 1, (xd, block, mism)
+    info = m.last_launch(p)
+    assert info["variant"] == 4 and info["block_threads"] == int(block or info["block_threads"])
+
+
 @pytest.mark.parametrize("width", ["4", "8", "16", "32"])
 def test_tile_widths_vs_fixture(smc, width, monkeypatch):
     """Every tile width of variant 2 (4/8/16/32 lanes per trajectory) gives the oracle's replicas."""
