@@ -238,7 +238,8 @@ def main():
     ap.add_argument("--impl", default="smc", choices=["smc", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--n", type=int, default=0, help="override fixed-N replica count (diagnostics)")
+    ap.add_argument("--replicas", "--n", dest="n", type=int, default=0,
+                    help="override fixed-N replica count (diagnostics; --replicas under torchrun)")
     ap.add_argument("--variant", type=int, default=0)
     args = ap.parse_args()
     cfg = workloads.get(args.workload)
