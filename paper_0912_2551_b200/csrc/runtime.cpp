@@ -301,16 +301,25 @@ void launch_slice(Model& m, PropKernel& pk, uint64_t seed, uint64_t lo, uint64_t
     } P{seed, lo, count, spec ? d.spec_cursor() : (unsigned long long*)d.ctl,
         (long long*)(spec ? d.spec_scratch() : d.counters()), dev_verdict, dev_events, m.event_cap, pk.tables,
         pk.lit_t, pk.lit_tau, pk.lit_mask, pk.lit_val, pk.lit_cap};
-    const uint64_t per_block = pk.variant != 2 ? (uint64_t)pk.block : (uint64_t)(pk.block / 32 * pk.per_warp);
+    // thread variant, slice smaller than the resident capacity: one CTA per SM with just
+    // enough warps for the slice (the compiled CTA size is an upper bound), so a small
+    // batch spreads over every SM instead of filling a few
+    int block = pk.block;
+    if (pk.variant == 1 && count < pk.capacity()) {
+        const uint64_t per_sm = (count + (uint64_t)d.sm_count - 1) / (uint64_t)d.sm_count;
+        block = (int)std::min<uint64_t>((uint64_t)pk.block, std::max<uint64_t>(32, (per_sm + 31) / 32 * 32));
+    }
+    const uint64_t per_block = pk.variant != 2 ? (uint64_t)block : (uint64_t)(pk.block / 32 * pk.per_warp);
     const uint64_t need = (count + per_block - 1) / per_block;
     const int grid = (int)std::min<uint64_t>((uint64_t)pk.grid_max, need);
     void* args[] = {&P};
     ck(cudaEventRecord(d.e0, stream()), "event");
-    ck(cudaLaunchKernel((const void*)pk.k->kernel, dim3((unsigned)grid), dim3((unsigned)pk.block), args,
+    ck(cudaLaunchKernel((const void*)pk.k->kernel, dim3((unsigned)grid), dim3((unsigned)block), args,
                         (size_t)pk.smem, stream()),
        "cudaLaunchKernel");
     ck(cudaEventRecord(d.e1, stream()), "event");
     pk.info.grid_blocks = grid;
+    pk.info.block_threads = block;
     pk.info.launches += 1;
     pk.timing_pending = true;
 }
