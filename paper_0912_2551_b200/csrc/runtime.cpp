@@ -301,11 +301,11 @@ void launch_slice(Model& m, PropKernel& pk, uint64_t seed, uint64_t lo, uint64_t
     } P{seed, lo, count, spec ? d.spec_cursor() : (unsigned long long*)d.ctl,
         (long long*)(spec ? d.spec_scratch() : d.counters()), dev_verdict, dev_events, m.event_cap, pk.tables,
         pk.lit_t, pk.lit_tau, pk.lit_mask, pk.lit_val, pk.lit_cap};
-    // thread variant, slice smaller than the resident capacity: one CTA per SM with just
+    // thread and sweep variants, slice smaller than the resident capacity: one CTA per SM with just
     // enough warps for the slice (the compiled CTA size is an upper bound), so a small
     // batch spreads over every SM instead of filling a few
     int block = pk.block;
-    if (pk.variant == 1 && count < pk.capacity()) {
+    if ((pk.variant == 1 || pk.variant == 4) && count < pk.capacity()) {   // (sweep: the column stride stays)
         const uint64_t per_sm = (count + (uint64_t)d.sm_count - 1) / (uint64_t)d.sm_count;
         block = (int)std::min<uint64_t>((uint64_t)pk.block, std::max<uint64_t>(32, (per_sm + 31) / 32 * 32));
     }

@@ -266,7 +266,7 @@ def test_sweep_shapes_vs_fixture(smc, xd, block, monkeypatch):
     mism = int(((v != np.array(fx["verdicts"][:n])) | (e != np.array(fx["events"][:n]))).sum())
     assert mism <= 1, (xd, block, mism)
     info = m.last_launch(p)
-    assert info["variant"] == 4 and info["block_threads"] == int(block or info["block_threads"])
+    assert info["variant"] == 4 and info["block_threads"] <= int(block or 384)   # launched CTA <= the compiled one
 
 
 @pytest.mark.parametrize("width", ["4", "8", "16", "32"])
