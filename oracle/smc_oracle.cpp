@@ -1264,7 +1264,8 @@ int orc_check_streaming(void* fp, int64_t n_entries, const double* t, const doub
 }
 
 // One batch of replicas [first, first+n): mode 0 = streaming (on-the-fly),
-// 1 = literal (simulate to the horizon, evaluate |=).  verdicts/events may be
+// 1 = literal (simulate to the horizon, evaluate |=; halts at the checkpoints of
+// reading R24 once the prefix decides).  verdicts/events may be
 // NULL.  counts[4] = {n_true, n_false, events, errors}.
 int orc_run(void* mp, void* fp, uint64_t seed, uint64_t first, uint64_t n, int32_t mode, int64_t event_cap,
             uint8_t* verdicts, int64_t* events, int64_t* counts) {
@@ -1295,9 +1296,28 @@ int orc_run(void* mp, void* fp, uint64_t seed, uint64_t first, uint64_t n, int32
                 simulate_trace(*M, seed, i, H, event_cap, keep, &tr, &err);
                 if (err) rr = {V_ERROR, tr.n()};
                 else {
-                    LiteralChecker lc(*f, tr);
-                    Tri v = lc.value(f->root, 0);
-                    rr = {v == T_TRUE ? V_TRUE : V_FALSE, tr.n()};
+                    // reading R24: after the sojourn of entry k is drawn, at k = 64, 128, 256, ...
+                    // (before the horizon step), the three-valued |= of the prefix entries 0..k
+                    // is final once definite; the replica then stops with k events.  The prefix
+                    // of the full trace is the prefix the simulation had at step k (the streams
+                    // are keyed by step).
+                    bool halted = false;
+                    for (int64_t k = 64; k < tr.n() && !halted; k *= 2) {
+                        Trace p;
+                        p.N = tr.N;
+                        p.t.assign(tr.t.begin(), tr.t.begin() + k + 1);
+                        p.tau.assign(tr.tau.begin(), tr.tau.begin() + k + 1);
+                        p.x.assign(tr.x.begin(), tr.x.begin() + (k + 1) * tr.N);
+                        p.absorbed = false;
+                        LiteralChecker pc(*f, p);
+                        const Tri pv = pc.value(f->root, 0);
+                        if (pv != T_UNKNOWN) { rr = {pv == T_TRUE ? V_TRUE : V_FALSE, k}; halted = true; }
+                    }
+                    if (!halted) {
+                        LiteralChecker lc(*f, tr);
+                        Tri v = lc.value(f->root, 0);
+                        rr = {v == T_TRUE ? V_TRUE : V_FALSE, tr.n()};
+                    }
                 }
             }
             if (verdicts) verdicts[q] = (uint8_t)rr.verdict;

@@ -335,6 +335,12 @@ std::string recording_monitor(const Property& P) {
          "        if (lead()) r = smc_lit_eval(tb, ub, mb, vb, n, absorbed, cap) == 1 ? 1 : 0;\n"
          "        return __shfl_sync(tmask, r, leader);\n"
          "    }\n"
+         "    __device__ __forceinline__ int eval3(long long n) {   // three-valued |= on the prefix (R24)\n"
+         "        int r = 2;\n"
+         "        __syncwarp(tmask);\n"
+         "        if (lead()) r = smc_lit_eval(tb, ub, mb, vb, n, false, cap);\n"
+         "        return __shfl_sync(tmask, r, leader);\n"
+         "    }\n"
          "    __device__ __forceinline__ void init() { res = -1; last = 0; }\n"
          "    template <class XA> __device__ __forceinline__ void enter(smc_u32 k, double t, double tp, const XA& x) {\n"
          "        (void)tp;\n"
@@ -348,6 +354,10 @@ std::string recording_monitor(const Property& P) {
          "        if (res >= 0) return;\n"
          "        if (lead()) ub[k] = tau;\n"
          "        if (tn > SMC_LIT_H) res = eval((long long)k, false);\n"
+         "        else if (k >= 64u && (k & (k - 1u)) == 0u) {   // checkpoint: halt once decided (R24)\n"
+         "            const int r = eval3((long long)k);\n"
+         "            if (r != 2) res = r;\n"
+         "        }\n"
          "    }\n"
          "    __device__ __forceinline__ void absorb() {\n"
          "        if (res < 0) res = eval(last, true);\n"

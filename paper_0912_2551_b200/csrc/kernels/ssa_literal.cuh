@@ -10,8 +10,11 @@
 // subformula bottom-up over the buffer, in the order and arithmetic of the
 // semantics (elapsed = tau_m + tau_{m+1} + ... left to right), three-valued,
 // and the root at sigma[0] gives the verdict (unknown -> false).
-// There is no on-the-fly halting for these formulas: the replica's events are
-// all events up to the horizon, as in the oracle's literal mode.  A trace
+// On-the-fly halting at checkpoints (reading R24): after the sojourn of entry k
+// is drawn, for k = 64, 128, 256, ..., the three-valued |= of the prefix (entries
+// 0..k, the unobserved future unknown) is evaluated; a definite value is final
+// (the semantics is monotone in the observed prefix) and the replica halts with
+// k events.  Otherwise the replica runs to the horizon as before.  A trace
 // longer than the buffer capacity ends the replica as an error.
 //
 // Generated hooks (codegen.cpp): as variant 1, plus SMC_LIT_H, SMC_LIT_NODES,
@@ -41,6 +44,7 @@ extern "C" __global__ void __launch_bounds__(SMC_BLOCK, 2) smc_ssa_literal(SmcPa
         tb[0] = 0.0;
         mb[0] = smc_lit_mask(x);
         bool absorbed = false, err = false;
+        int decided = -1;
         for (;;) {
             double A = a[0];
 #pragma unroll
@@ -56,6 +60,10 @@ extern "C" __global__ void __launch_bounds__(SMC_BLOCK, 2) smc_ssa_literal(SmcPa
             const double tn = __dadd_rn(t, tau);
             ub[k] = tau;
             if (tn > SMC_LIT_H) break;                    // overshoot: the trace covers the horizon
+            if (k >= 64 && (k & (k - 1)) == 0) {          // checkpoint k = 64 * 2^i: halt once the
+                const int r = smc_lit_eval(tb, ub, mb, vb, (long long)k, false, (long long)cap);
+                if (r != 2) { decided = r; break; }       // prefix decides |= (reading R24)
+            }
             if (k + 1 >= cap || k + 1 >= P.event_cap) { err = true; break; }
             // selection (Eq. 2b): first j with sum_{i<=j} a_i > u2 a0 (left to right)
             const double target = __dmul_rn(u2, A);
@@ -75,7 +83,8 @@ extern "C" __global__ void __launch_bounds__(SMC_BLOCK, 2) smc_ssa_literal(SmcPa
             mb[k] = smc_lit_mask(x);
         }
         int v = 2;
-        if (!err) v = smc_lit_eval(tb, ub, mb, vb, (long long)k, absorbed, (long long)cap) == 1 ? 1 : 0;
+        if (decided >= 0) v = decided;
+        else if (!err) v = smc_lit_eval(tb, ub, mb, vb, (long long)k, absorbed, (long long)cap) == 1 ? 1 : 0;
         if (v == 1) ++c_true;
         else if (v == 0) ++c_false;
         else ++c_err;
