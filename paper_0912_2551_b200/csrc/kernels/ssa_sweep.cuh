@@ -143,6 +143,24 @@ __device__ __forceinline__ int smc_pick(int gi, double base, double target, cons
     return j0;
 }
 
+// P at the last index i in [LO, HI) with le[i] (le is a prefix of trues: the prefixes are
+// non-decreasing), else fb -- a select tree of depth log2(G) instead of a G-long chain
+template <int LO, int HI> struct SmcLastLe {
+    static __device__ __forceinline__ double pick(const double (&P)[SMC_SW_G], const bool (&le)[SMC_SW_G], double fb) {
+        if constexpr (HI <= LO) {
+            return fb;
+        } else if constexpr (HI - LO == 1) {
+            return le[LO] ? P[LO] : fb;
+        } else {
+            // le[MID]: the answer is P[MID] or later; else it lies in [LO, MID) (or is fb)
+            constexpr int MID = (LO + HI) / 2;
+            const double right = SmcLastLe<MID + 1, HI>::pick(P, le, P[MID]);
+            const double left = SmcLastLe<LO, MID>::pick(P, le, fb);
+            return le[MID] ? right : left;
+        }
+    }
+};
+
 // rounding with u2 a0 >= every prefix: the last reaction with a_j > 0 (reading R11)
 __device__ __noinline__ int smc_last_positive_sw(const SmcXCol& X, const SmcSwTabs& T) {
     for (int j = SMC_M - 1; j > 0; --j)
@@ -253,13 +271,13 @@ extern "C" __global__ void __launch_bounds__(SMC_BLOCK, SMC_MINB) smc_ssa_sweep(
                     const double target = __dmul_rn(u_cur, A);
                     const smc_i64 tb = smc_ord(target);
                     int gi = 0;
-                    double base = 0.0;
+                    bool le[SMC_SW_G];
 #pragma unroll
                     for (int i = 0; i < SMC_SW_G; ++i) {
-                        const bool le = smc_ord(Pg[i]) <= tb;
-                        gi += le ? 1 : 0;
-                        base = le ? Pg[i] : base;
+                        le[i] = smc_ord(Pg[i]) <= tb;
+                        gi += le[i] ? 1 : 0;
                     }
+                    const double base = SmcLastLe<0, SMC_SW_G>::pick(Pg, le, 0.0);   // P_{gi-1} (0 if gi = 0)
                     const int j = (gi < SMC_SW_G) ? smc_pick(gi, base, target, X, T) : smc_last_positive_sw(X, T);
                     // ---- x += v_j (wrapping add; a negative result is a count overflow, R17)
                     const uint2 ce = *(const uint2*)(T.chg + 4 * j);
