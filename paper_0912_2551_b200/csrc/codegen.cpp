@@ -29,7 +29,8 @@ std::string ilit(int64_t v) { return "(" + std::to_string(v) + "LL)"; }
 // ---------------------------------------------------------------- monitor ---
 struct MonGen {
     const Property& P;
-    explicit MonGen(const Property& p) : P(p) {}
+    bool xd = false;   // the counts are binary64 (variant 1 / sweep binary64 modes)
+    explicit MonGen(const Property& p, bool xd_ = false) : P(p), xd(xd_) {}
 
     // general val tree: int64 (Int, species, + - *) or binary64 in tree order
     static std::string val(const Atom& at, int i) {
@@ -56,6 +57,19 @@ struct MonGen {
         const Atom& a = P.atoms[(size_t)i];
         static const char* cops[] = {" < ", " <= ", " >= ", " > ", " == ", " != "};
         if (a.general) return "(" + val(a, a.lhs) + cops[(int)a.op] + val(a, a.rhs) + ")";
+        if (xd) {
+            // binary64 counts: sum_s coef_s x_s + cst is formed exactly in binary64 when every
+            // partial sum is an integer below 2^53 (|coef| sum x (2^31 - 1) + |cst| < 2^53), so
+            // the comparison equals the int64 one with no fp64 -> int64 conversion
+            long double bound = std::fabs((long double)a.cst);
+            for (auto& kv : a.coef) bound += std::fabs((long double)kv.second) * 2147483647.0L;
+            if (bound < 9007199254740992.0L) {
+                std::string e = dlit((double)a.cst);
+                for (auto& kv : a.coef) e = "__fma_rn(" + dlit((double)kv.second) + ", x[" + std::to_string(kv.first) + "], " + e + ")";
+                static const char* dops[] = {" < ", " <= ", " >= ", " > ", " == ", " != "};
+                return "(" + e + dops[(int)a.op] + "0.0)";
+            }
+        }
         std::string s = "(";
         for (auto& kv : a.coef) s += "(smc_i64)x[" + std::to_string(kv.first) + "] * " + ilit(kv.second) + " + ";
         s += ilit(a.cst) + ")";
@@ -1114,7 +1128,16 @@ std::string generate_source(const Model& m, const Property& p, int variant, cons
         return o.str();
     }
     if (p.literal) o << literal_code(p) << "\n" << recording_monitor(p) << "\n";   // variant 2 only
-    else o << MonGen(p).emit() << "\n";
+    else {
+        bool xd = false;                // binary64 count arrays: variant 1 small models, sweep
+        if (variant == 4) xd = tl->sw_xd;
+        if (variant == 1) {
+            xd = m.M <= 8 && m.N <= 8;
+            if (const char* e = std::getenv("SMC_V1_XD")) xd = std::atoi(e) != 0;
+        }
+        if (const char* e = std::getenv("SMC_MON_XD")) xd = xd && std::atoi(e) != 0;
+        o << MonGen(p, xd).emit() << "\n";
+    }
     o << embedded_source(variant == 1 ? "ssa_thread.cuh" : (variant == 4 ? "ssa_sweep.cuh" : "ssa_tile.cuh")) << "\n";
     return o.str();
 }
