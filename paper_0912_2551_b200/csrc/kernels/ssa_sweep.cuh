@@ -22,14 +22,19 @@
 //   argument of variant 1), and not storing a[M] frees the 1.6 KB per trajectory
 //   that would cap residency.
 // * Selection (Eq. 2b), pass 2: the group g = #{P_i <= u2 a0} by integer compares
-//   of the non-negative doubles' bit patterns, then the member inside g by a
-//   running sum from P_{g-1} over the group's laws read from the smem law table
-//   (per-lane group, in chunks of independent law reads; one dependent add chain).
+//   of the non-negative doubles' bit patterns (P_{g-1} by a select tree), then the
+//   member inside g by a running sum from P_{g-1} over the group's laws re-evaluated
+//   from the sweep-format law table (pre-scaled column offsets; all reads of a chunk
+//   of SMC_SW_C laws independent; one dependent add chain).
 // * x += v_j from the change table; the monitor reads its atoms from the column.
+// * One CTA of up to 384 threads per SM (12 warps at ~168 registers fill the
+//   register file); a slice smaller than the resident capacity launches smaller CTAs
+//   (the column stride stays SMC_BLOCK).
 //
 // Generated hooks (codegen.cpp): SMC_N, SMC_M, SMC_BLOCK, SMC_MINB, SMC_SW_S, SMC_SW_G,
-//   SMC_OFF_X0/LAW/HREP/HK/HN/CHG, SMC_TAB_BYTES, SMC_ANY_HILL, SMC_ANY_GENERAL,
-//   SMC_ANY_EXPLICIT (+ smc_explicit4), smc_sweep(X, P), SMC_TMAX, SmcMon.
+//   SMC_SW_C, SMC_SW_XD, SMC_SW_ANYGEN, SMC_OFF_X0/LAW/SWLAW/HREP/HK/HN/CHG,
+//   SMC_TAB_BYTES, SMC_ANY_HILL, SMC_ANY_GENERAL, SMC_ANY_EXPLICIT (+ smc_explicit4),
+//   smc_sweep(X, P), SMC_TMAX, SmcMon.
 
 #ifndef SMC_BURST
 #define SMC_BURST 8
