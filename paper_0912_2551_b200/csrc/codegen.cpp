@@ -1070,7 +1070,9 @@ std::string generate_source(const Model& m, const Property& p, int variant, cons
         // 4 -> 1.14e10, 5 -> 8.8e9 events/s: the sweep's ILP needs the registers)
         const int blk = tl->sw_blk;
         const size_t per_cta = tl->bytes + (size_t)blk * (tl->sw_xd ? 8 : 4) * (size_t)(m.N + 1) + 1024 + 64;
-        int minb = (int)std::max<size_t>(1, std::min<size_t>(8, 233472 / per_cta));   // smem-bound CTAs per SM
+        // CTAs per SM: bounded by shared memory and by the ~384 resident threads whose
+        // ~168 registers (the sweep's ILP) fill the register file
+        int minb = (int)std::max<size_t>(1, std::min<size_t>((size_t)std::max(1, 384 / blk), 233472 / per_cta));
         if (const char* e = std::getenv("SMC_MINB")) minb = std::atoi(e);
         o << "#define SMC_SWEEP 1\n#define SMC_BLOCK " << blk << "\n#define SMC_MINB " << std::max(1, minb) << "\n";
         o << "#define SMC_SW_XD " << (tl->sw_xd ? 1 : 0) << "\n#define SMC_OFF_SWLAW " << tl->off_swlaw
