@@ -637,6 +637,23 @@ std::string sweep_code_xd(const Model& m, int S, int G) {
         o << "__device__ __forceinline__ double smc_law" << k << "(const double (&x)[SMC_N]) {\n";
         o << xd_law_body(m, k, form[(size_t)k], "smc_rc", nullptr) << "}\n";
     }
+    // SMC_SW_FMAACC (reading R25): g + c_k h_k with one rounding (fused multiply-add) for the
+    // mass-action laws of order <= 2; the others add their law value
+    bool fmaacc = true;
+    if (const char* e = std::getenv("SMC_SW_FMAACC")) fmaacc = std::atoi(e) != 0;
+    for (int k = 0; k < M; ++k) {
+        const Reaction& r = m.R[(size_t)k];
+        const std::string K = std::to_string(k), C = "smc_rc[" + K + "]";
+        const std::string a = std::to_string(r.s[0]), b = std::to_string(r.s[1]);
+        o << "__device__ __forceinline__ double smc_lawacc" << k << "(const double (&x)[SMC_N], double g) {\n    return ";
+        const int f = form[(size_t)k];
+        if (!fmaacc || r.hill || !r.rate.empty() || f == 4) o << "__dadd_rn(g, smc_law" << k << "(x));\n}\n";
+        else if (f == 0) o << "__dadd_rn(g, " << C << ");\n}\n";
+        else if (f == 1) o << "__fma_rn(" << C << ", x[" << a << "], g);\n}\n";
+        else if (f == 2) o << "__fma_rn(" << C << ", __dmul_rn(x[" << a << "], __dadd_rn(x[" << a << "], -1.0)), g);\n}\n";
+        else o << "__fma_rn(" << C << ", __dmul_rn(x[" << a << "], x[" << b << "]), g);\n}\n";
+    }
+    o << "#define SMC_SW_FMAACC " << (fmaacc ? 1 : 0) << "\n";
     bool any_explicit = false;
     for (auto& r : m.R) any_explicit |= !r.rate.empty();
     if (any_explicit) {
@@ -657,7 +674,7 @@ std::string sweep_code_xd(const Model& m, int S, int G) {
         for (int k = k0; k < k1; ++k) {
             const char* acc = (split == 2 && ((k - k0) & 1)) ? "h" : "g";
             if (k - k0 < split) o << "    " << acc << " = smc_law" << k << "(x);\n";
-            else o << "    " << acc << " = __dadd_rn(" << acc << ", smc_law" << k << "(x));\n";
+            else o << "    " << acc << " = smc_lawacc" << k << "(x, " << acc << ");\n";
         }
         if (split == 2 && k1 - k0 > 1) o << "    g = __dadd_rn(g, h);\n";
         if (gi == 0) o << "    P[0] = g;\n";

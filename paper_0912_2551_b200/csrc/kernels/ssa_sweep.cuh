@@ -114,6 +114,27 @@ __device__ __forceinline__ double smc_law_sw(int k, const SmcXCol& X, const SmcS
     return __dmul_rn(L.c, h);
 }
 
+// acc + a_k for pass 2, in the arithmetic of pass 1's accumulation: with SMC_SW_FMAACC
+// (reading R25) fma(c, h, acc) -- one rounding -- for the sweep-format laws, acc + a_k for
+// the general ones
+#ifndef SMC_SW_FMAACC
+#define SMC_SW_FMAACC 0
+#endif
+__device__ __forceinline__ double smc_acc_sw(int k, double acc, const SmcXCol& X, const SmcSwTabs& T) {
+#if SMC_SW_FMAACC && SMC_SW_XD
+    const SmcLaw L = T.swlaw[k];
+#if SMC_SW_ANYGEN
+    if (L.u0 & 2u) return __dadd_rn(acc, smc_law_gen(k, X, T));
+#endif
+    const char* xb = (const char*)X.p;
+    const double v0 = *(const double*)(xb + (L.u0 & ~3u));
+    const double v1 = *(const double*)(xb + L.u1);
+    return __fma_rn(L.c, __dmul_rn(v0, __dadd_rn(v1, (L.u0 & 1u) ? -1.0 : 0.0)), acc);
+#else
+    return __dadd_rn(acc, smc_law_sw(k, X, T));
+#endif
+}
+
 // non-negative doubles (and -0) order like their bit patterns as signed int64
 __device__ __forceinline__ smc_i64 smc_ord(double v) { return __double_as_longlong(v); }
 
@@ -131,13 +152,10 @@ __device__ __forceinline__ int smc_pick(int gi, double base, double target, cons
     double acc = base;
 #pragma unroll 1
     for (int c0 = j0; c0 < j0 + SMC_SW_S; c0 += SMC_SW_C) {
-        double av[SMC_SW_C];
-#pragma unroll
-        for (int m = 0; m < SMC_SW_C; ++m) av[m] = smc_law_sw(c0 + m, X, T);
         int cnt = 0;
 #pragma unroll
         for (int m = 0; m < SMC_SW_C; ++m) {
-            acc = __dadd_rn(acc, av[m]);
+            acc = smc_acc_sw(c0 + m, acc, X, T);      // the law reads do not depend on acc
             cnt += (smc_ord(acc) <= tb) ? 1 : 0;
         }
         if (cnt < SMC_SW_C) return c0 + cnt;

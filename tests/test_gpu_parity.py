@@ -247,14 +247,15 @@ def test_large_networks_vs_oracle_fixture(smc, name, variant):
     assert m.last_launch(p)["variant"] == variant
 
 
-@pytest.mark.parametrize("xd,block", [("0", None), ("1", "96"), ("0", "224")])
-def test_sweep_shapes_vs_fixture(smc, xd, block, monkeypatch):
-    """The sweep variant with int32 count columns (exact fma laws, I2F in the selection) and
-    other CTA sizes (the column stride and the pre-scaled law offsets follow it) gives the
-    oracle's C4 replicas."""
+@pytest.mark.parametrize("xd,block,fmaacc", [("0", None, "1"), ("1", "96", "1"), ("0", "224", "1"), ("1", None, "0")])
+def test_sweep_shapes_vs_fixture(smc, xd, block, fmaacc, monkeypatch):
+    """The sweep variant with int32 count columns (exact fma laws, I2F in the selection), other
+    CTA sizes (the column stride and the pre-scaled law offsets follow it) and with / without
+    the fused accumulation of reading R25 gives the oracle's C4 replicas."""
     import json
     import os
     monkeypatch.setenv("SMC_SW_XD", xd)
+    monkeypatch.setenv("SMC_SW_FMAACC", fmaacc)
     if block:
         monkeypatch.setenv("SMC_SW_BLOCK", block)
     fx = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "c4_oracle.json")))
