@@ -601,7 +601,7 @@ std::string xd_law_body(const Model& m, int k, int f, const char* rc, const Hill
     switch (f) {
         case 0: o << "    double v = " << C << ";\n"; break;
         case 1: o << "    double v = __dmul_rn(" << C << ", x[" << a << "]);\n"; break;
-        case 2: o << "    double v = __dmul_rn(" << C << ", __dmul_rn(x[" << a << "], __dadd_rn(x[" << a << "], -1.0)));\n"; break;
+        case 2: o << "    double v = __dmul_rn(" << C << ", __fma_rn(x[" << a << "], x[" << a << "], -x[" << a << "]));\n"; break;
         case 3: o << "    double v = __dmul_rn(" << C << ", __dmul_rn(x[" << a << "], x[" << b << "]));\n"; break;
         default: {                                   // order 3-4 / unfoldable homodimer: exact int64 h
             std::vector<std::string> terms;
@@ -650,7 +650,7 @@ std::string sweep_code_xd(const Model& m, int S, int G) {
         if (!fmaacc || r.hill || !r.rate.empty() || f == 4) o << "__dadd_rn(g, smc_law" << k << "(x));\n}\n";
         else if (f == 0) o << "__dadd_rn(g, " << C << ");\n}\n";
         else if (f == 1) o << "__fma_rn(" << C << ", x[" << a << "], g);\n}\n";
-        else if (f == 2) o << "__fma_rn(" << C << ", __dmul_rn(x[" << a << "], __dadd_rn(x[" << a << "], -1.0)), g);\n}\n";
+        else if (f == 2) o << "__fma_rn(" << C << ", __fma_rn(x[" << a << "], x[" << a << "], -x[" << a << "]), g);\n}\n";
         else o << "__fma_rn(" << C << ", __dmul_rn(x[" << a << "], x[" << b << "]), g);\n}\n";
     }
     o << "#define SMC_SW_FMAACC " << (fmaacc ? 1 : 0) << "\n";

@@ -107,7 +107,8 @@ __device__ __forceinline__ double smc_law_sw(int k, const SmcXCol& X, const SmcS
     const smc_xt v0 = *(const smc_xt*)(xb + (L.u0 & ~3u));
     const smc_xt v1 = *(const smc_xt*)(xb + L.u1);
 #if SMC_SW_XD
-    const double h = __dmul_rn(v0, __dadd_rn(v1, (L.u0 & 1u) ? -1.0 : 0.0));   // exact shift by 0 / -1
+    // x0 (x1 - d), d = 1 for a homodimer: one rounding of the exact x0 x1 - d x0
+    const double h = __fma_rn(v0, v1, (L.u0 & 1u) ? -v0 : 0.0);
 #else
     const double h = (double)((smc_i64)v0 * (smc_i64)(v1 - (int)(L.u0 & 1u)));
 #endif
@@ -129,7 +130,7 @@ __device__ __forceinline__ double smc_acc_sw(int k, double acc, const SmcXCol& X
     const char* xb = (const char*)X.p;
     const double v0 = *(const double*)(xb + (L.u0 & ~3u));
     const double v1 = *(const double*)(xb + L.u1);
-    return __fma_rn(L.c, __dmul_rn(v0, __dadd_rn(v1, (L.u0 & 1u) ? -1.0 : 0.0)), acc);
+    return __fma_rn(L.c, __fma_rn(v0, v1, (L.u0 & 1u) ? -v0 : 0.0), acc);
 #else
     return __dadd_rn(acc, smc_law_sw(k, X, T));
 #endif
