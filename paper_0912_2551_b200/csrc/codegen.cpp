@@ -926,7 +926,9 @@ TileLayout pack_tables(const Model& m, bool sweep) {
     // the dependency walk reads contiguous entries instead of random law-table rows (the
     // law-table gather was 24 % of C4's shared-memory wavefronts, 70 % of them bank-conflict
     // excess)
-    L.fatdep = !L.dep16 && N <= 4095;
+    // (only while the 16-byte entries keep the tables small: a dense dep(j) at M ~ 500 would
+    // otherwise not fit in shared memory)
+    L.fatdep = !L.dep16 && N <= 4095 && 16 * nnz <= 48 * 1024;
     if (const char* e = std::getenv("SMC_FATDEP")) L.fatdep = std::atoi(e) != 0 && !L.dep16 && N <= 4095;
     L.off_dep_off = o; o = align16(o + 4 * ((size_t)(L.depsp ? N : M) + 1));
     L.off_dep = o; o = align16(o + (L.fatdep ? 16 : (L.dep16 ? 2 : 4)) * (L.depsp ? nnz_sp : nnz));
