@@ -93,8 +93,8 @@ int smc_model_set_hill(smc_model* m, int32_t reaction, int32_t repressor, double
  * position) / SMC_E_ARG otherwise. */
 int smc_model_set_rate_expr(smc_model* m, int32_t reaction, const char* expr, const char* const* species_names);
 
-/* Force a kernel variant: 0 = automatic (1 for N, M <= 32; 4 for N <= 200,
- * M <= 512; else 2), 1 = thread-owned (registers; requires N <= 32 and
+/* Force a kernel variant: 0 = automatic (1 for N, M <= 32; 4 for N <= 160,
+ * M <= 1024; else 2), 1 = thread-owned (registers; requires N <= 32 and
  * M <= 32), 2 = warp-owned tile (propensities and counts in shared memory,
  * dependency graph), 4 = thread-owned sweep (counts in a shared-memory column,
  * every law re-evaluated per event; requires the counts of 128 trajectories to

@@ -53,10 +53,11 @@ int Model::variant() const {
     if (variant_forced) return variant_forced;
     if (N <= 32 && M <= 32) return 1;
     // sweep for mid-size networks (pass 1 is straight-line code over all M laws with the
-    // counts in registers); measured faster than the tile kernel up to M = 512 for N up to
-    // 160 (scripts/variant_boundary.py: 1.4-3.4x) and slower at C5 (N 200, M 1000: 0.56x).
-    // SMC_SWEEP=0/1 forces the automatic choice off / on
-    bool sweep = N <= 200 && M <= 512;
+    // counts in registers): the register copy of the counts decides -- measured faster than
+    // the tile kernel for N <= 160 up to M = 1000 (scripts/variant_boundary.py: 1.3-3.4x),
+    // slower at N = 200 (M 512: 0.54x, C5's M 1000: 0.56x).  SMC_SWEEP=0/1 forces the
+    // automatic choice off / on
+    bool sweep = N <= 160 && M <= 1024;
     if (const char* e = std::getenv("SMC_SWEEP")) sweep = std::atoi(e) != 0;
     return (sweep && sweep_fits()) ? 4 : 2;
 }

@@ -33,6 +33,8 @@ def main():
     smc.use_torch()
     sizes = [(64, 512, 40000), (80, 300, 40000), (100, 400, 40000), (128, 400, 30000), (128, 512, 30000),
              (160, 500, 20000)]
+    if len(sys.argv) > 1:                 # N,M,replicas ...
+        sizes = [tuple(int(v) for v in a.split(",")) for a in sys.argv[1:]]
     for (N, M, n) in sizes:
         net = workloads.random_network(11, N, M)
         cfg = dict(name="rn%d_%d" % (N, M), species=net["species"], x0=net["x0"], reactions=net["reactions"],
