@@ -2,6 +2,7 @@
 // hook), launch configuration of the persistent kernels, shard slices,
 // counters, the allreduce hook, and the iterative Wilson loop of Fig. 2.
 #include <cuda_runtime.h>
+#include <mutex>
 
 #include <algorithm>
 #include <cmath>
@@ -52,6 +53,33 @@ void* dalloc(size_t bytes) {
     }
     return p;
 }
+// Small pinned host blocks (the per-model count read-back and Wilson loop state) come
+// from a process-wide pool: cudaMallocHost / cudaFreeHost cost ~1 ms each (and the free
+// synchronises the device), which a user creating a model per query would pay every call.
+constexpr size_t kPinnedBlock = 1024;
+std::mutex g_pinned_mu;
+std::vector<void*> g_pinned_free;
+void* pinned_alloc(size_t bytes) {
+    if (bytes > kPinnedBlock) fail(SMC_E_ARG, "internal: pinned block too large");
+    std::lock_guard<std::mutex> lk(g_pinned_mu);
+    if (g_pinned_free.empty()) {
+        constexpr size_t kSlab = 64;
+        char* slab = nullptr;
+        if (cudaMallocHost((void**)&slab, kSlab * kPinnedBlock) != cudaSuccess || !slab)
+            fail(SMC_E_CUDA, "cudaMallocHost (pinned pool)");
+        for (size_t i = 0; i < kSlab; ++i) g_pinned_free.push_back(slab + i * kPinnedBlock);
+    }
+    void* b = g_pinned_free.back();
+    g_pinned_free.pop_back();
+    std::memset(b, 0, kPinnedBlock);
+    return b;
+}
+void pinned_free(void* b) {
+    if (!b) return;
+    std::lock_guard<std::mutex> lk(g_pinned_mu);
+    g_pinned_free.push_back(b);
+}
+
 void dfree(void* p) {
     if (!p) return;
     Hooks& h = hooks();
@@ -112,8 +140,8 @@ struct DeviceState {
         }
         if (e0) cudaEventDestroy(e0);
         if (e1) cudaEventDestroy(e1);
-        if (host_counts) cudaFreeHost(host_counts);
-        if (wst_host) cudaFreeHost(wst_host);
+        pinned_free(host_counts);
+        pinned_free(wst_host);
         dfree(wst_dev);
         dfree(ctl);
         dfree(spec_v);
@@ -140,7 +168,7 @@ DeviceState& device(Model& m) {
         ck(cudaDeviceGetAttribute(&d->sm_count, cudaDevAttrMultiProcessorCount, dev), "attr");
         ck(cudaDeviceGetAttribute(&d->max_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev), "attr");
         d->ctl = dalloc(128);
-        ck(cudaMallocHost((void**)&d->host_counts, 128), "cudaMallocHost");
+        d->host_counts = (int64_t*)pinned_alloc(128);
         ck(cudaEventCreate(&d->e0), "cudaEventCreate");
         ck(cudaEventCreate(&d->e1), "cudaEventCreate");
         m.dev.reset(d.release());
@@ -522,7 +550,7 @@ int device_estimate(Model& m, PropKernel& pk, uint64_t seed, double confidence, 
     DeviceState& d = *m.dev;
     if (!d.wst_dev) {
         d.wst_dev = (SmcWState*)dalloc(sizeof(SmcWState));
-        ck(cudaMallocHost((void**)&d.wst_host, sizeof(SmcWState)), "cudaMallocHost");
+        d.wst_host = (SmcWState*)pinned_alloc(sizeof(SmcWState));
     }
     SmcWState w{};
     w.N = wilson_sample_size(start, eps, z);
