@@ -1082,6 +1082,7 @@ std::string generate_source(const Model& m, const Property& p, int variant, cons
         if (const char* e = std::getenv("SMC_PIPE2")) pipe2 = std::atoi(e);
         o << "#define SMC_PIPE2 " << pipe2 << "\n";
         if (const char* e = std::getenv("SMC_UNROLL")) o << "#define SMC_UNROLL " << std::atoi(e) << "\n";
+        if (const char* e = std::getenv("SMC_BURST")) o << "#define SMC_BURST " << std::max(1, std::atoi(e)) << "\n";
     } else if (variant == 4) {
         // 128-thread CTAs; resident CTAs per SM bounded by the counts' shared memory
         // (tables + 128 columns of N+1 ints) and by registers (pass 1 keeps the counts and
