@@ -987,10 +987,12 @@ TileLayout pack_tables(const Model& m, bool sweep) {
         // flags: bit 0 homodimer (h = x (x - 1), c halved as above), bit 1 general law
         // (order 3-4, explicit, Hill: the kernel takes the law-table path)
         L.sw_s = sweep_group(m);
+        // independent law reads per chunk: the whole group for S <= 8 (C4: S = C = 7), else
+        // the largest divisor of S up to 8 ((64, 512): S = 18, C = 6 8.1e9 vs C = 3 7.9e9)
         L.sw_c = 1;
         if (L.sw_s <= 8) L.sw_c = L.sw_s;
         else
-            for (int c : {5, 4, 3, 2})
+            for (int c = 8; c >= 2; --c)
                 if (L.sw_s % c == 0) { L.sw_c = c; break; }
         if (const char* e = std::getenv("SMC_SW_C")) {
             const int c = std::atoi(e);
