@@ -270,6 +270,24 @@ def test_sweep_shapes_vs_fixture(smc, xd, block, fmaacc, monkeypatch):
     assert info["variant"] == 4 and info["block_threads"] <= int(block or 384)   # launched CTA <= the compiled one
 
 
+@pytest.mark.parametrize("N,M,form", [(64, 512, "F[0,0.01](S0 > {a})"), (64, 512, "G[0,0.01](S1 > {b})"),
+                                       (100, 400, "F[0,0.01](S0 > {c})")])
+def test_sweep_mid_size_networks_vs_oracle(smc, N, M, form):
+    """The sweep at the sizes its automatic choice covers beyond C4 (groups of 18 laws read in
+    chunks of 6, 288-thread CTAs; 100 species: 256-thread CTAs at the register cap) against
+    the oracle replica for replica (C4/C5-recipe random networks)."""
+    net = workloads.random_network(11, N, M)
+    x0 = net["x0"]
+    f = form.format(a=x0[0] + 15, b=x0[1] - 15, c=x0[0] + 40)
+    cfg = dict(name="rn%d_%d" % (N, M), species=net["species"], x0=x0, reactions=net["reactions"], formula=f,
+               t_max=0.0, seed=7, sampling=dict(mode="fixed", n=60))
+    a, ae, v, e, ov, oe = _compare(smc, cfg, 7, 0, 60)
+    assert ae >= 59 / 60, (N, M, f, a, ae)
+    assert e.mean() > 100
+    m, p = _pair(smc, cfg)
+    assert m.run(p, 1, 7) and m.last_launch(p)["variant"] == 4
+
+
 @pytest.mark.parametrize("width", ["4", "8", "16", "32"])
 def test_tile_widths_vs_fixture(smc, width, monkeypatch):
     """Every tile width of variant 2 (4/8/16/32 lanes per trajectory) gives the oracle's replicas."""
