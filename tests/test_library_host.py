@@ -186,3 +186,24 @@ def test_rate_expression_errors_and_codegen():
     assert ("__dadd_rn(__dadd_rn(__dmul_rn((-(double)x[0]), 0x1p+1), -__ddiv_rn(0x1.8p+1, (double)x[1])), 0x1p+0)"
             in src)
     assert "if (x[0] < 1) return 0.0;" in src
+
+
+def test_sweep_configuration_choices():
+    """The automatic shape of the sweep kernel (DESIGN.md §5 knob table): C4 gets binary64
+    columns in one 384-thread CTA per SM, groups of 7 laws read in one chunk and fused sums;
+    a (64, 512) network groups of 18 read in chunks of 6; C5 (N = 200) the tile kernel."""
+    cfg = workloads.c4()
+    m = smc.Model.from_config(cfg)
+    src = m.kernel_source(smc.Property(m, cfg["formula"]))
+    for d in ("#define SMC_BLOCK 384", "#define SMC_MINB 1", "#define SMC_SW_XD 1", "#define SMC_SW_S 7",
+              "#define SMC_SW_C 7", "#define SMC_SW_FMAACC 1", "smc_ssa_sweep"):
+        assert d in src, d
+    net = workloads.random_network(11, 64, 512)
+    cfg2 = dict(name="rn", species=net["species"], x0=net["x0"], reactions=net["reactions"],
+                formula="F[0,1](S0 > 5)", t_max=0.0, seed=1, sampling=dict(mode="fixed", n=1))
+    m2 = smc.Model.from_config(cfg2)
+    src2 = m2.kernel_source(smc.Property(m2, cfg2["formula"]))
+    assert "#define SMC_SW_S 18" in src2 and "#define SMC_SW_C 6" in src2 and "smc_ssa_sweep" in src2
+    c5 = workloads.c5()
+    m5 = smc.Model.from_config(c5)
+    assert "smc_ssa_tile" in m5.kernel_source(smc.Property(m5, c5["formula"]))
