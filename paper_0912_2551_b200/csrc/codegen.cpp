@@ -1100,6 +1100,7 @@ std::string generate_source(const Model& m, const Property& p, int variant, cons
         o << "#define SMC_SW_XD " << (tl->sw_xd ? 1 : 0) << "\n#define SMC_OFF_SWLAW " << tl->off_swlaw
           << "\n#define SMC_SW_C " << tl->sw_c << "\n";
         if (const char* e = std::getenv("SMC_BURST")) o << "#define SMC_BURST " << std::max(1, std::atoi(e)) << "\n";
+        if (const char* e = std::getenv("SMC_SW_DSCAN")) o << "#define SMC_SW_DSCAN " << std::atoi(e) << "\n";
         o << "#define SMC_SW_ANYGEN " << ((tl->any_hill || tl->any_general || tl->any_explicit) ? 1 : 0) << "\n";
         o << "#define SMC_OFF_X0 " << tl->off_x0 << "\n#define SMC_OFF_LAW " << tl->off_law
           << "\n#define SMC_OFF_HREP " << tl->off_hill_rep << "\n#define SMC_OFF_HK " << tl->off_hill_k

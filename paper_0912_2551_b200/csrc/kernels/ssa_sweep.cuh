@@ -39,6 +39,9 @@
 #ifndef SMC_BURST
 #define SMC_BURST 8
 #endif
+#ifndef SMC_SW_DSCAN
+#define SMC_SW_DSCAN 1     // 1: prefix scan by DSETP; 2: also the in-group count
+#endif
 
 struct SmcSwTabs {
     const int* x0;
@@ -157,7 +160,11 @@ __device__ __forceinline__ int smc_pick(int gi, double base, double target, cons
 #pragma unroll
         for (int m = 0; m < SMC_SW_C; ++m) {
             acc = smc_acc_sw(c0 + m, acc, X, T);      // the law reads do not depend on acc
+#if SMC_SW_DSCAN >= 2
+            cnt += (acc <= target) ? 1 : 0;
+#else
             cnt += (smc_ord(acc) <= tb) ? 1 : 0;
+#endif
         }
         if (cnt < SMC_SW_C) return c0 + cnt;
     }
@@ -298,7 +305,11 @@ extern "C" __global__ void __launch_bounds__(SMC_BLOCK, SMC_MINB) smc_ssa_sweep(
                     bool le[SMC_SW_G];
 #pragma unroll
                     for (int i = 0; i < SMC_SW_G; ++i) {
-                        le[i] = smc_ord(Pg[i]) <= tb;
+#if SMC_SW_DSCAN
+                        le[i] = Pg[i] <= target;                // one DSETP on the FP64 pipe
+#else
+                        le[i] = smc_ord(Pg[i]) <= tb;           // two ISETP on the integer pipe
+#endif
                         gi += le[i] ? 1 : 0;
                     }
                     const double base = SmcLastLe<0, SMC_SW_G>::pick(Pg, le, 0.0);   // P_{gi-1} (0 if gi = 0)
