@@ -1264,8 +1264,8 @@ int orc_check_streaming(void* fp, int64_t n_entries, const double* t, const doub
 }
 
 // One batch of replicas [first, first+n): mode 0 = streaming (on-the-fly),
-// 1 = literal (simulate to the horizon, evaluate |=; halts at the checkpoints of
-// reading R24 once the prefix decides).  verdicts/events may be
+// 1 = literal (simulate to the horizon, evaluate |=; the event count is the first
+// index at which the observed prefix decides |=).  verdicts/events may be
 // NULL.  counts[4] = {n_true, n_false, events, errors}.
 int orc_run(void* mp, void* fp, uint64_t seed, uint64_t first, uint64_t n, int32_t mode, int64_t event_cap,
             uint8_t* verdicts, int64_t* events, int64_t* counts) {
@@ -1296,13 +1296,16 @@ int orc_run(void* mp, void* fp, uint64_t seed, uint64_t first, uint64_t n, int32
                 simulate_trace(*M, seed, i, H, event_cap, keep, &tr, &err);
                 if (err) rr = {V_ERROR, tr.n()};
                 else {
-                    // reading R24: after the sojourn of entry k is drawn, at k = 64, 128, 256, ...
-                    // (before the horizon step), the three-valued |= of the prefix entries 0..k
-                    // is final once definite; the replica then stops with k events.  The prefix
-                    // of the full trace is the prefix the simulation had at step k (the streams
-                    // are keyed by step).
-                    bool halted = false;
-                    for (int64_t k = 64; k < tr.n() && !halted; k *= 2) {
+                    // On-the-fly halting (the replica stops as soon as the formula
+                    // is decided): the event count is the FIRST k at which the three-valued |=
+                    // of the observed prefix -- entries 0..k and the sojourn of entry k, the
+                    // unobserved future unknown -- is definite.  The prefix of the stored trace
+                    // is exactly what the simulation had observed after drawing step k (the
+                    // streams are keyed by step).  Definiteness is monotone in k (observing
+                    // more never revokes a definite value), so the first such k is found by
+                    // bisection over [0, n); if no proper prefix decides, the whole trace
+                    // (horizon overshoot or absorption) does, with all n events.
+                    auto prefix_value = [&](int64_t k) {
                         Trace p;
                         p.N = tr.N;
                         p.t.assign(tr.t.begin(), tr.t.begin() + k + 1);
@@ -1310,13 +1313,24 @@ int orc_run(void* mp, void* fp, uint64_t seed, uint64_t first, uint64_t n, int32
                         p.x.assign(tr.x.begin(), tr.x.begin() + (k + 1) * tr.N);
                         p.absorbed = false;
                         LiteralChecker pc(*f, p);
-                        const Tri pv = pc.value(f->root, 0);
-                        if (pv != T_UNKNOWN) { rr = {pv == T_TRUE ? V_TRUE : V_FALSE, k}; halted = true; }
-                    }
-                    if (!halted) {
+                        return pc.value(f->root, 0);
+                    };
+                    const int64_t n_ev = tr.n();
+                    const int64_t last = n_ev - 1;
+                    Tri pv = T_UNKNOWN;
+                    if (last >= 0) pv = prefix_value(last);
+                    if (pv != T_UNKNOWN) {
+                        int64_t lo = 0, hi = last;        // invariant: prefix hi is definite
+                        while (lo < hi) {
+                            const int64_t mid = lo + (hi - lo) / 2;
+                            if (prefix_value(mid) != T_UNKNOWN) hi = mid; else lo = mid + 1;
+                        }
+                        const Tri v = prefix_value(hi);
+                        rr = {v == T_TRUE ? V_TRUE : V_FALSE, hi};
+                    } else {
                         LiteralChecker lc(*f, tr);
                         Tri v = lc.value(f->root, 0);
-                        rr = {v == T_TRUE ? V_TRUE : V_FALSE, tr.n()};
+                        rr = {v == T_TRUE ? V_TRUE : V_FALSE, n_ev};
                     }
                 }
             }
