@@ -5,12 +5,19 @@ end-to-end and clock records.  One JSON line on rank 0.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C2] [--impl smc|reference]
 
-A step is one pass of the whole hot path over one batch: for a Wilson workload
-(C2, C5) the full Fig. 2 estimate (all rounds: SSA + on-the-fly monitor + counts
-+ allreduce + Wilson step); for a fixed-N workload (C1, C3, C4) one smc_run of
-its N replicas.  Default workload: C2 = BASELINE.json configs[1].
-Multi-GPU: one process per GPU (torchrun), NCCL allreduce of the counts per
-round, time = max over ranks.
+A step is one pass of the whole hot path over one batch:
+  * default workload C5 (BASELINE.json configs[4], 200 species x 1000 reactions, the
+    largest single-GPU configuration): one step = the FIRST ROUND of its Fig. 2 loop
+    (P:359-372), N = Eq. 4(p = 1, eps = 1e-4, 99.9 %) = 54,128 replicas per GPU
+    (SSA + on-the-fly monitor + counts + the NCCL allreduce of the round), through
+    smc_run; the complete Wilson stop (~2.7e8 replicas) is a separate long run
+    (scripts/c5_wilson_stop.py);
+  * a Wilson workload (--workload C2): the full Fig. 2 estimate (all rounds);
+  * a fixed-N workload (C1, C3, C4): one smc_run of its N replicas per GPU.
+Multi-GPU: one process per GPU (torchrun; `--gpus N` without torchrun re-launches
+itself under torch.distributed.run), each rank runs its own slice of every round
+(index-sharded), NCCL allreduce of the int64 counts per round, time =
+max over ranks.  Per-GPU work is fixed as N grows ("scaling": "weak").
 """
 import argparse
 import json
@@ -31,6 +38,47 @@ SM_COUNT_DEFAULT = 148
 
 def env_rank():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+
+
+def relaunch_under_torchrun(n):
+    """`bench.py --gpus N` outside torchrun: re-exec as N ranks (one per GPU) on 127.0.0.1."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_FILE", os.path.join("/tmp", "smc_nccl.%h.%p.log"))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(n),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def bench_config(name, impl="smc"):
+    """The bench workload: C5 = the first Fig. 2 round of configs[4] per GPU; others as defined.
+    N = Eq. 4 at p = 1 (Fig. 2's first line) from the library (GPU arm) or the oracle (reference arm)."""
+    cfg = workloads.get(name)
+    if cfg["name"] == "C5":
+        s = cfg["sampling"]
+        if impl == "reference":
+            from oracle import normal_quantile, wilson_sample_size
+            n1 = int(wilson_sample_size(1.0, s["half_width"], normal_quantile(s["confidence"])))
+        else:
+            from paper_0912_2551_b200 import smc_wilson_sample_size
+            n1 = int(smc_wilson_sample_size(1.0, s["half_width"], s["confidence"]))
+        cfg = workloads.with_sampling(cfg, mode="fixed", n=n1, round="first Fig. 2 round of the Wilson stop",
+                                      confidence=s["confidence"], half_width=s["half_width"])
+    return cfg
 
 
 # ------------------------------------------------------------- algorithmic work
@@ -223,7 +271,9 @@ def run_reference(args, cfg):
             "config": {"workload": cfg["name"], "formula": cfg["formula"], "sampling": cfg["sampling"],
                        "sample_per_step": "%s (time-budgeted %.0f s)" % (last["what"], budget)},
             "cpu_baseline": {"value": value, "unit": "events/s", "cores": last["procs"], "kind": "oracle",
-                             "sample": "%s per step, %d processes" % (last["what"], last["procs"])},
+                             "cpu": cpu_model(),
+                             "sample": "%s per step, %d single-threaded oracle processes on %s"
+                                       % (last["what"], last["procs"], cpu_model())},
             "e2e": {"value": value, "unit": "events/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -234,7 +284,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="C2")
+    ap.add_argument("--workload", default="C5")
     ap.add_argument("--impl", default="smc", choices=["smc", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -242,7 +292,9 @@ def main():
                     help="override fixed-N replica count (diagnostics; --replicas under torchrun)")
     ap.add_argument("--variant", type=int, default=0)
     args = ap.parse_args()
-    cfg = workloads.get(args.workload)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_under_torchrun(args.gpus)
+    cfg = bench_config(args.workload, args.impl)
     if args.n:
         cfg = workloads.with_sampling(cfg, mode="fixed", n=args.n)
     if args.impl == "reference":
@@ -253,6 +305,8 @@ def main():
 
     import paper_0912_2551_b200 as smc
     rank, local_rank, world = env_rank()
+    if world != args.gpus:
+        raise SystemExit("bench.py: --gpus %d but WORLD_SIZE=%d" % (args.gpus, world))
     torch.cuda.set_device(local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
@@ -272,7 +326,7 @@ def main():
             est = smc.estimate(model, prop, samp["confidence"], samp["half_width"], cfg["seed"])
             return est["events"], est["n_total"], est
         model.reset()
-        c = model.run(prop, samp["n"], cfg["seed"])
+        c = model.run(prop, samp["n"] * world, cfg["seed"])      # weak scaling: n replicas per GPU
         return c["events"], c["n_true"] + c["n_false"], c
 
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")   # > 126 MB L2
@@ -368,7 +422,7 @@ def main():
             r = smc.estimate(m2, p2, samp["confidence"], samp["half_width"], cfg["seed"])
             e2e_events += r["events"]
         else:
-            r = m2.run(p2, samp["n"], cfg["seed"])
+            r = m2.run(p2, samp["n"] * world, cfg["seed"])
             e2e_events += r["events"]
         torch.cuda.synchronize()
         e2e_ms += (time.perf_counter() - t0) * 1e3
@@ -385,15 +439,17 @@ def main():
         s = oracle_sample(cfg, args.cpu_seconds)
         cpu = {"value": s["events"] / s["seconds"], "unit": "events/s", "cores": s["procs"], "kind": "oracle",
                "trajectories_per_s": s["trajectories"] / s["seconds"],
-               "sample": "%s of %s (seed %d), %d processes, %.1f s"
-                         % (s["what"], cfg["name"], cfg["seed"], s["procs"], s["seconds"])}
+               "cpu": cpu_model(),
+               "sample": "%s of %s (seed %d), %d single-threaded oracle processes on %s, %.1f s"
+                         % (s["what"], cfg["name"], cfg["seed"], s["procs"], cpu_model(), s["seconds"])}
 
     if rank == 0:
         line = {"metric": "SSA events/s", "value": value, "unit": "events/s", "trajectories_per_s": traj_s,
                 "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": tot_ms / args.steps,
-                "higher_is_better": True, "scaling": "strong" if samp["mode"] == "wilson" else "strong",
+                "higher_is_better": True, "scaling": "strong" if samp["mode"] == "wilson" else "weak",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": cfg["name"], "formula": cfg["formula"], "sampling": samp,
+                           "replicas_per_step": (samp["n"] * world) if samp["mode"] == "fixed" else None,
                            "species": len(cfg["species"]), "reactions": len(cfg["reactions"]),
                            "parallelism": "dp%d" % world, "l2": "flushed (256 MB write) between timed steps",
                            "variant": info["variant"], "block": info["block_threads"], "grid": info["grid_blocks"],

@@ -64,7 +64,12 @@ extern "C" __global__ void __launch_bounds__(SMC_BLOCK, 2) smc_ssa_literal(SmcPa
                 const int r = smc_lit_eval(tb, ub, mb, vb, (long long)k, false, (long long)cap);
                 if (r != 2) { decided = r; break; }       // prefix decides |= (reading R24)
             }
-            if (k + 1 >= cap || k + 1 >= P.event_cap) { err = true; break; }
+            if (k + 1 >= P.event_cap) {                   // the next event would reach the cap: the
+                const int r = smc_lit_eval(tb, ub, mb, vb, (long long)k, false, (long long)cap);
+                if (r != 2) decided = r; else err = true;   // prefix decides now, else an error
+                break;
+            }
+            if (k + 1 >= cap) { err = true; break; }      // trace buffer full (reading R23)
             // selection (Eq. 2b): first j with sum_{i<=j} a_i > u2 a0 (left to right)
             const double target = __dmul_rn(u2, A);
             double acc = 0.0;

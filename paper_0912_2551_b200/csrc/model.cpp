@@ -189,19 +189,30 @@ int smc_model_set_variant(smc_model* h, int32_t variant) {
         set_error("smc_model_set_variant: thread-owned variant needs N <= 32 and M <= 32");
         return SMC_E_ARG;
     }
+    std::lock_guard<std::mutex> lk(m.mu);
+    if (m.dev && variant != m.variant_forced) {
+        set_error("smc_model_set_variant: model already used by a run");
+        return SMC_E_ARG;
+    }
     m.variant_forced = variant;
     return SMC_OK;
 }
 
 int smc_model_set_event_cap(smc_model* h, uint64_t cap) {
-    if (!h || cap < 1 || cap > 0xFFFFFFFFull) { set_error("smc_model_set_event_cap: 1 <= cap < 2^32"); return SMC_E_ARG; }
-    h->m.event_cap = cap;
+    // per-replica event counts are int32 on the device (events_out, spec_e)
+    if (!h || cap < 1 || cap > 0x7FFFFFFFull) { set_error("smc_model_set_event_cap: 1 <= cap <= 2^31 - 1"); return SMC_E_ARG; }
+    Model& m = h->m;
+    std::lock_guard<std::mutex> lk(m.mu);
+    if (m.dev && cap != m.event_cap) { set_error("smc_model_set_event_cap: model already used by a run"); return SMC_E_ARG; }
+    m.event_cap = cap;
     return SMC_OK;
 }
 
 int smc_model_set_speculation(smc_model* h, int32_t on) {
     if (!h) { set_error("smc_model_set_speculation: NULL model"); return SMC_E_ARG; }
-    h->m.speculate = on != 0;
+    Model& m = h->m;
+    std::lock_guard<std::mutex> lk(m.mu);
+    m.speculate = on != 0;
     return SMC_OK;
 }
 

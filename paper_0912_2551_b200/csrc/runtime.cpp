@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 
@@ -106,6 +107,7 @@ struct PropKernel {
     unsigned char* lit_val = nullptr;
     unsigned long long lit_cap = 0;
     smc_launch_info info{};
+    uint64_t cap_global = 0;               // sum of capacity() over the ranks (one allreduce)
     uint64_t capacity() const {            // trajectories resident at once on this GPU
         return (uint64_t)grid_max * (uint64_t)(variant != 2 ? block : (block / 32) * per_warp);
     }
@@ -130,6 +132,7 @@ struct DeviceState {
     SmcWState* wst_host = nullptr;  // pinned
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     int sm_count = 0, max_smem_optin = 0;
+    uint64_t spec_max = 0;          // most replicas one rank's speculative batch may hold
     std::map<uint64_t, PropKernel> kernels;
     ~DeviceState() {
         for (auto& kv : kernels) {
@@ -171,6 +174,13 @@ DeviceState& device(Model& m) {
         d->host_counts = (int64_t*)pinned_alloc(128);
         ck(cudaEventCreate(&d->e0), "cudaEventCreate");
         ck(cudaEventCreate(&d->e1), "cudaEventCreate");
+        // speculative per-replica buffers (1 byte verdict + 4 bytes events per replica) are
+        // held to a quarter of the free memory and 8 GiB; a round needing more runs
+        // non-speculatively into the counters (O(1) memory, identical counts)
+        size_t free_b = 0, total_b = 0;
+        ck(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+        d->spec_max = std::max<uint64_t>(1u << 20, std::min<uint64_t>(free_b / 4, (uint64_t)8 << 30) / 5);
+        if (const char* e = std::getenv("SMC_SPEC_MAX")) d->spec_max = std::max<uint64_t>(1, std::strtoull(e, nullptr, 10));
         m.dev.reset(d.release());
     }
     return *m.dev;
@@ -393,14 +403,31 @@ void harvest_spec_events(Model& m, PropKernel& pk) {
     d.spec_events_host = false;
 }
 
+// Sum of the ranks' resident capacities (world > 1): one allreduce of int64[4] through the
+// hook, once per property.  Every rank must size speculative batches from the same number.
+void global_capacity(Model& m, PropKernel& pk) {
+    Hooks& h = hooks();
+    if (h.world <= 1 || pk.cap_global) return;
+    DeviceState& d = *m.dev;
+    d.host_counts[0] = (int64_t)pk.capacity();
+    d.host_counts[1] = d.host_counts[2] = d.host_counts[3] = 0;
+    ck(cudaMemcpyAsync(d.counters(), d.host_counts, 32, cudaMemcpyHostToDevice, stream()), "H2D capacity");
+    if (h.allreduce && h.allreduce(d.counters(), 4, h.allreduce_user) != 0) fail(SMC_E_COMM, "allreduce hook failed");
+    ck(cudaMemcpyAsync(d.host_counts, d.counters(), 32, cudaMemcpyDeviceToHost, stream()), "D2H capacity");
+    ck(cudaStreamSynchronize(stream()), "cudaStreamSynchronize");
+    pk.cap_global = (uint64_t)std::max<int64_t>(1, d.host_counts[0]);
+}
+
 // Launch a speculative batch starting at replica `covered`: at least `need` replicas,
 // else as many as all GPUs hold at once, never past the conservative size `limit`.
+// S depends only on values every rank shares (need, limit, the allreduced capacity sum and
+// the budget), so the ranks' slices tile [covered, covered + S) exactly.
 void launch_batch(Model& m, PropKernel& pk, uint64_t seed, uint64_t covered, uint64_t need, uint64_t limit) {
     DeviceState& d = *m.dev;
     Hooks& h = hooks();
-    const uint64_t cap_all = pk.capacity() * (uint64_t)h.world;
+    const uint64_t cap_all = h.world > 1 ? pk.cap_global : pk.capacity();
     const uint64_t room = limit > covered ? limit - covered : 0;
-    const uint64_t S = std::max(need, std::min(cap_all, room));
+    const uint64_t S = std::max(need, std::min(std::min(cap_all, room), d.spec_max * (uint64_t)h.world));
     uint64_t lo = covered, hi = covered + S;
     if (h.world > 1) smc_shard_range(covered, S, h.rank, h.world, &lo, &hi);
     if (hi - lo > d.spec_cap) {
@@ -478,6 +505,12 @@ namespace {
 // One Fig. 2 step after a round's counts; the device twin is
 // smc_wilson_rounds() in aot_kernels.cu (same operations, same order).
 void wilson_host_step(SmcWState& w, const smc_counts& c, double eps, double z) {
+    // every replica of the round gives exactly one verdict or error on exactly one rank:
+    // a mis-tiled shard (or a failed reduction) shows up here and fails loudly
+    if (c.n_true < 0 || c.n_false < 0 || c.errors < 0 || c.n_true + c.n_false + c.errors != w.N) {
+        w.status = 3;
+        return;
+    }
     w.cursor += (unsigned long long)w.N;
     w.n_tot += c.n_true + c.n_false;                     // errors excluded from trials
     w.yes += c.n_true;
@@ -508,6 +541,10 @@ int wilson_finish(const SmcWState& w, double z, smc_estimate_t* out) {
     if (w.status == 2) {
         set_error("more than 1% of replicas ended in error (overflow / event cap / bad propensity)");
         return SMC_E_ERRRATE;
+    }
+    if (w.status == 3) {
+        set_error("a round's counts do not add up to its replica count (shards or reduction inconsistent)");
+        return SMC_E_COMM;
     }
     if (w.status != 1) {
         set_error("Wilson loop did not terminate");
@@ -542,8 +579,8 @@ int wilson_loop(Runner&& run, double confidence, double eps, double start, smc_e
 // loop state once.  A round only partly covered by the live batch is run on the host
 // (spec_round: counts the covered part, launches the next batch).  Identical results to
 // wilson_loop (test_speculative_rounds_identical).
-int device_estimate(Model& m, PropKernel& pk, uint64_t seed, double confidence, double eps, double start,
-                    uint64_t limit, smc_estimate_t* out) {
+int device_estimate(Model& m, const Property& p, PropKernel& pk, uint64_t seed, double confidence, double eps,
+                    double start, uint64_t limit, smc_estimate_t* out) {
     std::memset(out, 0, sizeof *out);
     const double z = normal_quantile(confidence);
     out->z = z;
@@ -556,6 +593,13 @@ int device_estimate(Model& m, PropKernel& pk, uint64_t seed, double confidence, 
     w.N = wilson_sample_size(start, eps, z);
     while (w.status == 0 && w.rounds < 100000) {
         const uint64_t end = w.cursor + (uint64_t)w.N;
+        if ((uint64_t)w.N > d.spec_max && !(d.spec_valid && w.cursor >= d.spec_begin && end <= d.spec_end)) {
+            harvest_spec_events(m, pk);                  // round too big to buffer: counters only
+            smc_counts c{};
+            run_round(m, p, seed, w.cursor, (uint64_t)w.N, &c);
+            wilson_host_step(w, c, eps, z);
+            continue;
+        }
         if (!(d.spec_valid && w.cursor >= d.spec_begin && end <= d.spec_end)) {
             if (d.spec_valid && w.cursor >= d.spec_begin && w.cursor < d.spec_end) {
                 smc_counts c{};
@@ -627,6 +671,7 @@ int smc_reset(smc_model* h) {
 
 int smc_run(smc_model* h, const smc_property* ph, uint64_t n, uint64_t seed, smc_counts* out) {
     if (!h || !ph || !out) { set_error("smc_run: NULL argument"); return SMC_E_ARG; }
+    if (ph->p->N != h->m.N) { set_error("smc_run: property compiled for a model with another species count"); return SMC_E_ARG; }
     return guard([&] {
         Model& m = h->m;
         std::lock_guard<std::mutex> lk(m.mu);
@@ -655,6 +700,7 @@ int smc_estimate_ex(smc_model* h, const smc_property* ph, double confidence, dou
                   "start in [0,1]");
         return SMC_E_ARG;
     }
+    if (ph->p->N != h->m.N) { set_error("smc_estimate: property compiled for a model with another species count"); return SMC_E_ARG; }
     return guard([&] {
         Model& m = h->m;
         std::lock_guard<std::mutex> lk(m.mu);
@@ -668,16 +714,20 @@ int smc_estimate_ex(smc_model* h, const smc_property* ph, double confidence, dou
         const uint64_t limit = (uint64_t)wilson_sample_size(0.5, half_width, normal_quantile(confidence));
         const bool speculate = m.speculate;
         if (speculate && hooks().world == 1) {
-            const int rc = device_estimate(m, pk, seed, confidence, half_width, start, limit, out);
+            const int rc = device_estimate(m, *ph->p, pk, seed, confidence, half_width, start, limit, out);
             harvest_spec_events(m, pk);
             return rc;
         }
+        if (speculate) global_capacity(m, pk);
+        const uint64_t world = (uint64_t)hooks().world;
         int rc = wilson_loop(
             [&](uint64_t base, uint64_t n, smc_counts* c) {
-                if (speculate) {
+                const bool covered = m.dev->spec_valid && base >= m.dev->spec_begin && base + n <= m.dev->spec_end;
+                if (speculate && (covered || n <= m.dev->spec_max * world)) {
                     spec_round(m, pk, seed, base, n, limit, c);
                     return (int)SMC_OK;
                 }
+                harvest_spec_events(m, pk);
                 return run_round(m, *ph->p, seed, base, n, c);
             },
             confidence, half_width, start, out);
@@ -723,6 +773,7 @@ int smc_estimate_with_runner(smc_run_fn run, void* user, double confidence, doub
 int smc_run_verdicts(smc_model* h, const smc_property* ph, uint64_t first, uint64_t n, uint64_t seed,
                      uint8_t* dev_verdict, int32_t* dev_events) {
     if (!h || !ph || !dev_verdict || !dev_events) { set_error("smc_run_verdicts: NULL argument"); return SMC_E_ARG; }
+    if (ph->p->N != h->m.N) { set_error("smc_run_verdicts: property compiled for a model with another species count"); return SMC_E_ARG; }
     return guard([&] {
         Model& m = h->m;
         std::lock_guard<std::mutex> lk(m.mu);
@@ -785,6 +836,7 @@ int smc_last_launch(const smc_model* h, const smc_property* ph, smc_launch_info*
 
 int smc_kernel_source(smc_model* h, const smc_property* ph, char* buf, size_t* len) {
     if (!h || !ph || !len) { set_error("smc_kernel_source: NULL"); return SMC_E_ARG; }
+    if (ph->p->N != h->m.N) { set_error("smc_kernel_source: property compiled for a model with another species count"); return SMC_E_ARG; }
     return guard([&] {
         Model& m = h->m;
         std::lock_guard<std::mutex> lk(m.mu);

@@ -16,3 +16,14 @@ def pytest_configure(config):
 @pytest.fixture(scope="session")
 def repo_root():
     return ROOT
+
+
+@pytest.fixture(scope="module")
+def smc():
+    """The C-ABI library with torch's allocator and stream (GPU tests only)."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("gpu test without a GPU")
+    import paper_0912_2551_b200 as smc
+    smc.use_torch()
+    return smc

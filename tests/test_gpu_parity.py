@@ -16,16 +16,6 @@ pytestmark = pytest.mark.gpu
 AGREE = 0.9999     # per-replica verdict agreement (log rounding may differ, north star)
 
 
-@pytest.fixture(scope="module")
-def smc():
-    import torch
-    if not torch.cuda.is_available():
-        pytest.fail("gpu test without a GPU")
-    import paper_0912_2551_b200 as smc
-    smc.use_torch()
-    return smc
-
-
 def _pair(smc, cfg, variant=0):
     m = smc.Model.from_config(cfg)
     if variant:

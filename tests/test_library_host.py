@@ -207,3 +207,21 @@ def test_sweep_configuration_choices():
     c5 = workloads.c5()
     m5 = smc.Model.from_config(c5)
     assert "smc_ssa_tile" in m5.kernel_source(smc.Property(m5, c5["formula"]))
+
+
+def test_property_of_another_model_and_event_cap_bounds():
+    """a property compiled for a model with another species count is rejected by
+    every run entry point before any device work; event caps stay within int32 (per-replica
+    event counts are int32 on the device)."""
+    m1 = smc.Model.from_config(workloads.c1())
+    m2 = smc.Model.from_config(workloads.c2())
+    p2 = smc.Property(m2, "F[0,50](P > 500)")
+    with pytest.raises(smc.SmcError):
+        m1.run(p2, 10, 1)
+    with pytest.raises(smc.SmcError):
+        smc.estimate(m1, p2, 0.99, 0.01, 1)
+    with pytest.raises(smc.SmcError):
+        m1.kernel_source(p2)
+    with pytest.raises(smc.SmcError):
+        m1.set_event_cap(2 ** 31)
+    m1.set_event_cap(2 ** 31 - 1)
