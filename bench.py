@@ -119,17 +119,20 @@ def model_stats(cfg):
     return [len(d) for d in deps], [len(c) for c in changes], sum(hill) / M
 
 
+# the committed ncu --set full summary the roofline's `traffic` comes from (named explicitly:
+# a stray capture in profiles/ must not change the bench line)
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "traffic_r01f8.json")
+
+
 def measured_profile(workload, kernel):
-    """The committed ncu --set full summary of the SSA kernel (profiles/traffic_<round>.json,
+    """The committed ncu --set full summary of the SSA kernel (TRAFFIC_FILE, written by
     scripts/ncu_traffic.py): DRAM bytes per launch, issue and shared-memory pipe utilisation."""
-    import glob
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "traffic_r*.json")))
-    if not files:
+    if not os.path.exists(TRAFFIC_FILE):
         return None, None
-    d = json.load(open(files[-1])).get(workload)
+    d = json.load(open(TRAFFIC_FILE)).get(workload)
     if not d or d.get("kernel") != kernel:
         return None, None
-    return d, "%s: %s (%s)" % (os.path.basename(files[-1]), d["capture"], d["note"])
+    return d, "%s: %s (%s)" % (os.path.basename(TRAFFIC_FILE), d["capture"], d["note"])
 
 
 # ------------------------------------------------------------------- clocks
@@ -386,7 +389,7 @@ def main():
     per_gpu_events = events / world
     achieved = sim_events * ipe / 32.0 / (tot_kernel_ms / 1e3) / 1e9
     achieved_counted = per_gpu_events * ipe / 32.0 / (tot_kernel_ms / 1e3) / 1e9
-    kname = "smc_ssa_" + {1: "thread", 2: "tile", 3: "literal", 4: "sweep"}[info["variant"]]
+    kname = "smc_ssa_" + {1: "thread", 2: "tile", 3: "literal", 4: "sweep", 5: "delta"}[info["variant"]]
     prof, traffic_src = measured_profile(cfg["name"], kname)
     traffic = prof["dram_bytes_per_launch"] if prof else None
     roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Gwarp-inst/s", "frac": achieved / peak,

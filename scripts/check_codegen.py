@@ -46,9 +46,12 @@ def main(names):
     for name in names:
         cfg = workloads.get(name)
         small = len(cfg["species"]) <= 32 and len(cfg["reactions"]) <= 32
-        for variant in ([1, 2, 4] if small else [2, 4]):
+        for variant in ([1, 2, 4] if small else [2, 4, 5]):
             m = smc.Model.from_config(cfg)
-            m.set_variant(variant)
+            try:
+                m.set_variant(variant)
+            except smc.SmcError:
+                continue
             p = smc.Property(m, cfg["formula"], t_max=cfg.get("t_max", 0.0))
             src = m.kernel_source(p)
             path = os.path.join(out, "%s_v%d.cu" % (name, variant))
