@@ -6,7 +6,9 @@
 // Variant 2 (tile): sizes and table offsets become constants; the tables
 // themselves are packed here (pack_tables) and staged to smem by TMA.
 // Both variants get the same generated monitor (reading R16 templates).
+#include <algorithm>
 #include <cmath>
+#include <map>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -868,6 +870,204 @@ int tile_width(const Model& m) {
     return m.M <= 256 ? 8 : (m.M <= 512 ? 16 : 32);
 }
 
+// Law kind of reaction j (ssa_tile.cuh smc_law_tab, ssa_delta.cuh smc_dh): h = x[s0] * x[s1]
+// with x[N] = 1 for kinds 0 (h = 1), 1 (x), 3 (x y); kind 2 (x(x-1)/2) as x * (x-1) with
+// c/2 (exact: halving); 4 general order 3-4 (int64); 5 explicit rate.  c = the table's rate.
+void law_kind(const Model& m, int j, uint32_t& kind, uint32_t& s0, uint32_t& s1, double& c) {
+    const Reaction& r = m.R[(size_t)j];
+    const int N = m.N;
+    s0 = s1 = (uint32_t)N;
+    c = r.c;
+    if (!r.rate.empty()) kind = 5;                  // explicit rate (generated smc_explicit)
+    else if (r.s[0] < 0) kind = 0;
+    else if (r.s[1] < 0 && r.st[0] == 1) { kind = 1; s0 = (uint32_t)r.s[0]; }
+    else if (r.s[1] < 0) {
+        kind = 2;
+        s0 = s1 = (uint32_t)r.s[0];
+        if ((c * 0.5) * 2.0 == c && c * 0.5 >= 0x1p-1021) c *= 0.5;   // fold the 1/2 (exact)
+        else { kind = 4; s1 = (uint32_t)N; }                       // subnormal rate: int64 path, x[N] = 1
+    } else { kind = (r.st[0] == 1 && r.st[1] == 1) ? 3u : 4u; s0 = (uint32_t)r.s[0]; s1 = (uint32_t)r.s[1]; }
+}
+
+// Variant 5 fixed point (reading R26): Cq_k = round(c_k 2^L) with c_k the table's rate.  The
+// group and total sums are sums of Cq_k h_k, h_k < 2^62 (counts < 2^31), so with
+// Cq_max < 2^(66 - ceil(log2 M)) no sum reaches 2^128.  Eligible when every law is mass
+// action of order <= 2 (kinds 0-3, no Hill) and the smallest positive rate still gets
+// Cq >= 2^36 (relative rounding of a term <= 2^-37; C5: rates 1e-3..1 -> Cq >= 2^44).
+int delta_scale(const Model& m) {
+    double cmax = 0.0, cmin = 0.0;
+    for (int j = 0; j < m.M; ++j) {
+        const Reaction& r = m.R[(size_t)j];
+        uint32_t kind, s0, s1;
+        double c;
+        law_kind(m, j, kind, s0, s1, c);
+        if (kind > 3 || r.hill || !(c >= 0.0) || !std::isfinite(c)) return -1;
+        if (c > 0.0) {
+            cmax = std::max(cmax, c);
+            cmin = (cmin == 0.0) ? c : std::min(cmin, c);
+        }
+    }
+    if (cmax == 0.0) return 0;
+    int lm = 0;
+    while ((1 << lm) < m.M) ++lm;                       // ceil(log2 M)
+    const int top = std::min(63, 66 - lm);              // Cq < 2^63 (u64) and M Cq 2^62 < 2^128
+    const int L = top - 1 - (int)std::floor(std::log2(cmax));   // cmax 2^L < 2^top
+    if (L < -900 || L > 900) return -1;
+    if (std::ldexp(cmin, L) < 0x1p36) return -1;
+    return L;
+}
+
+// Variant 5 tables: x0, the law table {s0 | kind << 16, s1, c} (the tile format), the change
+// lists and dep(j) as a reaction-indexed CSR with 2-byte entries k.
+TileLayout pack_delta_tables(const Model& m) {
+    TileLayout L;
+    const int N = m.N, M = m.M;
+    L.dl = delta_scale(m);
+    if (L.dl < 0) fail(SMC_E_MODEL, "delta variant: model not eligible (reading R26)");
+    // tile width 8 (C5: 2.9e9 events/s vs 2.4e9 at 16, 1.6e9 at 32); widths below 8 are not
+    // supported (TW = 4 hung on random networks)
+    L.tw = 8;
+    if (const char* e = std::getenv("SMC_TILE_WIDTH")) {
+        const int w = std::atoi(e);
+        if (w == 8 || w == 16 || w == 32) L.tw = w;
+    }
+    // G groups of S laws, both multiples of TW, G ~ sqrt(M)
+    int G = (int)std::ceil(std::sqrt((double)M));
+    if (const char* e = std::getenv("SMC_DG")) G = std::max(1, std::atoi(e));
+    G = (G + L.tw - 1) / L.tw * L.tw;
+    int S = (M + G - 1) / G;
+    S = (S + L.tw - 1) / L.tw * L.tw;
+    L.dg = G;
+    L.ds = S;
+    L.n_pad = (N + 1 + 3) & ~3;
+    L.tile_bytes = align16((size_t)16 * G + 4 * (size_t)L.n_pad);
+    // dep(j) dealt into R_j rounds of <= TW lanes such that no two entries of one round touch
+    // the same group: the entries sorted by group (largest multiplicity first) are dealt
+    // round robin over R_j = max(ceil(|dep(j)| / TW), max multiplicity) rounds -- a group's
+    // <= R_j entries land in distinct rounds, each round gets <= ceil(|dep(j)| / R_j) <= TW
+    // entries -- so each lane updates its group with a plain read-modify-write (no atomics).
+    // Stored compactly, round after round; dep_off[j] = start | R_j << 24, and the entry
+    // count of round r of j at rcnt[j * DRMAX + r].
+    std::vector<std::vector<std::vector<int>>> rounds((size_t)M);
+    size_t nnz = 0;
+    L.drmax = 1;
+    for (int j = 0; j < M; ++j) {
+        const auto& d = m.dep[(size_t)j];
+        L.max_dep = std::max<int>(L.max_dep, (int)d.size());
+        if (d.empty()) continue;
+        std::map<int, std::vector<int>> byg;
+        for (int k : d) byg[k / S].push_back(k);
+        std::vector<std::vector<int>> grp;
+        size_t mult = 0;
+        for (auto& kv : byg) { grp.push_back(kv.second); mult = std::max(mult, kv.second.size()); }
+        std::stable_sort(grp.begin(), grp.end(), [](const std::vector<int>& a, const std::vector<int>& b) {
+            return a.size() > b.size();
+        });
+        const int R = std::max<int>((int)mult, ((int)d.size() + L.tw - 1) / L.tw);
+        auto& rj = rounds[(size_t)j];
+        rj.assign((size_t)R, {});
+        int i = 0;
+        for (auto& gl : grp)
+            for (int k : gl) rj[(size_t)(i++ % R)].push_back(k);
+        nnz += d.size();
+        L.drmax = std::max(L.drmax, R);
+    }
+    if (L.drmax > 255) fail(SMC_E_MODEL, "delta variant: more than 255 dependency rounds");
+    if (nnz >= (1u << 24)) fail(SMC_E_MODEL, "delta variant: dependency table too large");
+    // entries: u16 k | (d0 + 4) << 10 | (d1 + 4) << 13 when M <= 1024 and every net change is in
+    // [-4, 3] (C4, C5: [-2, 2]); else u32 k | (d0 + 8) << 16 | (d1 + 8) << 20
+    int dmin = 0, dmax = 0;
+    for (auto& r : m.R)
+        for (auto& ch : r.change) { dmin = std::min(dmin, ch.second); dmax = std::max(dmax, ch.second); }
+    if (dmin < -8 || dmax > 7) fail(SMC_E_MODEL, "delta variant: a net change beyond [-8, 7]");
+    L.dep16 = M <= 1024 && dmin >= -4 && dmax <= 3;
+    // round descriptor per j: start | R << 24 | (count_r - 1) in 4-bit fields from bit 28 (u64),
+    // while R <= 9 and every round holds <= 16 entries; else the rcnt table
+    L.fatdep = L.drmax <= 9 && L.tw <= 16;
+    size_t o = 0;
+    L.off_x0 = o; o = align16(o + 4 * (size_t)L.n_pad);
+    L.off_law = o; o = align16(o + 16 * (size_t)M);
+    L.off_hill_k = o; o = align16(o + 8 * (size_t)M);       // Cq_k = round(c_k 2^L), u64
+    L.off_chg = o; o = align16(o + 2 * 4 * (size_t)M);
+    L.off_dep_off = o; o = align16(o + (L.fatdep ? 8 : 4) * ((size_t)M + 1));   // round descriptors
+    L.off_hill_rep = o; o = align16(o + (L.fatdep ? 0 : (size_t)M * (size_t)L.drmax));   // rcnt[j][r] (u8)
+    L.off_dep = o; o = align16(o + (L.dep16 ? 2 : 4) * nnz);
+    L.bytes = o;
+    L.blob.assign(L.bytes, 0);
+    auto* x0 = (int32_t*)(L.blob.data() + L.off_x0);
+    for (int s = 0; s < N; ++s) x0[s] = m.x0[(size_t)s];
+    x0[N] = 1;
+    auto* chg = (uint16_t*)(L.blob.data() + L.off_chg);
+    for (int j = 0; j < M; ++j) {
+        const Reaction& r = m.R[(size_t)j];
+        uint32_t kind, s0, s1;
+        double c;
+        law_kind(m, j, kind, s0, s1, c);
+        const uint32_t w0 = s0 | (kind << 16), w1 = s1;
+        unsigned char* law = L.blob.data() + L.off_law + 16 * (size_t)j;
+        std::memcpy(law, &w0, 4);
+        std::memcpy(law + 4, &w1, 4);
+        std::memcpy(law + 8, &c, 8);
+        const uint64_t cq = (uint64_t)std::nearbyint(std::ldexp(c, L.dl));   // exact scaling, round to nearest even
+        std::memcpy(L.blob.data() + L.off_hill_k + 8 * (size_t)j, &cq, 8);
+        if (r.change.size() > 4) fail(SMC_E_MODEL, "internal: more than 4 changed species");
+        for (int q = 0; q < 4; ++q) {
+            uint16_t e = 0xFFFF;
+            if (q < (int)r.change.size()) e = (uint16_t)((r.change[(size_t)q].first << 4) | (r.change[(size_t)q].second + 8));
+            chg[4 * j + q] = e;
+        }
+    }
+    // entry: k and the net changes d0, d1 that R_j applies to law k's operand species s0, s1
+    // (0 for an unchanged operand; ssa_delta.cuh smc_ddh)
+    auto* doff32 = (uint32_t*)(L.blob.data() + L.off_dep_off);
+    auto* doff64 = (uint64_t*)(L.blob.data() + L.off_dep_off);
+    auto* rcnt = L.blob.data() + L.off_hill_rep;
+    auto* dep32 = (uint32_t*)(L.blob.data() + L.off_dep);
+    auto* dep16 = (uint16_t*)(L.blob.data() + L.off_dep);
+    size_t pos = 0;
+    for (int j = 0; j < M; ++j) {
+        const auto& ch = m.R[(size_t)j].change;
+        const auto& rj = rounds[(size_t)j];
+        if (L.fatdep) {
+            uint64_t d = (uint64_t)pos | ((uint64_t)rj.size() << 24);
+            for (size_t r = 0; r < rj.size(); ++r) d |= (uint64_t)(rj[r].size() - 1) << (28 + 4 * r);
+            doff64[j] = d;
+        } else {
+            doff32[j] = (uint32_t)pos | ((uint32_t)rj.size() << 24);
+            for (size_t r = 0; r < rj.size(); ++r) rcnt[(size_t)j * L.drmax + r] = (uint8_t)rj[r].size();
+        }
+        for (size_t r = 0; r < rj.size(); ++r) {
+            for (int k : rj[r]) {
+                uint32_t kind, s0, s1;
+                double c;
+                law_kind(m, k, kind, s0, s1, c);
+                int d0 = 0, d1 = 0;
+                for (auto& cc : ch) {
+                    if ((uint32_t)cc.first == s0) d0 = cc.second;
+                    if ((uint32_t)cc.first == s1) d1 = cc.second;
+                }
+                if (L.dep16) dep16[pos++] = (uint16_t)((uint32_t)k | ((uint32_t)(d0 + 4) << 10) | ((uint32_t)(d1 + 4) << 13));
+                else dep32[pos++] = (uint32_t)k | ((uint32_t)(d0 + 8) << 16) | ((uint32_t)(d1 + 8) << 20);
+            }
+        }
+    }
+    if (L.fatdep) doff64[M] = pos; else doff32[M] = (uint32_t)pos;
+    // check: the rounds of dep(j) hold each k of dep(j) once, <= TW per round, no group twice
+    for (int j = 0; j < M; ++j) {
+        std::vector<int> seen;
+        for (auto& rr : rounds[(size_t)j]) {
+            std::vector<int> gr;
+            for (int k : rr) { seen.push_back(k); gr.push_back(k / S); }
+            std::sort(gr.begin(), gr.end());
+            if ((int)rr.size() > L.tw || std::adjacent_find(gr.begin(), gr.end()) != gr.end())
+                fail(SMC_E_MODEL, "internal: bad dependency round");
+        }
+        std::sort(seen.begin(), seen.end());
+        if (seen != m.dep[(size_t)j]) fail(SMC_E_MODEL, "internal: dep rounds do not cover dep(j)");
+    }
+    return L;
+}
+
 TileLayout pack_tables(const Model& m, bool sweep) {
     TileLayout L;
     const int N = m.N, M = m.M;
@@ -942,20 +1142,9 @@ TileLayout pack_tables(const Model& m, bool sweep) {
     std::vector<double> fat_c((size_t)M);
     for (int j = 0; j < M; ++j) {
         const Reaction& r = m.R[(size_t)j];
-        // law kind (ssa_tile.cuh smc_law_tab): h = x[s0] * x[s1] with x[N] = 1 for kinds
-        // 0 (h = 1), 1 (x), 3 (x y); kind 2 (x(x-1)/2) as x * (x-1) with c/2 (exact: halving);
-        // 4 general order 3-4 (int64); 5 explicit rate
-        uint32_t kind, s0 = (uint32_t)N, s1 = (uint32_t)N;
-        double c = r.c;
-        if (!r.rate.empty()) kind = 5;                  // explicit rate (generated smc_explicit)
-        else if (r.s[0] < 0) kind = 0;
-        else if (r.s[1] < 0 && r.st[0] == 1) { kind = 1; s0 = (uint32_t)r.s[0]; }
-        else if (r.s[1] < 0) {
-            kind = 2;
-            s0 = s1 = (uint32_t)r.s[0];
-            if ((c * 0.5) * 2.0 == c && c * 0.5 >= 0x1p-1021) c *= 0.5;   // fold the 1/2 (exact)
-            else { kind = 4; s1 = (uint32_t)N; }                       // subnormal rate: int64 path, x[N] = 1
-        } else { kind = (r.st[0] == 1 && r.st[1] == 1) ? 3u : 4u; s0 = (uint32_t)r.s[0]; s1 = (uint32_t)r.s[1]; }
+        uint32_t kind, s0, s1;
+        double c;
+        law_kind(m, j, kind, s0, s1, c);
         uint32_t w0 = s0 | (kind << 16) | ((uint32_t)(r.s[0] >= 0 ? r.st[0] : 1) << 20);
         uint32_t w1 = s1 | ((uint32_t)(r.s[1] >= 0 ? r.st[1] : 1) << 16);
 
@@ -1109,6 +1298,21 @@ std::string generate_source(const Model& m, const Property& p, int variant, cons
         o << "#define SMC_ANY_HILL " << (tl->any_hill ? 1 : 0) << "\n";
         o << "#define SMC_ANY_GENERAL " << (tl->any_general ? 1 : 0) << "\n";
         o << "#define SMC_ANY_EXPLICIT " << (tl->any_explicit ? 1 : 0) << "\n";
+    } else if (variant == 5) {
+        // upper bound of the CTA (register cap 65536 / blk: TW 32 64, 16 73, 8 102, <= 4 128)
+        int blk = tl->tw >= 32 ? 1024 : (tl->tw == 16 ? 896 : (tl->tw == 8 ? 832 : 512));
+        if (const char* e = std::getenv("SMC_DBLOCK")) blk = std::max(32, std::atoi(e) / 32 * 32);
+        o << "#define SMC_TW " << tl->tw << "\n#define SMC_DG " << tl->dg << "\n#define SMC_DS " << tl->ds
+          << "\n#define SMC_DBLOCK " << blk << "\n";
+        if (const char* e = std::getenv("SMC_DCHECK")) o << "#define SMC_DCHECK " << std::atoi(e) << "\n";
+        o << "#define SMC_DSCALE " << dlit(std::ldexp(1.0, tl->dl)) << "\n#define SMC_DINV " << dlit(std::ldexp(1.0, -tl->dl))
+          << "\n#define SMC_DHI " << dlit(std::ldexp(1.0, 64 - tl->dl)) << "\n";
+        o << "#define SMC_OFF_X0 " << tl->off_x0 << "\n#define SMC_OFF_LAW " << tl->off_law << "\n#define SMC_OFF_CQ "
+          << tl->off_hill_k << "\n#define SMC_OFF_CHG " << tl->off_chg << "\n#define SMC_OFF_DOFF " << tl->off_dep_off
+          << "\n#define SMC_OFF_DEP " << tl->off_dep << "\n#define SMC_OFF_RCNT " << tl->off_hill_rep
+          << "\n#define SMC_DRMAX " << tl->drmax << "\n#define SMC_DDEP16 " << (tl->dep16 ? 1 : 0)
+          << "\n#define SMC_DDESC64 " << (tl->fatdep ? 1 : 0) << "\n";
+        o << "#define SMC_TAB_BYTES " << tl->bytes << "\n#define SMC_TILE_BYTES " << tl->tile_bytes << "\n";
     } else {
         if (p.literal) {
             const double H = p.t_max > 0.0 ? p.t_max : p.horizon;
@@ -1163,7 +1367,9 @@ std::string generate_source(const Model& m, const Property& p, int variant, cons
         if (const char* e = std::getenv("SMC_MON_XD")) xd = xd && std::atoi(e) != 0;
         o << MonGen(p, xd).emit() << "\n";
     }
-    o << embedded_source(variant == 1 ? "ssa_thread.cuh" : (variant == 4 ? "ssa_sweep.cuh" : "ssa_tile.cuh")) << "\n";
+    o << embedded_source(variant == 1 ? "ssa_thread.cuh"
+                                      : (variant == 4 ? "ssa_sweep.cuh" : (variant == 5 ? "ssa_delta.cuh" : "ssa_tile.cuh")))
+      << "\n";
     return o.str();
 }
 

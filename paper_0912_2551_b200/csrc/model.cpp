@@ -49,6 +49,10 @@ void Model::build_deps() {
 // variant 4 (sweep) holds the counts of 128 trajectories per CTA in shared memory
 bool Model::sweep_fits() const { return N <= 4095 && 128 * 4 * (size_t)(N + 1) + 24 * (size_t)M + 4096 <= 200 * 1024; }
 
+// variant 5 (exact fixed-point group sums, dependency deltas): mass action of order <= 2
+// only, rates within the fixed-point range (delta_scale), 16-bit reaction indices
+bool Model::delta_fits() const { return M <= 65535 && N <= 65534 && delta_scale(*this) >= 0; }
+
 int Model::variant() const {
     if (variant_forced) return variant_forced;
     if (N <= 32 && M <= 32) return 1;
@@ -59,7 +63,12 @@ int Model::variant() const {
     // automatic choice off / on
     bool sweep = N <= 160 && M <= 1024;
     if (const char* e = std::getenv("SMC_SWEEP")) sweep = std::atoi(e) != 0;
-    return (sweep && sweep_fits()) ? 4 : 2;
+    if (sweep && sweep_fits()) return 4;
+    // larger mass-action networks (C5): the delta kernel (no stored propensities);
+    // SMC_DELTA=0 keeps the tile kernel
+    bool delta = true;
+    if (const char* e = std::getenv("SMC_DELTA")) delta = std::atoi(e) != 0;
+    return (delta && delta_fits()) ? 5 : 2;
 }
 
 }  // namespace smc
@@ -176,11 +185,16 @@ int smc_model_set_rate_expr(smc_model* h, int32_t reaction, const char* expr, co
 }
 
 int smc_model_set_variant(smc_model* h, int32_t variant) {
-    if (!h || variant < 0 || variant > 4 || variant == 3) {
-        set_error("smc_model_set_variant: variant 0 (automatic), 1, 2 or 4");
+    if (!h || variant < 0 || variant > 5 || variant == 3) {
+        set_error("smc_model_set_variant: variant 0 (automatic), 1, 2, 4 or 5");
         return SMC_E_ARG;
     }
     Model& m = h->m;
+    if (variant == 5 && !m.delta_fits()) {
+        set_error("smc_model_set_variant: delta variant needs mass action of order <= 2 with rates within 2^20 of "
+                  "each other (fixed-point group sums, reading R26)");
+        return SMC_E_ARG;
+    }
     if (variant == 4 && !m.sweep_fits()) {
         set_error("smc_model_set_variant: sweep variant needs the counts of 128 trajectories in shared memory");
         return SMC_E_ARG;

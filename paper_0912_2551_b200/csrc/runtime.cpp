@@ -109,16 +109,17 @@ struct PropKernel {
     smc_launch_info info{};
     uint64_t cap_global = 0;               // sum of capacity() over the ranks (one allreduce)
     uint64_t capacity() const {            // trajectories resident at once on this GPU
-        return (uint64_t)grid_max * (uint64_t)(variant != 2 ? block : (block / 32) * per_warp);
+        return (uint64_t)grid_max * (uint64_t)((variant != 2 && variant != 5) ? block : (block / 32) * per_warp);
     }
 };
 
 struct DeviceState {
-    void* tables[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};   // per variant: [1] Hill, [2] tile, [4] sweep
-    size_t table_bytes[5] = {0, 0, 0, 0, 0};
-    bool tables_ready[5] = {false, false, false, false, false};
+    void* tables[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};   // per variant: [1] Hill, [2] tile, [4] sweep, [5] delta
+    size_t table_bytes[6] = {0, 0, 0, 0, 0, 0};
+    bool tables_ready[6] = {false, false, false, false, false, false};
     TileLayout layout;              // variant 2
     TileLayout sw_layout;           // variant 4
+    TileLayout d_layout;            // variant 5
     void* ctl = nullptr;            // [0..8) cursor, [16..48) counters, [64..72) spec cursor, [80..112) spec scratch
     int64_t* host_counts = nullptr; // pinned
     // speculative batch of smc_estimate (prefix-exact rounds): this rank's slice [lo, hi)
@@ -221,7 +222,7 @@ PropKernel& prepare(Model& m, const Property& p) {
     // buffered trace + literal |= (reading R23): thread-owned models run variant 3, tile
     // models the tile kernel with the recording monitor
     if (p.literal && pk.variant == 1) pk.variant = 3;
-    if (p.literal && pk.variant == 4) pk.variant = 2;    // the recording monitor lives in the tile kernel
+    if (p.literal && (pk.variant == 4 || pk.variant == 5)) pk.variant = 2;   // the recording monitor lives in the tile kernel
     const TileLayout* tl = nullptr;
     const int v = pk.variant == 3 ? 1 : pk.variant;      // table set (variant 3 uses variant 1's)
     if (!d.tables_ready[v]) {
@@ -236,6 +237,10 @@ PropKernel& prepare(Model& m, const Property& p) {
             d.sw_layout = pack_tables(m, true);
             src = d.sw_layout.blob.data();
             bytes = d.sw_layout.bytes;
+        } else if (v == 5) {
+            d.d_layout = pack_delta_tables(m);
+            src = d.d_layout.blob.data();
+            bytes = d.d_layout.bytes;
         } else {
             ht = pack_hill_tables(m);
             src = ht.values.data();
@@ -251,10 +256,13 @@ PropKernel& prepare(Model& m, const Property& p) {
     }
     if (v == 2) tl = &d.layout;
     if (v == 4) tl = &d.sw_layout;
+    if (v == 5) tl = &d.d_layout;
     pk.tables = d.tables[v];
     pk.source = generate_source(m, p, pk.variant, tl);
     pk.k = get_kernel(pk.source, pk.variant == 1 ? "smc_ssa_thread"
-                                 : (pk.variant == 2 ? "smc_ssa_tile" : (pk.variant == 4 ? "smc_ssa_sweep" : "smc_ssa_literal")));
+                                 : (pk.variant == 2 ? "smc_ssa_tile"
+                                                    : (pk.variant == 4 ? "smc_ssa_sweep"
+                                                                       : (pk.variant == 5 ? "smc_ssa_delta" : "smc_ssa_literal"))));
     const void* fn = (const void*)pk.k->kernel;
     if (pk.variant == 3) {
         pk.block = 128;
@@ -274,6 +282,25 @@ PropKernel& prepare(Model& m, const Property& p) {
         int nb = 0;
         ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, pk.block, (size_t)pk.smem), "occupancy");
         if (nb < 1) fail(SMC_E_CUDA, "sweep kernel: no resident CTA");
+        pk.grid_max = nb * d.sm_count;
+    } else if (pk.variant == 5) {
+        // CTAs of SMC_DBLOCK threads (the compiled size); resident CTAs per SM from the
+        // occupancy API under the shared-memory budget (tables + one slice per tile)
+        // one CTA per SM: as many warps as the registers (the compiled bound) and the shared
+        // memory (one copy of the tables + TPW slices per warp) allow
+        cudaFuncAttributes fa;
+        ck(cudaFuncGetAttributes(&fa, fn), "cudaFuncGetAttributes");
+        pk.per_warp = 32 / tl->tw;
+        const size_t wb = (size_t)pk.per_warp * tl->tile_bytes;
+        const size_t avail = (size_t)d.max_smem_optin - fa.sharedSizeBytes;
+        if (tl->bytes + wb > avail) fail(SMC_E_CUDA, "delta kernel: tables and one warp's slices do not fit in shared memory");
+        const int W = (int)std::min<size_t>((size_t)fa.maxThreadsPerBlock / 32, (avail - tl->bytes) / wb);
+        pk.block = W * 32;
+        pk.smem = (int)(tl->bytes + (size_t)W * wb);
+        ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, pk.smem), "smem attr");
+        int nb = 0;
+        ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, pk.block, (size_t)pk.smem), "occupancy");
+        if (nb < 1) fail(SMC_E_CUDA, "delta kernel: no resident CTA");
         pk.grid_max = nb * d.sm_count;
     } else if (pk.variant == 1) {
         pk.block = thread_block(m);
@@ -347,7 +374,8 @@ void launch_slice(Model& m, PropKernel& pk, uint64_t seed, uint64_t lo, uint64_t
         const uint64_t per_sm = (count + (uint64_t)d.sm_count - 1) / (uint64_t)d.sm_count;
         block = (int)std::min<uint64_t>((uint64_t)pk.block, std::max<uint64_t>(32, (per_sm + 31) / 32 * 32));
     }
-    const uint64_t per_block = pk.variant != 2 ? (uint64_t)block : (uint64_t)(pk.block / 32 * pk.per_warp);
+    const uint64_t per_block = (pk.variant != 2 && pk.variant != 5) ? (uint64_t)block
+                                                                    : (uint64_t)(pk.block / 32 * pk.per_warp);
     const uint64_t need = (count + per_block - 1) / per_block;
     const int grid = (int)std::min<uint64_t>((uint64_t)pk.grid_max, need);
     void* args[] = {&P};
@@ -844,9 +872,10 @@ int smc_kernel_source(smc_model* h, const smc_property* ph, char* buf, size_t* l
         const int mv = m.variant();
         const int v = (ph->p->literal && mv == 1) ? 3 : mv;
         TileLayout tl;
-        const int vv = (ph->p->literal && v == 4) ? 2 : v;
+        const int vv = (ph->p->literal && (v == 4 || v == 5)) ? 2 : v;
         if (vv == 2 || vv == 4) tl = pack_tables(m, vv == 4);
-        std::string s = generate_source(m, *ph->p, vv, (vv == 2 || vv == 4) ? &tl : nullptr);
+        if (vv == 5) tl = pack_delta_tables(m);
+        std::string s = generate_source(m, *ph->p, vv, (vv == 2 || vv == 4 || vv == 5) ? &tl : nullptr);
         size_t need = s.size() + 1;
         if (buf) std::memcpy(buf, s.c_str(), std::min(*len, need));
         *len = need;

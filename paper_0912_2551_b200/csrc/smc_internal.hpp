@@ -66,8 +66,9 @@ struct Model {
     std::mutex mu;
     void build_deps();
     std::vector<int> law_species(int k) const;   // species read by a_k
-    int variant() const;                          // 1 thread-owned, 2 tile, 4 sweep
+    int variant() const;                          // 1 thread-owned, 2 tile, 4 sweep, 5 delta
     bool sweep_fits() const;
+    bool delta_fits() const;                      // variant 5 can hold the model
 };
 
 // -------------------------------------------------------------- property ---
@@ -164,9 +165,13 @@ struct TileLayout {               // packed model tables (variant 2), byte offse
     bool sw_xd = false;           // counts as binary64 columns
     int sw_blk = 128;             // CTA size = stride of the count columns
     int max_dep = 0;
+    // variant 5 (delta): G exact fixed-point group sums of S laws, Cq = round(c 2^L)
+    int dg = 0, ds = 0, drmax = 0, dl = 0;
     std::vector<uint8_t> blob;    // host copy
 };
 TileLayout pack_tables(const Model& m, bool sweep = false);   // sweep: law/change tables only (variant 4)
+TileLayout pack_delta_tables(const Model& m);                 // variant 5
+int delta_scale(const Model& m);  // L of variant 5, or -1 if the model is not eligible
 int thread_minb(const Model& m);    // resident 128-thread units per SM of variant 1 (codegen.cpp)
 int thread_block(const Model& m);   // CTA size of variant 1
 // variant 1: zero-order Hill propensities a_k(x_r), x_r < size, tabulated on the host with

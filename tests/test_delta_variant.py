@@ -28,7 +28,7 @@ def _fixture(name):
     return json.load(open(os.path.join(GOLDEN, "%s_oracle.json" % name.lower())))
 
 
-@pytest.mark.parametrize("width", ["4", "8", "16", "32"])
+@pytest.mark.parametrize("width", ["8", "16", "32"])
 @pytest.mark.parametrize("name", ["C4", "C5"])
 def test_fixture_every_tile_width(smc, name, width, monkeypatch):
     monkeypatch.setenv("SMC_TILE_WIDTH", width)
@@ -98,7 +98,7 @@ def test_random_mass_action_networks(smc, seed):
                t_max=0.0, seed=seed, sampling=dict(mode="fixed", n=300))
     oc, ov, oe = O.run(O.OracleModel(cfg), O.OracleFormula(cfg["formula"], cfg["species"]), seed, 0, 300)
     os_env = os.environ
-    os_env["SMC_TILE_WIDTH"] = ["4", "8", "16", "32"][seed % 4]
+    os_env["SMC_TILE_WIDTH"] = ["8", "16", "32"][seed % 3]
     try:
         m, p = _pair(smc, cfg)
         v, e = m.run_verdicts(p, 0, 300, seed)
