@@ -981,13 +981,13 @@ TileLayout pack_delta_tables(const Model& m) {
         for (auto& ch : r.change) { dmin = std::min(dmin, ch.second); dmax = std::max(dmax, ch.second); }
     if (dmin < -8 || dmax > 7) fail(SMC_E_MODEL, "delta variant: a net change beyond [-8, 7]");
     L.dep16 = M <= 1024 && dmin >= -4 && dmax <= 3;
-    // round descriptor per j: start | R << 24 | (count_r - 1) in 4-bit fields from bit 28 (u64),
-    // while R <= 9 and every round holds <= 16 entries; else the rcnt table
-    L.fatdep = L.drmax <= 9 && L.tw <= 16;
+    // round descriptor per j (u64): low word start | R << 24, high word (count_r - 1) in 4-bit
+    // fields, while R <= 8 and every round holds <= 16 entries; else the rcnt table
+    L.fatdep = L.drmax <= 8 && L.tw <= 16;
     size_t o = 0;
     L.off_x0 = o; o = align16(o + 4 * (size_t)L.n_pad);
-    L.off_law = o; o = align16(o + 16 * (size_t)M);
-    L.off_hill_k = o; o = align16(o + 8 * (size_t)M);       // Cq_k = round(c_k 2^L), u64
+    L.off_law = o; o = align16(o + 16 * (size_t)G * (size_t)S);   // in-group laws, permuted within groups
+    L.off_hill_k = o; o = align16(o + 16 * (size_t)M);      // dependency law {s0 | s1 << 16, kind, Cq_k}
     L.off_chg = o; o = align16(o + 2 * 4 * (size_t)M);
     L.off_dep_off = o; o = align16(o + (L.fatdep ? 8 : 4) * ((size_t)M + 1));   // round descriptors
     L.off_hill_rep = o; o = align16(o + (L.fatdep ? 0 : (size_t)M * (size_t)L.drmax));   // rcnt[j][r] (u8)
@@ -998,18 +998,35 @@ TileLayout pack_delta_tables(const Model& m) {
     for (int s = 0; s < N; ++s) x0[s] = m.x0[(size_t)s];
     x0[N] = 1;
     auto* chg = (uint16_t*)(L.blob.data() + L.off_chg);
+    for (int p = M; p < G * S; ++p) {               // padding members: rate 0, x[N] * x[N]
+        const int CHd = S / L.tw, gp = p / S, mp = p % S;
+        const uint32_t w0 = (uint32_t)N | (1u << 16), w1 = (uint32_t)N;
+        unsigned char* law = L.blob.data() + L.off_law + 16 * ((size_t)gp * S + (size_t)(mp % CHd) * L.tw + (size_t)(mp / CHd));
+        std::memcpy(law, &w0, 4);
+        std::memcpy(law + 4, &w1, 4);
+    }
     for (int j = 0; j < M; ++j) {
         const Reaction& r = m.R[(size_t)j];
         uint32_t kind, s0, s1;
         double c;
         law_kind(m, j, kind, s0, s1, c);
+        // in-group law table: member m of group g (lane m / CH, chunk slot m % CH) stored at
+        // g S + (m % CH) TW + m / CH, so the TW lanes reading chunk slot c hit consecutive
+        // 16-byte entries (conflict-free); padding up to G S: rate 0, operands x[N] = 1
         const uint32_t w0 = s0 | (kind << 16), w1 = s1;
-        unsigned char* law = L.blob.data() + L.off_law + 16 * (size_t)j;
+        const int CHd = S / L.tw, gj = j / S, mj = j % S;
+        unsigned char* law = L.blob.data() + L.off_law + 16 * ((size_t)gj * S + (size_t)(mj % CHd) * L.tw + (size_t)(mj / CHd));
         std::memcpy(law, &w0, 4);
         std::memcpy(law + 4, &w1, 4);
         std::memcpy(law + 8, &c, 8);
-        const uint64_t cq = (uint64_t)std::nearbyint(std::ldexp(c, L.dl));   // exact scaling, round to nearest even
-        std::memcpy(L.blob.data() + L.off_hill_k + 8 * (size_t)j, &cq, 8);
+        // the dependency pass's law entry: operands, kind, Cq_k = round(c_k 2^L) (exact scaling,
+        // round to nearest even)
+        const uint64_t cq = (uint64_t)std::nearbyint(std::ldexp(c, L.dl));
+        const uint32_t ops = s0 | (s1 << 16);
+        unsigned char* dl = L.blob.data() + L.off_hill_k + 16 * (size_t)j;
+        std::memcpy(dl, &ops, 4);
+        std::memcpy(dl + 4, &kind, 4);
+        std::memcpy(dl + 8, &cq, 8);
         if (r.change.size() > 4) fail(SMC_E_MODEL, "internal: more than 4 changed species");
         for (int q = 0; q < 4; ++q) {
             uint16_t e = 0xFFFF;
@@ -1030,7 +1047,7 @@ TileLayout pack_delta_tables(const Model& m) {
         const auto& rj = rounds[(size_t)j];
         if (L.fatdep) {
             uint64_t d = (uint64_t)pos | ((uint64_t)rj.size() << 24);
-            for (size_t r = 0; r < rj.size(); ++r) d |= (uint64_t)(rj[r].size() - 1) << (28 + 4 * r);
+            for (size_t r = 0; r < rj.size(); ++r) d |= (uint64_t)(rj[r].size() - 1) << (32 + 4 * r);
             doff64[j] = d;
         } else {
             doff32[j] = (uint32_t)pos | ((uint32_t)rj.size() << 24);

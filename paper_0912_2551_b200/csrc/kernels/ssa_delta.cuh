@@ -40,11 +40,17 @@
 //   SMC_DSCALE (2^L), SMC_DINV (2^-L), SMC_DHI (2^(64-L)), SMC_OFF_X0/LAW/CQ/CHG/DOFF/DEP,
 //   SMC_TAB_BYTES, SMC_TILE_BYTES, SMC_DBLOCK, SMC_TMAX, SmcMon.
 
+struct __align__(16) SmcDLaw {       // the dependency pass's law entry
+    unsigned ops;                     // s0 | s1 << 16 (x[N] = 1 for a missing operand)
+    unsigned kind;                    // 0..3 (2: homodimer x (x - 1))
+    smc_u64 cq;                       // Cq_k = round(c_k 2^L)
+};
+
 struct SmcDTabs {
     const int* x0;
     const SmcLaw* law;               // {s0 | kind << 16, s1, c} (kind 0..3, c folded for kind 2)
     const unsigned short* chg;       // [M][4]: species << 4 | (delta + 8), 0xFFFF = none
-    const smc_u64* cq;               // [M]: Cq_k = round(c_k 2^L)
+    const SmcDLaw* dlaw;             // [M]: operands, kind, Cq_k
 #if SMC_DDESC64
     const smc_u64* dep_off;          // [M+1]: start | rounds << 24 | (entries of round r - 1) << (28 + 4 r)
 #else
@@ -60,18 +66,23 @@ struct SmcDTabs {
 
 // exact integer h_k in the table's form: x0 * x1 (kinds 0, 1, 3 with x[N] = 1), x0 (x0 - 1)
 // (kind 2; 0 for x0 <= 1).  Counts < 2^31, so the product fits int64 exactly.
-__device__ __forceinline__ smc_i64 smc_dh(const SmcLaw& L, const int* xs) {
-    const int v0 = xs[L.u0 & 0xFFFFu];
-    const int v1 = (((L.u0 >> 16) & 7u) == 2u) ? v0 - 1 : xs[L.u1 & 0xFFFFu];
+__device__ __forceinline__ smc_i64 smc_dh(const SmcDLaw& L, const int* xs) {
+    const int v0 = xs[L.ops & 0xFFFFu];
+    const int v1 = (L.kind == 2u) ? v0 - 1 : xs[L.ops >> 16];
     return (smc_i64)v0 * v1;
 }
 // a_k = c_k * h_k in binary64: h = fl(x0 * x1) (a single rounding of the exact integer
 // product), the same operations as variants 1, 2 and 4 -- equal to the oracle's
 // c_k * (double)h_k bit for bit (reading R20)
 __device__ __forceinline__ double smc_dlaw(const SmcLaw& L, const int* xs) {
+    // (double)(x0 * xb) of the exact int64 product: the same single rounding as fl(x0 * xb)
+    // (the second operand is read only for x0 x1: kind 1 has x[N] = 1 -- fewer shared loads)
+    const unsigned kind = (L.u0 >> 16) & 7u;
     const int v0 = xs[L.u0 & 0xFFFFu];
-    const int xb = (((L.u0 >> 16) & 7u) == 2u) ? max(v0 - 1, 0) : xs[L.u1 & 0xFFFFu];
-    return __dmul_rn(L.c, __dmul_rn((double)v0, (double)xb));
+    int xb = 1;
+    if (kind == 3u) xb = xs[L.u1 & 0xFFFFu];
+    else if (kind == 2u) xb = max(v0 - 1, 0);
+    return __dmul_rn(L.c, __ll2double_rn((smc_i64)v0 * xb));
 }
 
 // group g -> 16-byte slot in the tile's slice
@@ -91,34 +102,25 @@ __device__ __forceinline__ double smc_g2d(ulonglong2 w) {
 //   x0 x1:       a x1 + b x0 - a b           (x_old = x_new - d; kind 1: x1 = x[N] = 1, b = 0)
 //   x0 (x0 - 1): a (2 x0 - a - 1)            (homodimer, s0 = s1)
 // exact in int64 (counts < 2^31, |d| <= 8)
-__device__ __forceinline__ smc_i64 smc_ddh(const SmcLaw& L, int a, int b, const int* xs) {
-    const int x0 = xs[L.u0 & 0xFFFFu];
-    if (((L.u0 >> 16) & 7u) == 2u) return (smc_i64)a * (2 * (smc_i64)x0 - a - 1);
-    const int x1 = xs[L.u1 & 0xFFFFu];
+__device__ __forceinline__ smc_i64 smc_ddh(const SmcDLaw& L, int a, int b, const int* xs) {
+    const int x0 = xs[L.ops & 0xFFFFu];
+    if (L.kind == 2u) return (smc_i64)a * (2 * (smc_i64)x0 - a - 1);
+    if (L.kind != 3u) return (smc_i64)a;          // x0 * x[N]: b = 0, x1 = 1
+    const int x1 = xs[L.ops >> 16];
     return (smc_i64)a * x1 + (smc_i64)b * x0 - (smc_i64)(a * b);
 }
 
-// Sg +/-= Cq |dh| (128-bit, carry / borrow into the high word), a plain read-modify-write:
-// the rounds of dep(j) are packed so that no two lanes of a round touch the same group
+// Sg += Cq dh, two's complement 128-bit: low word = Cq dh mod 2^64, high word = the unsigned
+// high product minus Cq when dh < 0 (signed correction), plus the carry of the low word.  A
+// plain read-modify-write: the rounds of dep(j) are packed so that no two lanes of a round
+// touch the same group.
 __device__ __forceinline__ void smc_gadd(ulonglong2* w, smc_u64 cq, smc_i64 dh) {
-    const smc_u64 m = (smc_u64)(dh < 0 ? -dh : dh);
-    smc_u64 lo, hi;
-    if ((m >> 32) == 0ull) {                          // |dh| < 2^32: two 32 x 32 -> 64 products
-        const smc_u64 p0 = (smc_u64)(smc_u32)cq * m, p1 = (cq >> 32) * m;
-        lo = p0 + (p1 << 32);
-        hi = (p1 >> 32) + (lo < p0 ? 1ull : 0ull);
-    } else {
-        lo = cq * m;
-        hi = __umul64hi(cq, m);
-    }
+    const smc_u64 d = (smc_u64)dh;
+    const smc_u64 lo = cq * d;
+    const smc_u64 hi = __umul64hi(cq, d) - (dh < 0 ? cq : 0ull);
     ulonglong2 v = *w;
-    if (dh > 0) {
-        v.x += lo;
-        v.y += hi + (v.x < lo ? 1ull : 0ull);
-    } else {
-        v.y -= hi + (v.x < lo ? 1ull : 0ull);
-        v.x -= lo;
-    }
+    v.x += lo;
+    v.y += hi + (v.x < lo ? 1ull : 0ull);
     *w = v;
 }
 
@@ -151,7 +153,7 @@ extern "C" __global__ void __launch_bounds__(SMC_DBLOCK, 1) smc_ssa_delta(SmcPar
 #else
     T.dep_off = (const unsigned*)(smem + SMC_OFF_DOFF);
 #endif
-    T.cq = (const smc_u64*)(smem + SMC_OFF_CQ);
+    T.dlaw = (const SmcDLaw*)(smem + SMC_OFF_CQ);
     T.rcnt = (const unsigned char*)(smem + SMC_OFF_RCNT);
 #if SMC_DDEP16
     T.dep = (const unsigned short*)(smem + SMC_OFF_DEP);
@@ -201,8 +203,8 @@ extern "C" __global__ void __launch_bounds__(SMC_DBLOCK, 1) smc_ssa_delta(SmcPar
                     for (int m = 0; m < S; ++m) {
                         const int kk = g * S + m;
                         if (kk < SMC_M) {
-                            const SmcLaw L = T.law[kk];
-                            const smc_u64 h = (smc_u64)smc_dh(L, xs), cq = T.cq[kk];
+                            const SmcDLaw L = T.dlaw[kk];
+                            const smc_u64 h = (smc_u64)smc_dh(L, xs), cq = L.cq;
                             const smc_u64 plo = cq * h;
                             lo += plo;
                             hi += __umul64hi(cq, h) + (lo < plo ? 1ull : 0ull);
@@ -299,8 +301,7 @@ extern "C" __global__ void __launch_bounds__(SMC_DBLOCK, 1) smc_ssa_delta(SmcPar
             double cs = 0.0;
 #pragma unroll
             for (int c = 0; c < CH; ++c) {
-                const int kk = g * S + tl * CH + c;
-                av[c] = (kk < SMC_M) ? smc_dlaw(T.law[kk], xs) : 0.0;
+                av[c] = smc_dlaw(T.law[g * S + c * TW + tl], xs);   // member tl CH + c (permuted table)
                 cs = (c == 0) ? av[0] : __dadd_rn(cs, av[c]);
             }
             double ps = cs;
@@ -355,15 +356,16 @@ extern "C" __global__ void __launch_bounds__(SMC_DBLOCK, 1) smc_ssa_delta(SmcPar
             // counts and the changes R_j applied to law k's operands; one round at a time (the
             // <= TW entries of a round touch distinct groups: plain read-modify-writes)
 #if SMC_DDESC64
-            const int nr = (int)((desc >> 24) & 15ull);
+            const unsigned dlo = (unsigned)desc, dhi = (unsigned)(desc >> 32);
 #else
-            const int nr = (int)(desc >> 24);
+            const unsigned dlo = desc;
 #endif
-            unsigned at = (unsigned)desc & 0xFFFFFFu;
+            const int nr = (int)(dlo >> 24);
+            unsigned at = dlo & 0xFFFFFFu;
 #pragma unroll 1
             for (int r = 0; __any_sync(SMC_FULL, r < nr); ++r) {
 #if SMC_DDESC64
-                const int cnt = (r < nr) ? (int)((desc >> (28 + 4 * r)) & 15ull) + 1 : 0;
+                const int cnt = (r < nr) ? (int)((dhi >> (4 * r)) & 15u) + 1 : 0;
 #else
                 const int cnt = (r < nr) ? (int)T.rcnt[j * SMC_DRMAX + r] : 0;
 #endif
@@ -374,9 +376,8 @@ extern "C" __global__ void __launch_bounds__(SMC_DBLOCK, 1) smc_ssa_delta(SmcPar
 #else
                     const int kk = (int)(e & 0xFFFFu), a = (int)((e >> 16) & 15u) - 8, b = (int)((e >> 20) & 15u) - 8;
 #endif
-                    const SmcLaw L = T.law[kk];
-                    const smc_i64 dh = smc_ddh(L, a, b, xs);
-                    if (dh != 0) smc_gadd(gs + smc_gslot(kk / S), T.cq[kk], dh);
+                    const SmcDLaw L = T.dlaw[kk];
+                    smc_gadd(gs + smc_gslot(kk / S), L.cq, smc_ddh(L, a, b, xs));
                 }
                 at += (unsigned)cnt;
                 __syncwarp();
@@ -392,8 +393,8 @@ extern "C" __global__ void __launch_bounds__(SMC_DBLOCK, 1) smc_ssa_delta(SmcPar
                     for (int m = 0; m < S; ++m) {
                         const int kk = gg * S + m;
                         if (kk < SMC_M) {
-                            const SmcLaw L = T.law[kk];
-                            const smc_u64 h = (smc_u64)smc_dh(L, xs), cq = T.cq[kk];
+                            const SmcDLaw L = T.dlaw[kk];
+                            const smc_u64 h = (smc_u64)smc_dh(L, xs), cq = L.cq;
                             const smc_u64 plo = cq * h;
                             lo += plo;
                             hi += __umul64hi(cq, h) + (lo < plo ? 1ull : 0ull);
