@@ -988,11 +988,19 @@ TileLayout pack_delta_tables(const Model& m) {
     L.off_x0 = o; o = align16(o + 4 * (size_t)L.n_pad);
     L.off_law = o; o = align16(o + 16 * (size_t)G * (size_t)S);   // in-group laws, permuted within groups
     L.off_hill_k = o; o = align16(o + 16 * (size_t)M);      // dependency law {s0 | s1 << 16, kind, Cq_k}
+    // the laws (random gathers every event) are staged in shared memory; the per-event
+    // tables read once per event (change lists, round descriptors, dependency entries) stay
+    // in global memory and are read through the L1 (SMC_DGLOBAL=0: all in shared memory) --
+    // freeing shared memory for more resident trajectories
+    bool dglobal = true;
+    if (const char* e = std::getenv("SMC_DGLOBAL")) dglobal = std::atoi(e) != 0;
+    L.smem_bytes = o;
     L.off_chg = o; o = align16(o + 2 * 4 * (size_t)M);
     L.off_dep_off = o; o = align16(o + (L.fatdep ? 8 : 4) * ((size_t)M + 1));   // round descriptors
     L.off_hill_rep = o; o = align16(o + (L.fatdep ? 0 : (size_t)M * (size_t)L.drmax));   // rcnt[j][r] (u8)
     L.off_dep = o; o = align16(o + (L.dep16 ? 2 : 4) * nnz);
     L.bytes = o;
+    if (!dglobal) L.smem_bytes = L.bytes;
     L.blob.assign(L.bytes, 0);
     auto* x0 = (int32_t*)(L.blob.data() + L.off_x0);
     for (int s = 0; s < N; ++s) x0[s] = m.x0[(size_t)s];
@@ -1317,7 +1325,7 @@ std::string generate_source(const Model& m, const Property& p, int variant, cons
         o << "#define SMC_ANY_EXPLICIT " << (tl->any_explicit ? 1 : 0) << "\n";
     } else if (variant == 5) {
         // upper bound of the CTA (register cap 65536 / blk: TW 32 64, 16 73, 8 102, <= 4 128)
-        int blk = tl->tw >= 32 ? 1024 : (tl->tw == 16 ? 896 : (tl->tw == 8 ? 832 : 512));
+        int blk = tl->tw >= 32 ? 1024 : (tl->tw == 16 ? 896 : (tl->tw == 8 ? 960 : 512));
         if (const char* e = std::getenv("SMC_DBLOCK")) blk = std::max(32, std::atoi(e) / 32 * 32);
         o << "#define SMC_TW " << tl->tw << "\n#define SMC_DG " << tl->dg << "\n#define SMC_DS " << tl->ds
           << "\n#define SMC_DBLOCK " << blk << "\n";
@@ -1329,7 +1337,8 @@ std::string generate_source(const Model& m, const Property& p, int variant, cons
           << "\n#define SMC_OFF_DEP " << tl->off_dep << "\n#define SMC_OFF_RCNT " << tl->off_hill_rep
           << "\n#define SMC_DRMAX " << tl->drmax << "\n#define SMC_DDEP16 " << (tl->dep16 ? 1 : 0)
           << "\n#define SMC_DDESC64 " << (tl->fatdep ? 1 : 0) << "\n";
-        o << "#define SMC_TAB_BYTES " << tl->bytes << "\n#define SMC_TILE_BYTES " << tl->tile_bytes << "\n";
+        o << "#define SMC_TAB_BYTES " << tl->smem_bytes << "\n#define SMC_TILE_BYTES " << tl->tile_bytes << "\n";
+        o << "#define SMC_DGLOBAL " << (tl->smem_bytes < tl->bytes ? 1 : 0) << "\n";
     } else {
         if (p.literal) {
             const double H = p.t_max > 0.0 ? p.t_max : p.horizon;

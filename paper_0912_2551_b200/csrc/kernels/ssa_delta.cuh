@@ -147,18 +147,24 @@ extern "C" __global__ void __launch_bounds__(SMC_DBLOCK, 1) smc_ssa_delta(SmcPar
     SmcDTabs T;
     T.x0 = (const int*)(smem + SMC_OFF_X0);
     T.law = (const SmcLaw*)(smem + SMC_OFF_LAW);
-    T.chg = (const unsigned short*)(smem + SMC_OFF_CHG);
-#if SMC_DDESC64
-    T.dep_off = (const smc_u64*)(smem + SMC_OFF_DOFF);
+    // per-event tables: global memory through the L1 (SMC_DGLOBAL) or the staged shared copy
+#if SMC_DGLOBAL
+    const unsigned char* const tb = (const unsigned char*)P.tables;
 #else
-    T.dep_off = (const unsigned*)(smem + SMC_OFF_DOFF);
+    const unsigned char* const tb = smem;
+#endif
+    T.chg = (const unsigned short*)(tb + SMC_OFF_CHG);
+#if SMC_DDESC64
+    T.dep_off = (const smc_u64*)(tb + SMC_OFF_DOFF);
+#else
+    T.dep_off = (const unsigned*)(tb + SMC_OFF_DOFF);
 #endif
     T.dlaw = (const SmcDLaw*)(smem + SMC_OFF_CQ);
-    T.rcnt = (const unsigned char*)(smem + SMC_OFF_RCNT);
+    T.rcnt = (const unsigned char*)(tb + SMC_OFF_RCNT);
 #if SMC_DDEP16
-    T.dep = (const unsigned short*)(smem + SMC_OFF_DEP);
+    T.dep = (const unsigned short*)(tb + SMC_OFF_DEP);
 #else
-    T.dep = (const unsigned*)(smem + SMC_OFF_DEP);
+    T.dep = (const unsigned*)(tb + SMC_OFF_DEP);
 #endif
     unsigned char* const slice = smem + SMC_TAB_BYTES + ((size_t)warp * TPW + (size_t)tile) * SMC_TILE_BYTES;
     ulonglong2* const gs = (ulonglong2*)slice;                  // G exact group sums

@@ -293,10 +293,11 @@ PropKernel& prepare(Model& m, const Property& p) {
         pk.per_warp = 32 / tl->tw;
         const size_t wb = (size_t)pk.per_warp * tl->tile_bytes;
         const size_t avail = (size_t)d.max_smem_optin - fa.sharedSizeBytes;
-        if (tl->bytes + wb > avail) fail(SMC_E_CUDA, "delta kernel: tables and one warp's slices do not fit in shared memory");
-        const int W = (int)std::min<size_t>((size_t)fa.maxThreadsPerBlock / 32, (avail - tl->bytes) / wb);
+        const size_t tb = tl->smem_bytes;              // the staged part of the tables
+        if (tb + wb > avail) fail(SMC_E_CUDA, "delta kernel: tables and one warp's slices do not fit in shared memory");
+        const int W = (int)std::min<size_t>((size_t)fa.maxThreadsPerBlock / 32, (avail - tb) / wb);
         pk.block = W * 32;
-        pk.smem = (int)(tl->bytes + (size_t)W * wb);
+        pk.smem = (int)(tb + (size_t)W * wb);
         ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, pk.smem), "smem attr");
         int nb = 0;
         ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, pk.block, (size_t)pk.smem), "occupancy");

@@ -167,6 +167,7 @@ struct TileLayout {               // packed model tables (variant 2), byte offse
     int max_dep = 0;
     // variant 5 (delta): G exact fixed-point group sums of S laws, Cq = round(c 2^L)
     int dg = 0, ds = 0, drmax = 0, dl = 0;
+    size_t smem_bytes = 0;        // variant 5: the TMA-staged prefix (the rest is read through L1)
     std::vector<uint8_t> blob;    // host copy
 };
 TileLayout pack_tables(const Model& m, bool sweep = false);   // sweep: law/change tables only (variant 4)
