@@ -94,18 +94,23 @@ int smc_model_set_hill(smc_model* m, int32_t reaction, int32_t repressor, double
 int smc_model_set_rate_expr(smc_model* m, int32_t reaction, const char* expr, const char* const* species_names);
 
 /* Force a kernel variant: 0 = automatic (1 for N, M <= 32; 4 for N <= 160,
- * M <= 1024; else 2), 1 = thread-owned (registers; requires N <= 32 and
- * M <= 32), 2 = warp-owned tile (propensities and counts in shared memory,
- * dependency graph), 4 = thread-owned sweep (counts in a shared-memory column,
- * every law re-evaluated per event; requires the counts of 128 trajectories to
- * fit in shared memory).  3 (buffered trace + literal |=) is not selectable: it
- * is chosen by the formula.  All variants compute the same replicas up to the
- * ulp-level summation orders of reading R12.  SMC_E_ARG if the
- * variant cannot hold the model. */
+ * M <= 1024; else 5 when eligible, else 2), 1 = thread-owned (registers;
+ * requires N <= 32 and M <= 32), 2 = tile-owned (propensities and counts in
+ * shared memory, dependency graph), 4 = thread-owned sweep (counts in a
+ * shared-memory column, every law re-evaluated per event; requires the counts
+ * of 128 trajectories to fit in shared memory), 5 = tile-owned delta kernel (no
+ * stored propensities: exact 128-bit fixed-point group sums updated by the
+ * dependency graph, reading R26; requires mass action of order <= 2 and rates
+ * within ~2^20 of each other).  3 (buffered trace + literal |=) is not
+ * selectable: it is chosen by the formula.  All variants compute the same
+ * replicas up to the ulp-level summation orders of readings R12/R26 (DESIGN.md
+ * §5).  Must be called before the first run (SMC_E_ARG afterwards, or if the
+ * variant cannot hold the model). */
 int smc_model_set_variant(smc_model* m, int32_t variant);
 
 /* Per-replica event cap (default 2^31 - 1): a replica reaching it undecided is
- * counted as an error.  cap >= 1. */
+ * counted as an error.  1 <= cap <= 2^31 - 1 (per-replica event
+ * counts are int32 on the device).  Must be called before the first run. */
 int smc_model_set_event_cap(smc_model* m, uint64_t cap);
 
 /* smc_estimate runs each Fig. 2 round prefix-exactly from a speculative batch
@@ -156,7 +161,8 @@ typedef struct {
  * cursor resets to 0 when seed differs from the previous call's.  With a
  * shard set (smc_set_shard) this rank runs its slice [lo, hi) of the range
  * and the counts are summed over ranks by the allreduce hook.
- * out: the (global) counts.  Errors: SMC_E_ARG, SMC_E_CUDA, SMC_E_COMM. */
+ * out: the (global) counts.  Errors: SMC_E_ARG (also: a property compiled for a
+ * model with another species count), SMC_E_CUDA, SMC_E_COMM. */
 int smc_run(smc_model* m, const smc_property* p, uint64_t n, uint64_t seed, smc_counts* out);
 
 /* cursor <- 0 */
@@ -178,6 +184,10 @@ typedef struct {
  * confidence, half_width, seed) and of nothing else (not of the GPU count).
  * confidence = 1 - alpha in (0,1), half_width = eps in (0, 0.5).
  * On error after some rounds, out holds the partial state.
+ * Every round's global counts must add up to its replica count (true + false +
+ * errors == N), else SMC_E_COMM (mis-tiled shards or a failed reduction).
+ * Speculative per-replica buffers are held to a quarter of the free device
+ * memory and 8 GiB; a larger round runs non-speculatively (same result).
  * Errors: SMC_E_ARG, SMC_E_CUDA, SMC_E_COMM, SMC_E_ERRRATE. */
 int smc_estimate(smc_model* m, const smc_property* p, double confidence, double half_width,
                  uint64_t seed, smc_estimate_t* out);

@@ -641,6 +641,16 @@ struct LiteralChecker {
     LiteralChecker(const Formula& f_, const Trace& tr_) : f(f_), tr(tr_) {
         memo.assign(f.nodes.size(), std::vector<int8_t>((size_t)tr.n() + 1, -1));
     }
+    // Start from the DEFINITE values of a checker on a shorter prefix of the same trace: the
+    // three-valued semantics is monotone in the observed prefix (observing more never revokes
+    // a definite value), so those values hold on this prefix too; unknown ones are recomputed.
+    void seed(const LiteralChecker& shorter) {
+        for (size_t n = 0; n < memo.size(); ++n) {
+            const auto& src = shorter.memo[n];
+            for (size_t m = 0; m < src.size() && m < memo[n].size(); ++m)
+                if (src[m] == T_FALSE || src[m] == T_TRUE) memo[n][m] = src[m];
+        }
+    }
 
     // phi' U^I phi'' at sigma^m:  exists i: sigma^i |= phi'',
     // sum_{j<i} delta(sigma^m, j) in I, and sigma^j |= phi' for all j < i.
@@ -1293,7 +1303,10 @@ int orc_run(void* mp, void* fp, uint64_t seed, uint64_t first, uint64_t n, int32
                 // the literal checker evaluates atoms on stored states: keep all species
                 std::vector<int> keep;
                 for (int s = 0; s < M->N; ++s) keep.push_back(s);
-                simulate_trace(*M, seed, i, H, event_cap, keep, &tr, &err);
+                // the event cap truncates the stored trace (the replica is an error only if
+                // no prefix with fewer than event_cap events decides |=, below)
+                simulate_trace(*M, seed, i, H, event_cap, keep, &tr, &err, false);
+                const bool truncated = !err && !tr.absorbed && (int64_t)tr.tau.size() == tr.n();
                 if (err) rr = {V_ERROR, tr.n()};
                 else {
                     // On-the-fly halting (the replica stops as soon as the formula
@@ -1305,30 +1318,53 @@ int orc_run(void* mp, void* fp, uint64_t seed, uint64_t first, uint64_t n, int32
                     // more never revokes a definite value), so the first such k is found by
                     // bisection over [0, n); if no proper prefix decides, the whole trace
                     // (horizon overshoot or absorption) does, with all n events.
-                    auto prefix_value = [&](int64_t k) {
-                        Trace p;
+                    // prefix k's checker, seeded with the definite values of the longest prefix
+                    // known to be undecided (`base`); bisection over [0, n) by monotonicity
+                    std::unique_ptr<LiteralChecker> base;
+                    auto prefix_check = [&](int64_t k, std::unique_ptr<Trace>& keep) {
+                        keep.reset(new Trace());
+                        Trace& p = *keep;
                         p.N = tr.N;
                         p.t.assign(tr.t.begin(), tr.t.begin() + k + 1);
                         p.tau.assign(tr.tau.begin(), tr.tau.begin() + k + 1);
                         p.x.assign(tr.x.begin(), tr.x.begin() + (k + 1) * tr.N);
                         p.absorbed = false;
-                        LiteralChecker pc(*f, p);
-                        return pc.value(f->root, 0);
+                        std::unique_ptr<LiteralChecker> pc(new LiteralChecker(*f, p));
+                        if (base) pc->seed(*base);
+                        return pc;
                     };
                     const int64_t n_ev = tr.n();
                     const int64_t last = n_ev - 1;
-                    Tri pv = T_UNKNOWN;
-                    if (last >= 0) pv = prefix_value(last);
-                    if (pv != T_UNKNOWN) {
-                        int64_t lo = 0, hi = last;        // invariant: prefix hi is definite
-                        while (lo < hi) {
+                    std::unique_ptr<Trace> base_tr, hi_tr;
+                    int64_t lo = -1, hi = -1;                    // lo undecided, hi definite
+                    Tri hv = T_UNKNOWN;
+                    // gallop: prefixes 63, 127, 255, ... (each seeded from the previous one)
+                    for (int64_t k = std::min<int64_t>(63, last); k >= 0 && hi < 0;
+                         k = (k == last) ? -1 : std::min<int64_t>(2 * k + 1, last)) {
+                        std::unique_ptr<Trace> kt;
+                        auto pc = prefix_check(k, kt);
+                        const Tri v = pc->value(f->root, 0);
+                        if (v != T_UNKNOWN) { hi = k; hv = v; }
+                        else { lo = k; base = std::move(pc); base_tr = std::move(kt); }
+                    }
+                    if (hi >= 0) {
+                        while (hi - lo > 1) {
                             const int64_t mid = lo + (hi - lo) / 2;
-                            if (prefix_value(mid) != T_UNKNOWN) hi = mid; else lo = mid + 1;
+                            std::unique_ptr<Trace> kt;
+                            auto pc = prefix_check(mid, kt);
+                            const Tri v = pc->value(f->root, 0);
+                            if (v != T_UNKNOWN) { hi = mid; hv = v; }
+                            else { lo = mid; base = std::move(pc); base_tr = std::move(kt); }
                         }
-                        const Tri v = prefix_value(hi);
-                        rr = {v == T_TRUE ? V_TRUE : V_FALSE, hi};
+                    }
+                    const Tri pv = hv;
+                    if (pv != T_UNKNOWN) {
+                        rr = {pv == T_TRUE ? V_TRUE : V_FALSE, hi};
+                    } else if (truncated) {
+                        rr = {V_ERROR, n_ev};             // event cap reached undecided
                     } else {
                         LiteralChecker lc(*f, tr);
+                        if (base) lc.seed(*base);
                         Tri v = lc.value(f->root, 0);
                         rr = {v == T_TRUE ? V_TRUE : V_FALSE, n_ev};
                     }

@@ -105,7 +105,10 @@ struct PropKernel {
     double* lit_tau = nullptr;
     unsigned* lit_mask = nullptr;
     unsigned char* lit_val = nullptr;
-    unsigned long long lit_cap = 0;
+    unsigned long long lit_cap = 0;        // entries per replica slot of the current launch
+    size_t lit_entries = 0, lit_per_entry = 0;
+    int lit_per_cta = 0;                   // replicas per CTA (0: not a literal kernel)
+    size_t lit_nodes = 0;                  // subformula nodes of the literal |=
     smc_launch_info info{};
     uint64_t cap_global = 0;               // sum of capacity() over the ranks (one allreduce)
     uint64_t capacity() const {            // trajectories resident at once on this GPU
@@ -187,29 +190,42 @@ DeviceState& device(Model& m) {
     return *m.dev;
 }
 
-// Trace buffers of the literal |= (reading R23) for `per_cta` replicas per CTA: at most a
-// quarter of the free device memory and 16 GiB per property; every resident replica
-// gets >= 4096 entries (fewer resident CTAs if needed) and no more than the event cap.
-void alloc_traces(Model& m, const Property& p, PropKernel& pk, int per_cta) {
+// Trace buffers of the literal |= (reading R23), sized PER LAUNCH: the `grid` CTAs of this
+// launch hold `per_cta` replicas each, and every resident replica gets an equal share of the
+// budget (a quarter of the free device memory, at most 16 GiB per property) up to the event
+// cap (<= 2^24 entries).  A small batch (e.g. 2,000 replicas) therefore gets long traces --
+// full horizons of C3 / C4 -- while a machine-filling batch gets >= 4096 entries per replica
+// (fewer resident CTAs if needed).  The buffers grow when a launch needs more entries.
+void size_traces(Model& m, PropKernel& pk, int per_cta, int& grid) {
     size_t free_b = 0, total_b = 0;
     ck(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
-    const size_t budget = std::min<size_t>(free_b / 4, (size_t)16 << 30);
-    const size_t per_entry = 8 + 8 + 4 + p.lnodes.size();
+    const size_t held = (size_t)pk.lit_entries * pk.lit_per_entry;   // ours, reusable
+    const size_t budget = std::min<size_t>((free_b + held) / 4, (size_t)16 << 30);
+    const size_t per_entry = 8 + 8 + 4 + pk.lit_nodes;
     const size_t want_cap = (size_t)std::min<uint64_t>(m.event_cap + 2, 1ull << 24);
-    size_t slots = (size_t)pk.grid_max * (size_t)per_cta;
     const size_t min_cap = std::min<size_t>(want_cap, 4096);
-    if (budget / (slots * per_entry) < min_cap) {
-        const size_t blocks = std::max<size_t>(1, budget / (min_cap * per_entry * (size_t)per_cta));
-        pk.grid_max = (int)std::min<size_t>((size_t)pk.grid_max, blocks);
-        slots = (size_t)pk.grid_max * (size_t)per_cta;
-    }
+    if (budget / ((size_t)grid * (size_t)per_cta * per_entry) < min_cap)
+        grid = (int)std::max<size_t>(1, budget / (min_cap * per_entry * (size_t)per_cta));
+    const size_t slots = (size_t)grid * (size_t)per_cta;
     const size_t cap = std::min<size_t>(budget / (slots * per_entry), want_cap);
     if (cap < 16) fail(SMC_E_CUDA, "literal |=: not enough device memory for trace buffers");
+    if (slots * cap > pk.lit_entries || per_entry != pk.lit_per_entry) {
+        dfree(pk.lit_t);
+        dfree(pk.lit_tau);
+        dfree(pk.lit_mask);
+        dfree(pk.lit_val);
+        pk.lit_t = pk.lit_tau = nullptr;
+        pk.lit_mask = nullptr;
+        pk.lit_val = nullptr;
+        pk.lit_entries = 0;
+        pk.lit_t = (double*)dalloc(slots * cap * 8);
+        pk.lit_tau = (double*)dalloc(slots * cap * 8);
+        pk.lit_mask = (unsigned*)dalloc(slots * cap * 4);
+        pk.lit_val = (unsigned char*)dalloc(slots * cap * pk.lit_nodes);
+        pk.lit_entries = slots * cap;
+        pk.lit_per_entry = per_entry;
+    }
     pk.lit_cap = cap;
-    pk.lit_t = (double*)dalloc(slots * cap * 8);
-    pk.lit_tau = (double*)dalloc(slots * cap * 8);
-    pk.lit_mask = (unsigned*)dalloc(slots * cap * 4);
-    pk.lit_val = (unsigned char*)dalloc(slots * cap * p.lnodes.size());
 }
 
 PropKernel& prepare(Model& m, const Property& p) {
@@ -270,7 +286,8 @@ PropKernel& prepare(Model& m, const Property& p) {
         ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, pk.block, 0), "occupancy");
         pk.grid_max = std::max(1, nb) * d.sm_count;
         pk.smem = 0;
-        alloc_traces(m, p, pk, pk.block);
+        pk.lit_per_cta = pk.block;          // buffers sized per launch (size_traces)
+        pk.lit_nodes = p.lnodes.size();
     } else if (pk.variant == 4) {
         pk.block = tl->sw_blk;
         pk.smem = (int)(tl->bytes + (size_t)pk.block * (tl->sw_xd ? 8 : 4) * (size_t)(m.N + 1));
@@ -330,7 +347,10 @@ PropKernel& prepare(Model& m, const Property& p) {
         pk.smem = (int)(tl->bytes + (size_t)best_w * wb);
         pk.grid_max = best_nb * d.sm_count;
         pk.per_warp = 32 / tl->tw;
-        if (p.literal) alloc_traces(m, p, pk, best_w * pk.per_warp);   // one trace per tile
+        if (p.literal) {                   // one trace per tile, sized per launch (size_traces)
+            pk.lit_per_cta = best_w * pk.per_warp;
+            pk.lit_nodes = p.lnodes.size();
+        }
     }
     pk.info.variant = pk.variant;
     pk.info.block_threads = pk.block;
@@ -378,7 +398,15 @@ void launch_slice(Model& m, PropKernel& pk, uint64_t seed, uint64_t lo, uint64_t
     const uint64_t per_block = (pk.variant != 2 && pk.variant != 5) ? (uint64_t)block
                                                                     : (uint64_t)(pk.block / 32 * pk.per_warp);
     const uint64_t need = (count + per_block - 1) / per_block;
-    const int grid = (int)std::min<uint64_t>((uint64_t)pk.grid_max, need);
+    int grid = (int)std::min<uint64_t>((uint64_t)pk.grid_max, need);
+    if (pk.lit_per_cta) {                  // literal |=: this launch's trace buffers
+        size_traces(m, pk, pk.lit_per_cta, grid);
+        P.lit_t = pk.lit_t;
+        P.lit_tau = pk.lit_tau;
+        P.lit_mask = pk.lit_mask;
+        P.lit_val = pk.lit_val;
+        P.lit_cap = pk.lit_cap;
+    }
     void* args[] = {&P};
     ck(cudaEventRecord(d.e0, stream()), "event");
     ck(cudaLaunchKernel((const void*)pk.k->kernel, dim3((unsigned)grid), dim3((unsigned)block), args,

@@ -25,7 +25,9 @@ def dram(rep):
         return float(r[hdr.index(m)]) if m in hdr and r[hdr.index(m)] not in ("", "n/a") else None
     wf, wfi = f("memory_l1_wavefronts_shared"), f("memory_l1_wavefronts_shared_ideal")
     return {"kernel": r[hdr.index("Kernel Name")], "dram_bytes_per_launch": tot,
-            "duration_ns": float(r[hdr.index("gpu__time_duration.sum")]) * (1e6 if units[hdr.index("gpu__time_duration.sum")] == "ms" else 1.0),
+            "duration_ns": float(r[hdr.index("gpu__time_duration.sum")]) *
+                           {"s": 1e9, "ms": 1e6, "us": 1e3, "usecond": 1e3, "msecond": 1e6, "second": 1e9}.get(
+                               units[hdr.index("gpu__time_duration.sum")], 1.0),
             "issue_active_pct": f("smsp__issue_active.avg.pct_of_peak_sustained_active"),
             "smem_wavefront_pct": f("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"),
             "smem_wavefront_excess": (wf / wfi) if wf and wfi else None}

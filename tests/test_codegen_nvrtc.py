@@ -13,7 +13,7 @@ sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(
 from check_codegen import nvrtc_cubin  # noqa: E402
 
 CASES = [("C1", 1), ("C1", 4), ("C2", 1), ("C2", 2), ("C2", 4), ("C3", 1), ("C3", 2), ("C3", 4), ("C4", 2), ("C4", 4),
-         ("C5", 2), ("C5", 4), ("EXPL", 1), ("EXPL", 2), ("EXPL", 4), ("CC", 1), ("CC", 2), ("CC", 4)]
+         ("C5", 2), ("C5", 4), ("C5", 5), ("C4", 5), ("C2", 5), ("EXPL", 1), ("EXPL", 2), ("EXPL", 4), ("CC", 1), ("CC", 2), ("CC", 4)]
 
 
 def _compile(cfg, variant, formula=None, t_max=0.0):

@@ -123,10 +123,17 @@ def test_variant_selection_and_errors():
     cfg = workloads.c4()
     m = smc.Model.from_config(cfg)
     p = smc.Property(m, cfg["formula"])
-    for v, entry in ((2, "smc_ssa_tile"), (4, "smc_ssa_sweep"), (0, "smc_ssa_sweep")):
+    for v, entry in ((2, "smc_ssa_tile"), (4, "smc_ssa_sweep"), (5, "smc_ssa_delta"), (0, "smc_ssa_sweep")):
         m.set_variant(v)
         assert entry in m.kernel_source(p)
-    for bad in (3, 5, -1, 1):            # 3 is the literal variant (chosen by the formula), 1 needs N, M <= 32
+    # the automatic choice for C5 (N = 200: beyond the sweep) is the delta kernel
+    m5 = smc.Model.from_config(workloads.c5())
+    assert "smc_ssa_delta" in m5.kernel_source(smc.Property(m5, workloads.c5()["formula"]))
+    # the delta kernel needs mass action of order <= 2 (C3's Hill laws are not)
+    m3 = smc.Model.from_config(workloads.c3())
+    with pytest.raises(smc.SmcError):
+        m3.set_variant(5)
+    for bad in (3, 6, -1, 1):            # 3 is the literal variant (chosen by the formula), 1 needs N, M <= 32
         with pytest.raises(smc.SmcError):
             m.set_variant(bad)
     # a literal (nested) formula on a sweep model runs the tile kernel's recording monitor
@@ -191,7 +198,8 @@ def test_rate_expression_errors_and_codegen():
 def test_sweep_configuration_choices():
     """The automatic shape of the sweep kernel (DESIGN.md §5 knob table): C4 gets binary64
     columns in one 384-thread CTA per SM, groups of 7 laws read in one chunk and fused sums;
-    a (64, 512) network groups of 18 read in chunks of 6; C5 (N = 200) the tile kernel."""
+    a (64, 512) network groups of 18 read in chunks of 6; C5 (N = 200) the delta kernel with
+    8-lane tiles, 32 groups of 32 laws and the per-event tables in global memory."""
     cfg = workloads.c4()
     m = smc.Model.from_config(cfg)
     src = m.kernel_source(smc.Property(m, cfg["formula"]))
@@ -206,7 +214,10 @@ def test_sweep_configuration_choices():
     assert "#define SMC_SW_S 18" in src2 and "#define SMC_SW_C 6" in src2 and "smc_ssa_sweep" in src2
     c5 = workloads.c5()
     m5 = smc.Model.from_config(c5)
-    assert "smc_ssa_tile" in m5.kernel_source(smc.Property(m5, c5["formula"]))
+    src5 = m5.kernel_source(smc.Property(m5, c5["formula"]))
+    for d in ("smc_ssa_delta", "#define SMC_TW 8", "#define SMC_DG 32", "#define SMC_DS 32", "#define SMC_DGLOBAL 1",
+              "#define SMC_DDEP16 1", "#define SMC_DDESC64 1"):
+        assert d in src5, d
 
 
 def test_property_of_another_model_and_event_cap_bounds():

@@ -181,7 +181,7 @@ def test_hill_propensity():
 
 def test_streaming_equals_literal_on_models():
     """On-the-fly verdicts == literal |= on the full trace for C1, C2 and C3."""
-    for cfg, n in [(workloads.c1(), 2000), (workloads.c2(), 300), (workloads.c3(), 12), (workloads.c3r(), 200)]:
+    for cfg, n in [(workloads.c1(), 2000), (workloads.c2(), 300), (workloads.c3(), 3), (workloads.c3r(), 60)]:
         c1, v1, e1 = _estimate(cfg, cfg["formula"], n, cfg["seed"], mode="stream")
         c2, v2, e2 = _estimate(cfg, cfg["formula"], n, cfg["seed"], mode="literal")
         assert (v1 == v2).all(), cfg["name"]
