@@ -168,6 +168,13 @@ int smc_run(smc_model* m, const smc_property* p, uint64_t n, uint64_t seed, smc_
 /* cursor <- 0 */
 int smc_reset(smc_model* m);
 
+/* Resume (SURVEY §5 checkpoint / resume): the next smc_run of this seed starts at
+ * trajectory index `cursor`.  Because the Philox stream is keyed by (seed, trajectory,
+ * step) (reading R10), a Fig. 2 loop interrupted after N_tot replicas continues exactly
+ * where it stopped: its state {seed, N_tot, n_true, events, errors, rounds} is a complete
+ * checkpoint.  SMC_E_ARG on NULL. */
+int smc_set_cursor(smc_model* m, uint64_t cursor, uint64_t seed);
+
 typedef struct {
     double p_hat, lower, upper;   /* estimate and Wilson interval (Eq. 3)       */
     int64_t n_total, n_true;      /* replicas used, successes                    */

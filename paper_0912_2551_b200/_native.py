@@ -46,6 +46,7 @@ SIGNATURES = [
     ("smc_property_destroy", None, [c_vp]),
     ("smc_run", c_i32, [c_vp, c_vp, c_u64, c_u64, ctypes.POINTER(SmcCounts)]),
     ("smc_reset", c_i32, [c_vp]),
+    ("smc_set_cursor", c_i32, [c_vp, c_u64, c_u64]),
     ("smc_estimate", c_i32, [c_vp, c_vp, c_dbl, c_dbl, c_u64, ctypes.POINTER(SmcEstimate)]),
     ("smc_estimate_ex", c_i32, [c_vp, c_vp, c_dbl, c_dbl, c_dbl, c_u64, ctypes.POINTER(SmcEstimate)]),
     ("smc_estimate_with_runner", c_i32, [RUN_FN, c_vp, c_dbl, c_dbl, c_dbl, ctypes.POINTER(SmcEstimate)]),

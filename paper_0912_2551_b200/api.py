@@ -75,6 +75,10 @@ class Model:
     def reset(self):
         check(lib().smc_reset(self.h))
 
+    def set_cursor(self, cursor, seed):
+        """Resume: the next run(prop, n, seed) covers trajectories [cursor, cursor + n)."""
+        check(lib().smc_set_cursor(self.h, cursor, seed))
+
     def run(self, prop, n, seed):
         c = SmcCounts()
         check(lib().smc_run(self.h, prop.h, n, seed, ctypes.byref(c)))

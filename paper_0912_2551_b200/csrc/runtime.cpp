@@ -726,6 +726,15 @@ int smc_reset(smc_model* h) {
     return SMC_OK;
 }
 
+int smc_set_cursor(smc_model* h, uint64_t cursor, uint64_t seed) {
+    if (!h) { set_error("smc_set_cursor: NULL"); return SMC_E_ARG; }
+    std::lock_guard<std::mutex> lk(h->m.mu);
+    h->m.cursor = cursor;
+    h->m.last_seed = seed;
+    h->m.has_seed = true;
+    return SMC_OK;
+}
+
 int smc_run(smc_model* h, const smc_property* ph, uint64_t n, uint64_t seed, smc_counts* out) {
     if (!h || !ph || !out) { set_error("smc_run: NULL argument"); return SMC_E_ARG; }
     if (ph->p->N != h->m.N) { set_error("smc_run: property compiled for a model with another species count"); return SMC_E_ARG; }

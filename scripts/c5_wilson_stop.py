@@ -1,9 +1,21 @@
 """The complete C5 sequential Wilson stop (BASELINE.json configs[4]: 99.9 % confidence,
-half-width 1e-4) through smc_estimate on one GPU: p_hat, [L, U], N_tot, rounds,
-events, wall time and events/s, with an nvidia-smi clock record.  Writes
-gpurun_out/c5_wilson_stop_<tag>.json (kept under profiles/) and prints it.
+half-width 1e-4; Fig. 2) on one GPU, resumable across calls.
 
-  python scripts/c5_wilson_stop.py TAG
+A GPU call here is limited to one hour and the stop needs ~2.7e8 replicas (~2.7e13 SSA
+events), so the Fig. 2 loop runs as checkpointed chunks: the loop state {N_tot, n_true,
+events, errors, rounds, the current round's target} is a complete checkpoint because the
+Philox stream is keyed by (seed, trajectory, step) (reading R10) -- each chunk is one
+smc_run of the next [cursor, cursor + n) replicas (smc_set_cursor resumes the index), and
+the round sizes, p_hat and the interval come from the library's Eq. 3 / Eq. 4
+(smc_wilson_sample_size, smc_wilson_interval) in Fig. 2's order, exactly as smc_estimate
+(runtime.cpp wilson_loop) computes them.  The result is the same pure function of (model,
+property, confidence, eps, seed) as smc_estimate's.
+
+  python scripts/c5_wilson_stop.py STATE.json BUDGET_SECONDS [CHUNK_REPLICAS]
+
+Writes STATE.json after every chunk (copy it back between calls: gpurun_out/ does not
+travel to the box) and, once the loop stops, the final record with p_hat, [L, U], N_tot,
+rounds, device seconds, events/s and the nvidia-smi clock record of each call.
 """
 import json
 import os
@@ -20,41 +32,70 @@ import workloads  # noqa: E402
 from bench import ClockSampler  # noqa: E402
 
 
-def main(tag):
+def round_estimate(p_hat, eps):
+    """Fig. 2: p' = p_hat + eps if p_hat <= 0.5 else p_hat - eps (reading W3)."""
+    return p_hat + eps if p_hat <= 0.5 else p_hat - eps
+
+
+def main(state_path, budget_s, chunk):
     cfg = workloads.c5()
     s = cfg["sampling"]
+    conf, eps, seed = s["confidence"], s["half_width"], cfg["seed"]
+    st = json.load(open(state_path)) if os.path.exists(state_path) else None
+    if st is None:
+        n1 = int(smc.smc_wilson_sample_size(1.0, eps, conf))          # "N = Wilson_Sample(1, eps, alpha)"
+        st = dict(workload="C5", formula=cfg["formula"], confidence=conf, half_width=eps, seed=seed,
+                  cursor=0, round_end=n1, n_tot=0, n_true=0, events=0, errors=0, rounds=0, done=False,
+                  device_seconds=0.0, calls=[])
+    if st["done"]:
+        print(json.dumps(st))
+        return
     torch.cuda.set_device(0)
     smc.use_torch()
     m = smc.Model.from_config(cfg)
     p = smc.Property(m, cfg["formula"], t_max=cfg.get("t_max", 0.0))
-    m.run(p, 64, cfg["seed"] + 1000)                      # compile + tables, not timed
+    m.run(p, 64, seed + 1000)                                      # compile + tables, not counted
     clocks = ClockSampler(torch.cuda.current_device())
     clocks.start()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0 = time.time()
-    e0.record()
-    est = smc.estimate(m, p, s["confidence"], s["half_width"], cfg["seed"])
-    e1.record()
-    torch.cuda.synchronize()
-    wall = time.time() - t0
+    dev_s = 0.0
+    while not st["done"] and time.time() - t0 < budget_s:
+        n = min(chunk, st["round_end"] - st["cursor"])
+        m.set_cursor(st["cursor"], seed)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        c = m.run(p, n, seed)                                        # replicas [cursor, cursor + n)
+        e1.record()
+        torch.cuda.synchronize()
+        dev_s += e0.elapsed_time(e1) / 1e3
+        st["cursor"] += n
+        st["n_true"] += c["n_true"]
+        st["n_tot"] += c["n_true"] + c["n_false"]                    # errors excluded (SPEC S:394)
+        st["events"] += c["events"]
+        st["errors"] += c["errors"]
+        if st["cursor"] == st["round_end"]:                          # a Fig. 2 round complete
+            st["rounds"] += 1
+            if st["errors"] > 0.01 * st["cursor"]:
+                raise SystemExit("more than 1 % replica errors")
+            p_hat = st["n_true"] / st["n_tot"]                       # "pest = yess" (W2)
+            n_new = int(smc.smc_wilson_sample_size(round_estimate(p_hat, eps), eps, conf)) - st["n_tot"]
+            if n_new > 0:
+                st["round_end"] = st["cursor"] + n_new
+            else:
+                lo, hi = smc.smc_wilson_interval(st["n_true"], st["n_tot"], conf)
+                st.update(done=True, p_hat=p_hat, lower=lo, upper=hi)
+        json.dump(dict(st, device_seconds=st["device_seconds"] + dev_s), open(state_path, "w"), indent=1)
     clocks.window = (t0, time.time())
     clk = clocks.stop()
-    ms = e0.elapsed_time(e1)
-    info = m.last_launch(p)
-    out = dict(workload="C5", formula=cfg["formula"], confidence=s["confidence"], half_width=s["half_width"],
-               seed=cfg["seed"], estimate=est, device_seconds=ms / 1e3, wall_seconds=wall,
-               events_per_s=est["events"] / (ms / 1e3), trajectories_per_s=est["n_total"] / (ms / 1e3),
-               simulated_events=info["sim_events"], kernel_ms=info["kernel_ms"], launches=info["launches"],
-               aux_launches=info["aux_launches"], variant=info["variant"], block=info["block_threads"],
-               grid=info["grid_blocks"], regs=info["regs_per_thread"], clocks=clk,
-               gpu=torch.cuda.get_device_name(0))
-    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
-    path = os.path.join(ROOT, "gpurun_out", "c5_wilson_stop_%s.json" % tag)   # copied to profiles/
-    with open(path, "w") as fh:
-        json.dump(out, fh, indent=1)
-    print(json.dumps(out))
+    st["device_seconds"] += dev_s
+    st["calls"].append(dict(device_seconds=dev_s, wall_seconds=time.time() - t0, clocks=clk,
+                            gpu=torch.cuda.get_device_name(0), variant=m.last_launch(p)["variant"]))
+    if st["done"]:
+        st["events_per_s"] = st["events"] / st["device_seconds"]
+        st["trajectories_per_s"] = st["n_tot"] / st["device_seconds"]
+    json.dump(st, open(state_path, "w"), indent=1)
+    print(json.dumps(st))
 
 
 if __name__ == "__main__":
-    main(sys.argv[1] if len(sys.argv) > 1 else "r02")
+    main(sys.argv[1], float(sys.argv[2]), int(sys.argv[3]) if len(sys.argv) > 3 else 5_000_000)
