@@ -229,7 +229,9 @@ def oracle_sample(cfg, budget_s, procs=None, first_chunk=None):
         return dict(events=ev, trajectories=tr, seconds=el, procs=procs, n=last["n_total"], runs=runs,
                     what="%d complete Fig. 2 estimates (%d replicas each)" % (runs, last["n_total"]))
     total_n = samp["n"] if samp["mode"] == "fixed" else None
-    chunk = first_chunk or procs * 8
+    # one replica per process first on the large networks (a C5 replica is ~1e5 events at
+    # M = 1000 full recomputes: seconds of oracle time), so the sample stays bounded
+    chunk = first_chunk or (procs * 8 if len(cfg["reactions"]) <= 256 else procs)
     first = 0
     tot = dict(n_true=0, n_false=0, events=0, errors=0)
     t0 = time.perf_counter()
