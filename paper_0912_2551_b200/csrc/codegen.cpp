@@ -123,6 +123,10 @@ struct MonGen {
             if (lf.kind == LeafKind::GU) o << "    bool w" << i << "; double D" << i << ";\n";
         }
         o << "    __device__ __forceinline__ void bind(const SmcParams&, smc_u64, unsigned, int) {}\n";
+        // a streaming monitor stops the moment it decides: the events applied are the count;
+        // reaching the event cap undecided is an error
+        o << "    __device__ __forceinline__ long long events(long long k) const { return k; }\n";
+        o << "    __device__ __forceinline__ int at_cap(long long) { return 2; }\n";
         // init
         o << "    __device__ __forceinline__ void init() {\n";
         for (size_t i = 0; i < L; ++i) {
@@ -327,6 +331,18 @@ std::string literal_code(const Property& P) {
         o << "    }\n";
     }
     o << "    return vb[" << P.lroot << "LL * cap];\n}\n";
+    // the exact first decision index: the three-valued |= of the prefix is
+    // monotone in the prefix, so given prefix `hi` definite (value r) and prefix `lo`
+    // undecided (-1: none), bisection finds the first definite prefix in (lo, hi]
+    o << "__device__ __noinline__ long long smc_lit_first(const double* __restrict__ tb, const double* __restrict__ ub,\n"
+         "                                             const unsigned* __restrict__ mb, unsigned char* __restrict__ vb,\n"
+         "                                             long long lo, long long hi, long long cap, int& r) {\n"
+         "    while (hi - lo > 1) {\n"
+         "        const long long mid = lo + (hi - lo) / 2;\n"
+         "        const int v = smc_lit_eval(tb, ub, mb, vb, mid, false, cap);\n"
+         "        if (v != 2) { hi = mid; r = v; } else lo = mid;\n"
+         "    }\n"
+         "    return hi;\n}\n";
     return o.str();
 }
 
@@ -338,6 +354,7 @@ std::string recording_monitor(const Property& P) {
     std::ostringstream o;
     o << "struct SmcMon {   // recording monitor for: " << P.text << "\n"
          "    double* tb; double* ub; unsigned* mb; unsigned char* vb; long long cap, last; int res;\n"
+         "    long long undecided, decided_at;   // longest prefix found undecided; first decision index\n"
          "    unsigned tmask; int leader;   // the tile's lanes; the tile's first lane writes and evaluates\n"
          "    __device__ __forceinline__ void bind(const SmcParams& Q, smc_u64 slot, unsigned mask, int lead) {\n"
          "        cap = (long long)Q.lit_cap; tmask = mask; leader = lead;\n"
@@ -357,7 +374,16 @@ std::string recording_monitor(const Property& P) {
          "        if (lead()) r = smc_lit_eval(tb, ub, mb, vb, n, false, cap);\n"
          "        return __shfl_sync(tmask, r, leader);\n"
          "    }\n"
-         "    __device__ __forceinline__ void init() { res = -1; last = 0; }\n"
+         "    // exact first decision index (leader lane), broadcast with the value\n"
+         "    __device__ __forceinline__ int first(long long lo, long long hi, int r) {\n"
+         "        long long k = hi;\n"
+         "        __syncwarp(tmask);\n"
+         "        if (lead()) k = smc_lit_first(tb, ub, mb, vb, lo, hi, cap, r);\n"
+         "        r = __shfl_sync(tmask, r, leader);\n"
+         "        decided_at = (long long)__shfl_sync(tmask, (int)k, leader);\n"
+         "        return r;\n"
+         "    }\n"
+         "    __device__ __forceinline__ void init() { res = -1; last = 0; undecided = -1; decided_at = -1; }\n"
          "    template <class XA> __device__ __forceinline__ void enter(smc_u32 k, double t, double tp, const XA& x) {\n"
          "        (void)tp;\n"
          "        if (res >= 0) return;\n"
@@ -366,17 +392,37 @@ std::string recording_monitor(const Property& P) {
          "        if (lead()) { tb[k] = t; mb[k] = mk; }\n"
          "        last = (long long)k;\n"
          "    }\n"
+         "    // at the end of the trace (horizon overshoot after entry n, or absorption at n): the\n"
+         "    // first definite proper prefix if any (P:291-294), else the whole trace with n events\n"
+         "    __device__ __forceinline__ void finish(long long n, bool absorbed) {\n"
+         "        if (n - 1 > undecided) {\n"
+         "            const int r = eval3(n - 1);\n"
+         "            if (r != 2) { res = first(undecided, n - 1, r); return; }\n"
+         "        }\n"
+         "        res = eval(n, absorbed);\n"
+         "        decided_at = n;\n"
+         "    }\n"
          "    __device__ __forceinline__ void advance(smc_u32 k, double tn, double tau) {\n"
          "        if (res >= 0) return;\n"
          "        if (lead()) ub[k] = tau;\n"
-         "        if (tn > SMC_LIT_H) res = eval((long long)k, false);\n"
-         "        else if (k >= 64u && (k & (k - 1u)) == 0u) {   // checkpoint: halt once decided (R24)\n"
+         "        if (tn > SMC_LIT_H) finish((long long)k, false);\n"
+         "        else if (k >= 64u && (k & (k - 1u)) == 0u) {   // checkpoint (R24): the prefix decides?\n"
          "            const int r = eval3((long long)k);\n"
-         "            if (r != 2) res = r;\n"
+         "            if (r != 2) res = first(undecided, (long long)k, r);   // then its first decision index\n"
+         "            else undecided = (long long)k;\n"
          "        }\n"
          "    }\n"
          "    __device__ __forceinline__ void absorb() {\n"
-         "        if (res < 0) res = eval(last, true);\n"
+         "        if (res < 0) finish(last, true);\n"
+         "    }\n"
+         "    __device__ __forceinline__ long long events(long long k) const { return decided_at >= 0 ? decided_at : k; }\n"
+         "    // the event cap reached at entry k undecided: the prefix up to entry k - 1 may decide\n"
+         "    __device__ __forceinline__ int at_cap(long long k) {\n"
+         "        if (k - 1 > undecided) {\n"
+         "            const int r = eval3(k - 1);\n"
+         "            if (r != 2) return first(undecided, k - 1, r);\n"
+         "        }\n"
+         "        return 2;\n"
          "    }\n"
          "    __device__ __forceinline__ void timeout() {}\n"
          "    __device__ __forceinline__ int verdict() const { return res; }\n"

@@ -10,15 +10,18 @@
 // subformula bottom-up over the buffer, in the order and arithmetic of the
 // semantics (elapsed = tau_m + tau_{m+1} + ... left to right), three-valued,
 // and the root at sigma[0] gives the verdict (unknown -> false).
-// On-the-fly halting at checkpoints (reading R24): after the sojourn of entry k
-// is drawn, for k = 64, 128, 256, ..., the three-valued |= of the prefix (entries
-// 0..k, the unobserved future unknown) is evaluated; a definite value is final
-// (the semantics is monotone in the observed prefix) and the replica halts with
-// k events.  Otherwise the replica runs to the horizon as before.  A trace
-// longer than the buffer capacity ends the replica as an error.
+// On-the-fly halting (reading R24): after the sojourn of entry k is drawn, at the
+// checkpoints k = 64, 128, 256, ..., the three-valued |= of the prefix (entries 0..k,
+// the unobserved future unknown) is evaluated; a definite value is final (the
+// semantics is monotone in the observed prefix) and the replica stops -- its event
+// count is the FIRST decision index k* (P:291-294), found by bisection over the
+// buffered prefixes between the last undecided checkpoint and k (smc_lit_first), the
+// same count the oracle's literal mode returns.  Otherwise the replica runs to the
+// horizon (and k* is searched among its proper prefixes).  A trace longer than the
+// buffer capacity ends the replica as an error.
 //
 // Generated hooks (codegen.cpp): as variant 1, plus SMC_LIT_H, SMC_LIT_NODES,
-//   smc_lit_mask(x), smc_lit_eval(t, tau, mask, val, n, absorbed, cap).
+//   smc_lit_mask(x), smc_lit_eval(t, tau, mask, val, n, absorbed, cap), smc_lit_first.
 
 extern "C" __global__ void __launch_bounds__(SMC_BLOCK, 2) smc_ssa_literal(SmcParams P) {
     const smc_u64 gtid = (smc_u64)blockIdx.x * blockDim.x + threadIdx.x;
@@ -45,6 +48,7 @@ extern "C" __global__ void __launch_bounds__(SMC_BLOCK, 2) smc_ssa_literal(SmcPa
         mb[0] = smc_lit_mask(x);
         bool absorbed = false, err = false;
         int decided = -1;
+        long long und = -1, kev = -1;                      // longest prefix undecided; first decision index
         for (;;) {
             double A = a[0];
 #pragma unroll
@@ -60,13 +64,23 @@ extern "C" __global__ void __launch_bounds__(SMC_BLOCK, 2) smc_ssa_literal(SmcPa
             const double tn = __dadd_rn(t, tau);
             ub[k] = tau;
             if (tn > SMC_LIT_H) break;                    // overshoot: the trace covers the horizon
-            if (k >= 64 && (k & (k - 1)) == 0) {          // checkpoint k = 64 * 2^i: halt once the
-                const int r = smc_lit_eval(tb, ub, mb, vb, (long long)k, false, (long long)cap);
-                if (r != 2) { decided = r; break; }       // prefix decides |= (reading R24)
+            if (k >= 64 && (k & (k - 1)) == 0) {          // checkpoint k = 64 * 2^i (R24): halt once the
+                int r = smc_lit_eval(tb, ub, mb, vb, (long long)k, false, (long long)cap);
+                if (r != 2) {                             // prefix decides |=; its first decision index
+                    kev = smc_lit_first(tb, ub, mb, vb, und, (long long)k, (long long)cap, r);
+                    decided = r;
+                    break;
+                }
+                und = (long long)k;
             }
             if (k + 1 >= P.event_cap) {                   // the next event would reach the cap: the
-                const int r = smc_lit_eval(tb, ub, mb, vb, (long long)k, false, (long long)cap);
-                if (r != 2) decided = r; else err = true;   // prefix decides now, else an error
+                int r = smc_lit_eval(tb, ub, mb, vb, (long long)k, false, (long long)cap);
+                if (r != 2) {                             // prefix decides now, else an error
+                    kev = smc_lit_first(tb, ub, mb, vb, und, (long long)k, (long long)cap, r);
+                    decided = r;
+                } else {
+                    err = true;
+                }
                 break;
             }
             if (k + 1 >= cap) { err = true; break; }      // trace buffer full (reading R23)
@@ -88,8 +102,18 @@ extern "C" __global__ void __launch_bounds__(SMC_BLOCK, 2) smc_ssa_literal(SmcPa
             mb[k] = smc_lit_mask(x);
         }
         int v = 2;
-        if (decided >= 0) v = decided;
-        else if (!err) v = smc_lit_eval(tb, ub, mb, vb, (long long)k, absorbed, (long long)cap) == 1 ? 1 : 0;
+        if (decided >= 0) {
+            v = decided;
+        } else if (!err) {
+            // end of the trace (horizon overshoot after entry k, or absorption at k): the first
+            // definite proper prefix if any, else the whole trace with k events
+            if ((long long)k - 1 > und) {
+                int r = smc_lit_eval(tb, ub, mb, vb, (long long)k - 1, false, (long long)cap);
+                if (r != 2) { kev = smc_lit_first(tb, ub, mb, vb, und, (long long)k - 1, (long long)cap, r); v = r; }
+            }
+            if (v == 2) v = smc_lit_eval(tb, ub, mb, vb, (long long)k, absorbed, (long long)cap) == 1 ? 1 : 0;
+        }
+        if (kev >= 0) k = (smc_u64)kev;                    // events: the first decision index
         if (v == 1) ++c_true;
         else if (v == 0) ++c_false;
         else ++c_err;

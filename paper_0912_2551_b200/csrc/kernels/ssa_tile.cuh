@@ -458,16 +458,17 @@ extern "C" __global__ void __launch_bounds__(768, 1) smc_ssa_tile(SmcParams P) {
                     ++k;
                     mon.enter(k, t, tp, xs);
                     v = mon.verdict();
-                    if (v < 0 && (smc_u64)k >= P.event_cap) v = 2;
+                    if (v < 0 && (smc_u64)k >= P.event_cap) v = mon.at_cap((long long)k);
                 }
             }
             if (act && v >= 0) {
-                if (tl == 0) {
+                const long long ke = mon.events((long long)k);   // the recording monitor: the first
+                if (tl == 0) {                                    // decision index
                     if (v == 1) ++c_true;
                     else if (v == 0) ++c_false;
                     else ++c_err;
-                    c_ev += k;
-                    if (P.verdicts) { P.verdicts[rel] = (unsigned char)v; P.events_out[rel] = (int)k; }
+                    c_ev += ke;
+                    if (P.verdicts) { P.verdicts[rel] = (unsigned char)v; P.events_out[rel] = (int)ke; }
                 }
                 act = false;
             }

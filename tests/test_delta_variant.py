@@ -107,3 +107,39 @@ def test_random_mass_action_networks(smc, seed):
     bad = int(((v.cpu().numpy() != ov) | (e.cpu().numpy() != oe)).sum())
     assert bad == 0, (seed, N, M, cfg["formula"], bad)
     assert oe.mean() > 20
+
+
+def test_set_cursor_resumes_the_stream(smc):
+    """smc_set_cursor (checkpoint / resume): [0, n) in two resumed halves equals
+    one run of n, and a Fig. 2 loop driven round by round through smc_run from a fresh
+    model per round (the chunked C5 Wilson-stop driver's pattern) equals smc_estimate."""
+    cfg = workloads.c2()
+    m, p = _pair(smc, cfg, variant=0)
+    whole = m.run(p, 6000, 2)
+    m2, p2 = _pair(smc, cfg, variant=0)
+    a = m2.run(p2, 2500, 2)
+    m3, p3 = _pair(smc, cfg, variant=0)
+    m3.set_cursor(2500, 2)
+    b = m3.run(p3, 3500, 2)
+    assert {k: a[k] + b[k] for k in a} == whole
+    # Fig. 2 by hand, one fresh model per round, resumed by cursor
+    conf, eps = 0.99, 0.01
+    n_tot = yes = cursor = rounds = 0
+    N = smc.smc_wilson_sample_size(1.0, eps, conf)
+    while True:
+        mr, pr = _pair(smc, cfg, variant=0)
+        mr.set_cursor(cursor, 7)
+        c = mr.run(pr, N, 7)
+        cursor += N
+        n_tot += c["n_true"] + c["n_false"]
+        yes += c["n_true"]
+        rounds += 1
+        ph = yes / n_tot
+        n_new = smc.smc_wilson_sample_size(ph + eps if ph <= 0.5 else ph - eps, eps, conf) - n_tot
+        if n_new <= 0:
+            break
+        N = n_new
+    me, pe = _pair(smc, cfg, variant=0)
+    est = smc.estimate(me, pe, conf, eps, 7)
+    assert (est["n_total"], est["n_true"], est["rounds"]) == (n_tot, yes, rounds)
+    assert (est["lower"], est["upper"]) == smc.smc_wilson_interval(yes, n_tot, conf)

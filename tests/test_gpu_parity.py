@@ -505,25 +505,6 @@ def _iso_cfg():
                 formula="", t_max=0.0, seed=5, sampling=dict(mode="fixed", n=2000))
 
 
-def _literal_gpu_events(cfg, formula, t_max, seed, first, oe):
-    """The oracle's literal mode returns the exact first index k* at which the observed prefix
-    decides |=.  The literal GPU variant (reading R24) tests the prefix only at the
-    checkpoints k = 64, 128, 256, ... below the horizon step, so its event count is the first
-    checkpoint >= k* when that lies below the horizon entry count n, else n.  This mapping is
-    the kernel's design choice and lives here, not in the oracle."""
-    om = O.OracleModel(cfg)
-    of = O.OracleFormula(formula, cfg["species"], t_max)
-    H = t_max if t_max > 0 else of.reach
-    out = np.array(oe, np.int64)
-    for q, k in enumerate(oe):
-        n = len(om.simulate(seed, first + q, H)["t"]) - 1
-        cp = 64
-        while cp < k:
-            cp *= 2
-        out[q] = cp if cp < n else n
-    return out
-
-
 NESTED = [("iso", "F[0,3](A <= 5 & G[0,0.5](B >= 4))"), ("iso", "G[0,1.5](!(A < 7) | F[0.2,1](B <= 3))"),
           ("iso", "F[0.5,3](X[0,0.3](A == 6))"), ("iso", "F[0,3](G[0.2,0.6](A > 4))"),
           ("iso", "(F[0,1](B > 3)) U[0,3] (A < 5)"), ("iso", "!F[0,1](A == 7) | G[0,0.5](X[0,0.2](B > 2))"),
@@ -548,7 +529,6 @@ def test_nested_formulas_literal_variant_vs_oracle(smc, case):
     om = O.OracleModel(cfg)
     of = O.OracleFormula(f, cfg["species"], t_max)
     oc, ov, oe = O.run(om, of, 5, 0, 2000, mode="literal")
-    oe = _literal_gpu_events(cfg, f, t_max, 5, 0, oe)
     assert float(((v == ov) & (e == oe)).mean()) == 1.0, (f, float((v == ov).mean()), float((e == oe).mean()))
 
 
@@ -565,7 +545,6 @@ def test_nested_formulas_tile_recording_monitor_vs_oracle(smc, case):
     v, e = v.cpu().numpy(), e.cpu().numpy().astype(np.int64)
     assert m.last_launch(p)["variant"] == 2
     oc, ov, oe = O.run(O.OracleModel(cfg), O.OracleFormula(f, cfg["species"], t_max), 5, 0, 1000, mode="literal")
-    oe = _literal_gpu_events(cfg, f, t_max, 5, 0, oe)
     assert float(((v == ov) & (e == oe)).mean()) == 1.0, (f, float((v == ov).mean()), float((e == oe).mean()))
 
 
@@ -578,7 +557,6 @@ def test_nested_formula_on_c4_tile_vs_oracle(smc):
     v, e = v.cpu().numpy(), e.cpu().numpy().astype(np.int64)
     assert m.last_launch(p)["variant"] == 2
     oc, ov, oe = O.run(O.OracleModel(cfg), O.OracleFormula(f, cfg["species"]), 4, 0, 40, mode="literal")
-    oe = _literal_gpu_events(cfg, f, 0.0, 4, 0, oe)
     assert int(((v != ov) | (e != oe)).sum()) == 0
 
 
@@ -635,8 +613,6 @@ def test_random_models_and_formulas_vs_oracle(smc, seed):
     of = O.OracleFormula(cfg["formula"], cfg["species"])
     mode = "stream" if of.streamable else "literal"
     oc, ov, oe = O.run(O.OracleModel(cfg), of, seed, 0, 400, mode=mode)
-    if mode == "literal":
-        oe = _literal_gpu_events(cfg, cfg["formula"], 0.0, seed, 0, oe)
     for variant in (1, 2, 4):
         m, p = _pair(smc, cfg, variant)
         v, e = m.run_verdicts(p, 0, 400, seed)
