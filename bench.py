@@ -206,6 +206,8 @@ def oracle_sample(cfg, budget_s, procs=None, first_chunk=None):
     from oracle import wilson_procedure
     procs = procs or os.cpu_count() or 1
     samp = cfg["sampling"]
+    # formulas outside the streaming fragment: the oracle's literal mode (same verdicts)
+    mode = "stream" if O.OracleFormula(cfg["formula"], cfg["species"], cfg.get("t_max", 0.0)).streamable else "literal"
     if samp["mode"] == "wilson" and len(cfg["reactions"]) <= 32:
         t0 = time.perf_counter()
         ev = tr = runs = 0
@@ -214,7 +216,7 @@ def oracle_sample(cfg, budget_s, procs=None, first_chunk=None):
             acc = dict(events=0, n=0)
 
             def batch(first, n):
-                c, _, _ = O.run_parallel(cfg, cfg["formula"], cfg["seed"], first, n, procs=procs,
+                c, _, _ = O.run_parallel(cfg, cfg["formula"], cfg["seed"], first, n, mode=mode, procs=procs,
                                          t_max=cfg.get("t_max", 0.0))
                 acc["events"] += c["events"]
                 acc["n"] += n
@@ -239,7 +241,7 @@ def oracle_sample(cfg, budget_s, procs=None, first_chunk=None):
         n = chunk if total_n is None else min(chunk, total_n - first)
         if n <= 0:
             break
-        c, _, _ = O.run_parallel(cfg, cfg["formula"], cfg["seed"], first, n, procs=procs,
+        c, _, _ = O.run_parallel(cfg, cfg["formula"], cfg["seed"], first, n, mode=mode, procs=procs,
                                  chunk=max(1, n // (procs * 2)), t_max=cfg.get("t_max", 0.0))
         for k in tot:
             tot[k] += c[k]
@@ -296,10 +298,14 @@ def main():
     ap.add_argument("--replicas", "--n", dest="n", type=int, default=0,
                     help="override fixed-N replica count (diagnostics; --replicas under torchrun)")
     ap.add_argument("--variant", type=int, default=0)
+    ap.add_argument("--formula", default=None,
+                    help="override the workload's formula (e.g. a nested one: the literal |= path)")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         relaunch_under_torchrun(args.gpus)
     cfg = bench_config(args.workload, args.impl)
+    if args.formula:
+        cfg = dict(cfg, formula=args.formula)
     if args.n:
         cfg = workloads.with_sampling(cfg, mode="fixed", n=args.n)
     if args.impl == "reference":
@@ -392,6 +398,7 @@ def main():
     achieved = sim_events * ipe / 32.0 / (tot_kernel_ms / 1e3) / 1e9
     achieved_counted = per_gpu_events * ipe / 32.0 / (tot_kernel_ms / 1e3) / 1e9
     kname = "smc_ssa_" + {1: "thread", 2: "tile", 3: "literal", 4: "sweep", 5: "delta"}[info["variant"]]
+    # (a nested formula on a tile model runs the tile kernel with the recording monitor)
     prof, traffic_src = measured_profile(cfg["name"], kname)
     traffic = prof["dram_bytes_per_launch"] if prof else None
     roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Gwarp-inst/s", "frac": achieved / peak,
