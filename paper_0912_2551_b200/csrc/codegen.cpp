@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <sstream>
 
 #include "smc_internal.hpp"
@@ -245,188 +246,90 @@ struct MonGen {
     }
 };
 
-// ------------------------------------------------- literal |= (variant 3) ---
-// smc_lit_mask(x): atom bit mask of a state; smc_lit_eval(): every subformula, children
-// first, at every buffered entry m, transcribing P:229-237 (three-valued, reading R4):
-// elapsed = tau_m + tau_{m+1} + ... (left to right), the next (unknown) entry of a
-// non-absorbed trace at elapsed + tau_n.
-std::string literal_code(const Property& P) {
+// ---------------------------------------- window monitor (literal |=, R23/R27) ---
+// The nodes of the formula reachable from the root, children before parents, with the time
+// (and, for root-level booleans, the number of positions) the root can reach through each
+// node: a node creates position m only while t_m <= tlim (relative slack 1e-6 covers the
+// rounding between entry times and the left-to-right elapsed sums, R27) and m < plim.
+struct WinNode {
+    LNode n;
+    int a = -1, b = -1, par = -1;
+    double tlim = 0.0;
+    long long plim = 1;
+};
+
+std::vector<WinNode> window_nodes(const Property& P) {
+    std::vector<int> order, remap(P.lnodes.size(), -1);
+    std::function<void(int)> post = [&](int i) {
+        const LNode& n = P.lnodes[(size_t)i];
+        if (n.a >= 0) post(n.a);
+        if (n.b >= 0) post(n.b);
+        remap[(size_t)i] = (int)order.size();
+        order.push_back(i);
+    };
+    post(P.lroot);
+    std::vector<WinNode> w(order.size());
+    for (size_t q = 0; q < order.size(); ++q) {
+        w[q].n = P.lnodes[(size_t)order[q]];
+        w[q].a = w[q].n.a >= 0 ? remap[(size_t)w[q].n.a] : -1;
+        w[q].b = w[q].n.b >= 0 ? remap[(size_t)w[q].n.b] : -1;
+    }
+    const double BIG = 1e300;
+    const long long PINF = 0x7fffffff;
+    w.back().tlim = 0.0;                     // the root: position 0 only
+    w.back().plim = 1;
+    for (int q = (int)w.size() - 1; q >= 0; --q) {
+        WinNode& x = w[(size_t)q];
+        for (int c : {x.a, x.b}) {
+            if (c < 0) continue;
+            WinNode& y = w[(size_t)c];
+            y.par = q;
+            const bool temporal = x.n.k == LNode::F || x.n.k == LNode::G || x.n.k == LNode::U;
+            if (temporal || x.n.k == LNode::X) {
+                y.tlim = (x.tlim >= BIG || !x.n.I.finite()) ? BIG : (x.tlim + x.n.I.hi) * (1.0 + 1e-6) + 1e-300;
+                y.plim = temporal ? PINF : std::min(PINF, x.plim + 1);
+            } else {
+                y.tlim = x.tlim;
+                y.plim = x.plim;
+            }
+        }
+    }
+    return w;
+}
+
+size_t win_bytes(const Property& P) {
+    const auto w = window_nodes(P);
+    size_t nt = 0;
+    for (auto& x : w) nt += (x.n.k == LNode::F || x.n.k == LNode::G || x.n.k == LNode::U) ? 1 : 0;
+    return 16 + 8 * w.size() + 32 * nt;
+}
+
+// smc_lit_mask(x): atom bit mask of a state; the node table of ssa_window.cuh
+std::string window_code(const Property& P) {
     std::ostringstream o;
     MonGen mg(P);
     o << "template <class XA> __device__ __forceinline__ unsigned smc_lit_mask(const XA& x) {\n    unsigned mk = 0u;\n";
     for (size_t i = 0; i < P.atoms.size(); ++i) o << "    if " << mg.atom((int)i) << " mk |= " << (1u << i) << "u;\n";
     o << "    return mk;\n}\n";
-    o << "__device__ __noinline__ int smc_lit_eval(const double* __restrict__ tb, const double* __restrict__ ub,\n"
-         "                                         const unsigned* __restrict__ mb, unsigned char* __restrict__ vb,\n"
-         "                                         long long n, bool absorbed, long long cap) {\n    (void)tb;\n";
-    for (size_t i = 0; i < P.lnodes.size(); ++i) {
-        const LNode& nd = P.lnodes[i];
-        o << "    {   // node " << i << "\n        unsigned char* V = vb + " << i << "LL * cap;\n";
-        const std::string A = "(vb + " + std::to_string(nd.a) + "LL * cap)";
-        const std::string B = "(vb + " + std::to_string(nd.b) + "LL * cap)";
-        switch (nd.k) {
-            case LNode::ATOM:
-                o << "        for (long long m = 0; m <= n; ++m) V[m] = (unsigned char)((mb[m] >> " << nd.atom << ") & 1u);\n";
-                break;
-            case LNode::TRUE_: o << "        for (long long m = 0; m <= n; ++m) V[m] = 1;\n"; break;
-            case LNode::FALSE_: o << "        for (long long m = 0; m <= n; ++m) V[m] = 0;\n"; break;
-            case LNode::NOT:
-                o << "        const unsigned char* Va = " << A << ";\n"
-                  << "        for (long long m = 0; m <= n; ++m) V[m] = (unsigned char)smc_knot(Va[m]);\n";
-                break;
-            case LNode::AND: case LNode::OR:
-                o << "        const unsigned char* Va = " << A << ";\n        const unsigned char* Vb = " << B << ";\n"
-                  << "        for (long long m = 0; m <= n; ++m) V[m] = (unsigned char)"
-                  << (nd.k == LNode::AND ? "smc_kand" : "smc_kor") << "(Va[m], Vb[m]);\n";
-                break;
-            case LNode::X:   // sigma |= X^I phi iff sigma^1 |= phi and delta(sigma,0) in I
-                o << "        const unsigned char* Va = " << A << ";\n"
-                  << "        for (long long m = 0; m <= n; ++m) {\n"
-                  << "            const double d = ub[m];\n"
-                  << "            if (m < n) V[m] = " << MonGen::contains(nd.I, "d") << " ? Va[m + 1] : 0;\n"
-                  << "            else V[m] = absorbed ? 0 : (" << MonGen::contains(nd.I, "d") << " ? 2 : 0);\n"
-                  << "        }\n";
-                break;
-            case LNode::U: case LNode::F: {   // P:235-236; F == tt U
-                const bool hasA = nd.k == LNode::U;
-                const std::string P2 = nd.k == LNode::U ? B : A;
-                if (hasA) o << "        const unsigned char* V1 = " << A << ";\n";
-                o << "        const unsigned char* V2 = " << P2 << ";\n"
-                  << "        for (long long m = 0; m <= n; ++m) {\n"
-                  << "            int res = 0, pre = 1;\n            double el = 0.0;\n            bool done = false;\n"
-                  << "            for (long long k = m; k <= n; ++k) {\n"
-                  << "                if (k > m) el = __dadd_rn(el, ub[k - 1]);\n"
-                  << "                if (" << MonGen::beyond(nd.I, "el") << ") { done = true; break; }\n"
-                  << "                if " << MonGen::contains(nd.I, "el") << " res = smc_kor(res, smc_kand(pre, V2[k]));\n"
-                  << "                if (res == 1) { done = true; break; }\n"
-                  << "                pre = smc_kand(pre, " << (hasA ? "V1[k]" : "1") << ");\n"
-                  << "                if (pre == 0) { done = true; break; }\n"
-                  << "            }\n"
-                  << "            if (!done && !absorbed) {\n"
-                  << "                const double tail = __dadd_rn(el, ub[n]);\n"
-                  << "                if (!(" << MonGen::beyond(nd.I, "tail") << ")) res = smc_kor(res, smc_kand(pre, 2));\n"
-                  << "            }\n"
-                  << "            V[m] = (unsigned char)res;\n"
-                  << "        }\n";
-                break;
-            }
-            case LNode::G:   // G == !F!
-                o << "        const unsigned char* Va = " << A << ";\n"
-                  << "        for (long long m = 0; m <= n; ++m) {\n"
-                  << "            int res = 0;\n            double el = 0.0;\n            bool done = false;\n"
-                  << "            for (long long k = m; k <= n; ++k) {\n"
-                  << "                if (k > m) el = __dadd_rn(el, ub[k - 1]);\n"
-                  << "                if (" << MonGen::beyond(nd.I, "el") << ") { done = true; break; }\n"
-                  << "                if " << MonGen::contains(nd.I, "el") << " res = smc_kor(res, smc_knot(Va[k]));\n"
-                  << "                if (res == 1) { done = true; break; }\n"
-                  << "            }\n"
-                  << "            if (!done && !absorbed) {\n"
-                  << "                const double tail = __dadd_rn(el, ub[n]);\n"
-                  << "                if (!(" << MonGen::beyond(nd.I, "tail") << ")) res = smc_kor(res, 2);\n"
-                  << "            }\n"
-                  << "            V[m] = (unsigned char)smc_knot(res);\n"
-                  << "        }\n";
-                break;
-        }
-        o << "    }\n";
+    const auto w = window_nodes(P);
+    o << "#define SMC_WIN_NODES " << w.size() << "\n#define SMC_WIN_ROOT " << w.size() - 1
+      << "\n#define SMC_WIN_PER_ENTRY " << win_bytes(P) << "\ntemplate <int I> struct SmcWN;\n";
+    size_t ost = 16 + 8 * w.size();
+    for (size_t i = 0; i < w.size(); ++i) {
+        const WinNode& x = w[i];
+        const bool temporal = x.n.k == LNode::F || x.n.k == LNode::G || x.n.k == LNode::U;
+        const bool fin = x.n.I.finite();
+        o << "template <> struct SmcWN<" << i << "> {   // " << (int)x.n.k << "\n"
+          << "    static constexpr int kind = " << (int)x.n.k << ", a = " << x.a << ", b = " << x.b
+          << ", atom = " << x.n.atom << ", par = " << x.par << ";\n"
+          << "    static constexpr double lo = " << dlit(x.n.I.lo) << ", hi = " << dlit(fin ? x.n.I.hi : 0.0)
+          << ", tlim = " << dlit(x.tlim) << ";\n"
+          << "    static constexpr bool lo_open = " << (x.n.I.lo_open ? "true" : "false")
+          << ", hi_open = " << (x.n.I.hi_open ? "true" : "false") << ", hi_inf = " << (fin ? "false" : "true") << ";\n"
+          << "    static constexpr int plim = " << x.plim << ";\n"
+          << "    static constexpr long long oq = " << 16 + 8 * i << ", ost = " << (temporal ? ost : 0) << ";\n};\n";
+        if (temporal) ost += 32;
     }
-    o << "    return vb[" << P.lroot << "LL * cap];\n}\n";
-    // the exact first decision index: the three-valued |= of the prefix is
-    // monotone in the prefix, so given prefix `hi` definite (value r) and prefix `lo`
-    // undecided (-1: none), bisection finds the first definite prefix in (lo, hi]
-    o << "__device__ __noinline__ long long smc_lit_first(const double* __restrict__ tb, const double* __restrict__ ub,\n"
-         "                                             const unsigned* __restrict__ mb, unsigned char* __restrict__ vb,\n"
-         "                                             long long lo, long long hi, long long cap, int& r) {\n"
-         "    while (hi - lo > 1) {\n"
-         "        const long long mid = lo + (hi - lo) / 2;\n"
-         "        const int v = smc_lit_eval(tb, ub, mb, vb, mid, false, cap);\n"
-         "        if (v != 2) { hi = mid; r = v; } else lo = mid;\n"
-         "    }\n"
-         "    return hi;\n}\n";
-    return o.str();
-}
-
-// Recording monitor (tile variant, formulas outside R16; reading R23): the same interface
-// as the template monitors; the tile's first lane buffers (t_k, tau_k, atom mask_k) of the
-// tile's replica and, once the trace passes the horizon or is absorbed, evaluates |= with
-// smc_lit_eval; the verdict reaches the other lanes by a shuffle (no shared writes).
-std::string recording_monitor(const Property& P) {
-    std::ostringstream o;
-    o << "struct SmcMon {   // recording monitor for: " << P.text << "\n"
-         "    double* tb; double* ub; unsigned* mb; unsigned char* vb; long long cap, last; int res;\n"
-         "    long long undecided, decided_at;   // longest prefix found undecided; first decision index\n"
-         "    unsigned tmask; int leader;   // the tile's lanes; the tile's first lane writes and evaluates\n"
-         "    __device__ __forceinline__ void bind(const SmcParams& Q, smc_u64 slot, unsigned mask, int lead) {\n"
-         "        cap = (long long)Q.lit_cap; tmask = mask; leader = lead;\n"
-         "        tb = Q.lit_t + slot * (smc_u64)cap; ub = Q.lit_tau + slot * (smc_u64)cap;\n"
-         "        mb = Q.lit_mask + slot * (smc_u64)cap; vb = Q.lit_val + slot * (smc_u64)cap * SMC_LIT_NODES;\n"
-         "    }\n"
-         "    __device__ __forceinline__ bool lead() const { return (int)(threadIdx.x & 31u) == leader; }\n"
-         "    __device__ __forceinline__ int eval(long long n, bool absorbed) {\n"
-         "        int r = 0;\n"
-         "        __syncwarp(tmask);                          // the leader's trace writes are visible\n"
-         "        if (lead()) r = smc_lit_eval(tb, ub, mb, vb, n, absorbed, cap) == 1 ? 1 : 0;\n"
-         "        return __shfl_sync(tmask, r, leader);\n"
-         "    }\n"
-         "    __device__ __forceinline__ int eval3(long long n) {   // three-valued |= on the prefix (R24)\n"
-         "        int r = 2;\n"
-         "        __syncwarp(tmask);\n"
-         "        if (lead()) r = smc_lit_eval(tb, ub, mb, vb, n, false, cap);\n"
-         "        return __shfl_sync(tmask, r, leader);\n"
-         "    }\n"
-         "    // exact first decision index (leader lane), broadcast with the value\n"
-         "    __device__ __forceinline__ int first(long long lo, long long hi, int r) {\n"
-         "        long long k = hi;\n"
-         "        __syncwarp(tmask);\n"
-         "        if (lead()) k = smc_lit_first(tb, ub, mb, vb, lo, hi, cap, r);\n"
-         "        r = __shfl_sync(tmask, r, leader);\n"
-         "        decided_at = (long long)__shfl_sync(tmask, (int)k, leader);\n"
-         "        return r;\n"
-         "    }\n"
-         "    __device__ __forceinline__ void init() { res = -1; last = 0; undecided = -1; decided_at = -1; }\n"
-         "    template <class XA> __device__ __forceinline__ void enter(smc_u32 k, double t, double tp, const XA& x) {\n"
-         "        (void)tp;\n"
-         "        if (res >= 0) return;\n"
-         "        if ((long long)k >= cap - 1) { res = 2; return; }   // trace buffer full: replica error\n"
-         "        const unsigned mk = smc_lit_mask(x);\n"
-         "        if (lead()) { tb[k] = t; mb[k] = mk; }\n"
-         "        last = (long long)k;\n"
-         "    }\n"
-         "    // at the end of the trace (horizon overshoot after entry n, or absorption at n): the\n"
-         "    // first definite proper prefix if any (P:291-294), else the whole trace with n events\n"
-         "    __device__ __forceinline__ void finish(long long n, bool absorbed) {\n"
-         "        if (n - 1 > undecided) {\n"
-         "            const int r = eval3(n - 1);\n"
-         "            if (r != 2) { res = first(undecided, n - 1, r); return; }\n"
-         "        }\n"
-         "        res = eval(n, absorbed);\n"
-         "        decided_at = n;\n"
-         "    }\n"
-         "    __device__ __forceinline__ void advance(smc_u32 k, double tn, double tau) {\n"
-         "        if (res >= 0) return;\n"
-         "        if (lead()) ub[k] = tau;\n"
-         "        if (tn > SMC_LIT_H) finish((long long)k, false);\n"
-         "        else if (k >= 64u && (k & (k - 1u)) == 0u) {   // checkpoint (R24): the prefix decides?\n"
-         "            const int r = eval3((long long)k);\n"
-         "            if (r != 2) res = first(undecided, (long long)k, r);   // then its first decision index\n"
-         "            else undecided = (long long)k;\n"
-         "        }\n"
-         "    }\n"
-         "    __device__ __forceinline__ void absorb() {\n"
-         "        if (res < 0) finish(last, true);\n"
-         "    }\n"
-         "    __device__ __forceinline__ long long events(long long k) const { return decided_at >= 0 ? decided_at : k; }\n"
-         "    // the event cap reached at entry k undecided: the prefix up to entry k - 1 may decide\n"
-         "    __device__ __forceinline__ int at_cap(long long k) {\n"
-         "        if (k - 1 > undecided) {\n"
-         "            const int r = eval3(k - 1);\n"
-         "            if (r != 2) return first(undecided, k - 1, r);\n"
-         "        }\n"
-         "        return 2;\n"
-         "    }\n"
-         "    __device__ __forceinline__ void timeout() {}\n"
-         "    __device__ __forceinline__ int verdict() const { return res; }\n"
-         "};\n";
     return o.str();
 }
 
@@ -1319,6 +1222,8 @@ TileLayout pack_tables(const Model& m, bool sweep) {
     return L;
 }
 
+size_t window_bytes_per_entry(const Property& p) { return win_bytes(p); }
+
 std::string generate_source(const Model& m, const Property& p, int variant, const TileLayout* tl) {
     std::ostringstream o;
     o << "// generated by libsmc codegen: model N=" << m.N << " M=" << m.M << ", variant " << variant << "\n";
@@ -1425,10 +1330,11 @@ std::string generate_source(const Model& m, const Property& p, int variant, cons
         o << "    }\n    return 0.0;\n}\n";
     }
     if (variant == 3) {
-        o << literal_code(p) << "\n" << embedded_source("ssa_literal.cuh") << "\n";
+        o << window_code(p) << "\n" << embedded_source("ssa_window.cuh") << "\n" << embedded_source("ssa_literal.cuh")
+          << "\n";
         return o.str();
     }
-    if (p.literal) o << literal_code(p) << "\n" << recording_monitor(p) << "\n";   // variant 2 only
+    if (p.literal) o << window_code(p) << "\n" << embedded_source("ssa_window.cuh") << "\n";   // variant 2 only
     else {
         bool xd = false;                // binary64 count arrays: variant 1 small models, sweep
         if (variant == 4) xd = tl->sw_xd;

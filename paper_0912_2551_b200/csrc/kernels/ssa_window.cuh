@@ -1,0 +1,428 @@
+// ssa_window.cuh -- the WINDOW MONITOR: on-the-fly literal |= for formulas
+// outside the streaming templates of reading R16 (arbitrary nesting, non-zero inner lower
+// bounds, X under F/G/U), with memory bounded by the formula's
+// windows instead of the trace (reading R27).
+//
+// Every subformula node is a stream that emits, in position order m = 0, 1, 2, ..., the
+// pair (v, r) of its value at sigma^m and the FIRST prefix index r at which that value is
+// definite in the three-valued semantics of a prefix (entries 0..n and the sojourn of
+// entry n, the future unknown; R24).  Values and r compose exactly (Kleene logic):
+//   atom / true / false at m: (bit, m);   NOT: (not v, r);
+//   AND: false at the min r of its false operands, true at the max r of both;  OR dual;
+//   X^I at m: tau_m in I ? the child's (v, r) at m+1 : (0, m);
+//   phi1 U^I phi2 at m: the OR over the terms k with elapsed(m, k) in I of
+//     (AND_{m<=j<k} phi1(j)) AND phi2(k) -- true at the min over true terms of
+//     max(r2(k), max_j r1(j)); false at max(n0, max over terms of their zero time), n0 =
+//     min(window close c, first prefix at which the AND is 0), c = the last k whose
+//     elapsed is not beyond I (elapsed(m, c+1) = elapsed(m, c) + tau_c is beyond);
+//   F^I phi = true U^I phi;  G^I phi = not F^I not phi.
+// elapsed(m, k) = tau_m + ... + tau_{k-1} left to right, exactly the oracle's sum, kept per
+// pending position.  A temporal node's pending positions all consume the child stream in
+// lock step (child position j updates every pending m <= j), so the state per position is
+// O(1) (elapsed, best true r, max zero r, the AND's state) and a position is final -- and
+// leaves the window -- once no later child value can change (v, r): a true term with r <=
+// j + 1 (later terms have r >= their position), the AND became 0, or the window closed.
+// The root's r is the replica's event count, identical to the oracle's exact
+// first decision index; the few events simulated until the root's r is known are not
+// counted (like speculative replicas).
+//
+// Memory per replica slot: W ring entries (W a power of two, per launch) of
+//   t_k, tau_k (8 + 8 B), one (v, r) queue per node (8 B), one 32-byte state per pending
+//   position of each temporal node;
+// a node only creates positions whose entry time is within the time the root can reach
+// through it (its `tlim`, the formula's reach along the path; `plim` positions for
+// root-level booleans), so the rings hold one window, not the trace.  A ring that would
+// overflow ends the replica as an error.
+//
+// Generated before this header (codegen.cpp window_code): SMC_WIN_NODES, SMC_WIN_ROOT,
+// SMC_WIN_PER_ENTRY, SMC_LIT_H, smc_lit_mask(x), and per node
+//   template <> struct SmcWN<i> { kind, a, b, atom, par, lo, hi, lo_open, hi_open, hi_inf,
+//                                 tlim, plim, oq, ost };
+// The same struct serves the thread-owned literal kernel (one lane per slot) and the tile
+// kernel (the TW lanes of a tile share a slot and split the pending positions).
+
+enum { SMC_WK_ATOM = 0, SMC_WK_TRUE, SMC_WK_FALSE, SMC_WK_NOT, SMC_WK_AND, SMC_WK_OR, SMC_WK_X, SMC_WK_U,
+       SMC_WK_F, SMC_WK_G };
+#define SMC_WINF 0x7fffffff
+
+struct SmcWSt {            // pending position of a temporal node (32 B)
+    double el;             // elapsed(m, j) over the consumed child positions
+    int tb;                // min r over true terms (SMC_WINF: none); once final: the result r
+    int zm;                // max zero time over the false terms (-1: none)
+    int p1;                // U: max r over the phi1 values (all 1 so far)
+    int pz;                // U: min r over the phi1 zeros (SMC_WINF: none)
+    int fl;                // bit 0 final, bits 1-2 value, bit 3 unknown term, bits 4-5 AND state
+    int pad;
+};
+
+template <int I> struct SmcWN;
+
+__device__ __forceinline__ smc_u64 smc_wpack(int v, int r) { return ((smc_u64)(unsigned)r << 2) | (smc_u64)v; }
+
+struct SmcMon {
+    char* S;                                   // this slot's rings
+    int W, msk;                                // ring entries (power of two)
+    int lane, nl;                              // this lane's index among the slot's nl lanes
+    unsigned gm;                               // the slot's lanes
+    int leader;
+    int qh[SMC_WIN_NODES], qt[SMC_WIN_NODES];  // output queue: consumed by the parent / emitted
+    int lo[SMC_WIN_NODES], hi[SMC_WIN_NODES];  // temporal: next position to emit / create; X: next
+    bool stop[SMC_WIN_NODES];                  // no more positions will be created
+    int ne;                                    // entries processed (positions 0 .. ne-1)
+    int ntau;                                  // sojourns known (tau_0 .. tau_{ntau-1})
+    bool pend;                                 // an entered entry not yet processed
+    unsigned pmask;
+    double pt;
+    int last;                                  // index of the last entered entry
+    int res, decided_at;
+    bool err;
+
+    __device__ __forceinline__ double* tt() const { return (double*)S; }
+    __device__ __forceinline__ double* tau() const { return (double*)(S + (long long)8 * W); }
+    template <int I> __device__ __forceinline__ smc_u64* q() const { return (smc_u64*)(S + (long long)SmcWN<I>::oq * W); }
+    template <int I> __device__ __forceinline__ SmcWSt* st() const { return (SmcWSt*)(S + (long long)SmcWN<I>::ost * W); }
+    __device__ __forceinline__ void sync() const { if (nl > 1) __syncwarp(gm); }
+
+    __device__ __forceinline__ void bind(const SmcParams& Q, smc_u64 slot, unsigned mask, int lead) {
+        W = (int)Q.lit_cap;
+        msk = W - 1;
+        S = (char*)Q.lit_t + slot * (smc_u64)W * (smc_u64)SMC_WIN_PER_ENTRY;
+        gm = mask;
+        leader = lead;
+        nl = __popc(mask);
+        lane = (int)(threadIdx.x & 31u) - lead;
+    }
+    __device__ __forceinline__ void init() {
+#pragma unroll
+        for (int i = 0; i < SMC_WIN_NODES; ++i) { qh[i] = qt[i] = lo[i] = hi[i] = 0; stop[i] = false; }
+        ne = ntau = 0;
+        pend = false;
+        last = 0;
+        res = -1;
+        decided_at = -1;
+        err = false;
+    }
+
+    template <int I> __device__ __forceinline__ static bool contains(double e) {
+        using D = SmcWN<I>;
+        const bool lo_ok = D::lo_open ? (e > D::lo) : (e >= D::lo);
+        if (D::hi_inf) return lo_ok;
+        return lo_ok && (D::hi_open ? (e < D::hi) : (e <= D::hi));
+    }
+    template <int I> __device__ __forceinline__ static bool beyond(double e) {
+        using D = SmcWN<I>;
+        if (D::hi_inf) return false;
+        return D::hi_open ? (e >= D::hi) : (e > D::hi);
+    }
+
+    // ---------------------------------------------------------------- queues
+    template <int I> __device__ __forceinline__ void emit(int v, int r) {
+        if (qt[I] - qh[I] >= W) { err = true; return; }
+        q<I>()[qt[I] & msk] = smc_wpack(v, r);            // every lane writes the same value
+        ++qt[I];
+    }
+    template <int C> __device__ __forceinline__ void peek(int p, int& v, int& r) const {
+        const smc_u64 e = q<C>()[p & msk];
+        v = (int)(e & 3ull);
+        r = (int)(e >> 2);
+    }
+    // node I will emit no more positions (stopped and drained into its queue)
+    template <int I> __device__ __forceinline__ bool ended() const {
+        using D = SmcWN<I>;
+        if constexpr (D::kind == SMC_WK_ATOM || D::kind == SMC_WK_TRUE || D::kind == SMC_WK_FALSE) return stop[I];
+        else if constexpr (D::kind == SMC_WK_X) return stop[I];
+        else if constexpr (D::kind == SMC_WK_F || D::kind == SMC_WK_G || D::kind == SMC_WK_U) return stop[I] && lo[I] == hi[I];
+        else if constexpr (D::kind == SMC_WK_NOT) return ended<D::a>() && qh[D::a] == qt[D::a];
+        else return (ended<D::a>() && qh[D::a] == qt[D::a]) || (ended<D::b>() && qh[D::b] == qt[D::b]);
+    }
+    // the parent of I consumes no more (it is done, or it is the root and the root is known)
+    template <int I> __device__ __forceinline__ bool dead() const {
+        using D = SmcWN<I>;
+        if constexpr (D::par < 0) return qt[I] > 0;
+        else return dead<D::par>() || ended<D::par>();
+    }
+
+    // ---------------------------------------------------------------- leaves
+    template <int I> __device__ __forceinline__ void leaf(int k, double t, unsigned mk) {
+        using D = SmcWN<I>;
+        if constexpr (D::kind == SMC_WK_ATOM || D::kind == SMC_WK_TRUE || D::kind == SMC_WK_FALSE) {
+            if (stop[I] || dead<I>()) return;
+            if (k >= D::plim || !(t <= D::tlim)) { stop[I] = true; return; }
+            const int v = D::kind == SMC_WK_ATOM ? (int)((mk >> D::atom) & 1u) : (D::kind == SMC_WK_TRUE ? 1 : 0);
+            emit<I>(v, k);                                 // an atom's value is known at its entry
+        }
+    }
+    template <int I> __device__ __forceinline__ void leaves(int k, double t, unsigned mk) {
+        if constexpr (I < SMC_WIN_NODES) { leaf<I>(k, t, mk); leaves<I + 1>(k, t, mk); }
+    }
+
+    // ---------------------------------------------------------------- temporal nodes
+    __device__ __forceinline__ static void tfinal(SmcWSt& s, int v, int r) {
+        s.tb = r;
+        s.fl = (s.fl & ~7) | 1 | (v << 1);
+    }
+    // the window of the position closed after term c (no later terms)
+    __device__ __forceinline__ static void tclose(SmcWSt& s, int c) {
+        const int pv = (s.fl >> 4) & 3;
+        if (s.tb != SMC_WINF) tfinal(s, 1, s.tb);
+        else if (s.fl & 8) tfinal(s, 2, SMC_WINF);
+        else tfinal(s, 0, max(pv == 0 ? min(c, s.pz) : c, s.zm));
+    }
+    // position m consumes child position j (the term j and the AND's operand j)
+    template <int I> __device__ __forceinline__ void tstep(SmcWSt& s, int m, int j, double tj, int v1, int r1, int v2,
+                                                           int r2) const {
+        using D = SmcWN<I>;
+        if (m < j) {
+            s.el = __dadd_rn(s.el, tj);                   // elapsed(m, j), left to right
+            if (beyond<I>(s.el)) { tclose(s, j - 1); return; }
+        }
+        int pv = (s.fl >> 4) & 3;
+        if (contains<I>(s.el)) {
+            if (pv == 0 || v2 == 0) s.zm = max(s.zm, min(pv == 0 ? s.pz : SMC_WINF, v2 == 0 ? r2 : SMC_WINF));
+            else if (pv == 1 && v2 == 1) s.tb = min(s.tb, max(s.p1, r2));
+            else s.fl |= 8;                               // an unknown term (end of trace only)
+        }
+        if constexpr (D::kind == SMC_WK_U) {
+            if (v1 == 0) { s.pz = min(s.pz, r1); pv = 0; }
+            else if (v1 == 1) { if (pv == 1) s.p1 = max(s.p1, r1); }
+            else if (pv == 1) pv = 2;
+            s.fl = (s.fl & ~0x30) | (pv << 4);
+        }
+        if (s.tb != SMC_WINF && (s.tb <= j + 1 || pv == 0)) tfinal(s, 1, s.tb);
+        else if (s.tb == SMC_WINF && !(s.fl & 8) && pv == 0 && s.pz <= j) tfinal(s, 0, max(s.pz, s.zm));
+    }
+    // the trace ended (or the child stream did) after child position jl: close or leave open
+    template <int I> __device__ __forceinline__ void tend(SmcWSt& s, int jl, bool fin, bool absorbed, int N) {
+        if (fin && absorbed && jl == N) { tclose(s, N); return; }     // no further entries (R7)
+        const double e2 = __dadd_rn(s.el, tau()[jl & msk]);
+        if (beyond<I>(e2)) { tclose(s, jl); return; }
+        if (!(fin && jl == N)) { err = true; return; }               // child ended inside the window
+        const int pv = (s.fl >> 4) & 3;                              // the future term is unknown
+        if (s.tb != SMC_WINF) tfinal(s, 1, s.tb);
+        else if (pv == 0 && !(s.fl & 8)) tfinal(s, 0, max(s.pz, s.zm));
+        else tfinal(s, 2, SMC_WINF);
+    }
+    template <int I> __device__ __forceinline__ void temit() {
+        using D = SmcWN<I>;
+        SmcWSt* ST = st<I>();
+        while (lo[I] < hi[I]) {
+            const int f = ST[lo[I] & msk].fl;
+            if (!(f & 1)) break;
+            int v = (f >> 1) & 3;
+            if (D::kind == SMC_WK_G && v != 2) v = 1 - v;   // G = not F not
+            emit<I>(v, ST[lo[I] & msk].tb);
+            ++lo[I];
+        }
+    }
+    template <int I> __device__ __forceinline__ void temporal(bool fin, bool absorbed, int N) {
+        using D = SmcWN<I>;
+        constexpr int A = D::a;
+        constexpr int B = D::kind == SMC_WK_U ? D::b : D::a;
+        SmcWSt* ST = st<I>();
+        for (;;) {
+            const int j = qh[B];
+            if (qh[B] >= qt[B] || (D::kind == SMC_WK_U && qh[A] >= qt[A])) break;
+            int v1 = 1, r1 = -1, v2, r2;
+            peek<B>(j, v2, r2);
+            if constexpr (D::kind == SMC_WK_U) peek<A>(j, v1, r1);
+            if constexpr (D::kind == SMC_WK_G) { if (v2 != 2) v2 = 1 - v2; }
+            if (!stop[I]) {                                   // position j of this node
+                if (j < D::plim && tt()[j & msk] <= D::tlim) {
+                    if (hi[I] - lo[I] >= W) { err = true; return; }
+                    hi[I] = j + 1;
+                } else {
+                    stop[I] = true;
+                }
+            }
+            const double tj = j > 0 ? tau()[(j - 1) & msk] : 0.0;
+            for (int m = lo[I] + lane; m < hi[I]; m += nl) {
+                SmcWSt s;
+                if (m == j) { s.el = 0.0; s.tb = SMC_WINF; s.zm = -1; s.p1 = -1; s.pz = SMC_WINF; s.fl = 1 << 4; s.pad = 0; }
+                else {
+                    s = ST[m & msk];
+                    if (s.fl & 1) continue;
+                }
+                tstep<I>(s, m, j, tj, v1, r1, v2, r2);
+                ST[m & msk] = s;
+            }
+            ++qh[B];
+            if constexpr (D::kind == SMC_WK_U) ++qh[A];
+            sync();
+            temit<I>();
+        }
+        const bool cend = ended<B>() && qh[B] == qt[B] && (D::kind != SMC_WK_U || (ended<A>() && qh[A] == qt[A]));
+        if (fin || cend) {                                    // no more child positions
+            stop[I] = true;
+            if (lo[I] < hi[I]) {
+                const int jl = qh[B] - 1;
+                for (int m = lo[I] + lane; m < hi[I]; m += nl) {
+                    SmcWSt s = ST[m & msk];
+                    if (s.fl & 1) continue;
+                    tend<I>(s, jl, fin, absorbed, N);
+                    ST[m & msk] = s;
+                }
+                sync();
+                temit<I>();
+            }
+        }
+    }
+
+    // ---------------------------------------------------------------- X, booleans
+    template <int I> __device__ __forceinline__ void xnode(bool fin, bool absorbed, int N) {
+        using D = SmcWN<I>;
+        constexpr int A = D::a;
+        while (!stop[I]) {
+            const int m = lo[I];
+            if (m >= ne) break;                               // entry m not processed yet
+            if (m >= D::plim || !(tt()[m & msk] <= D::tlim)) { stop[I] = true; break; }
+            int v = 0, r = m;
+            if (fin && m == N) {                              // the last entry
+                if (absorbed) { v = 0; r = N; }
+                else if (contains<I>(tau()[m & msk])) { v = 2; r = SMC_WINF; }
+            } else {
+                if (m >= ntau) break;                         // tau_m not drawn yet
+                if (contains<I>(tau()[m & msk])) {            // sigma^1 |= phi and delta(sigma, 0) in I
+                    while (qh[A] < m + 1 && qh[A] < qt[A]) ++qh[A];
+                    if (qh[A] == m + 1 && qh[A] < qt[A]) { peek<A>(m + 1, v, r); ++qh[A]; }
+                    else if (ended<A>()) { err = true; return; }
+                    else break;
+                }
+            }
+            emit<I>(v, r);
+            ++lo[I];
+            if (fin && m == N) stop[I] = true;
+        }
+        if (fin) stop[I] = true;
+    }
+    template <int I> __device__ __forceinline__ void boolean() {
+        using D = SmcWN<I>;
+        constexpr int A = D::a;
+        if constexpr (D::kind == SMC_WK_NOT) {
+            while (qh[A] < qt[A]) {
+                int v, r;
+                peek<A>(qh[A], v, r);
+                ++qh[A];
+                emit<I>(v == 2 ? 2 : 1 - v, r);
+            }
+        } else {
+            constexpr int B = D::b;
+            while (qh[A] < qt[A] && qh[B] < qt[B]) {
+                int va, ra, vb, rb;
+                peek<A>(qh[A], va, ra);
+                peek<B>(qh[B], vb, rb);
+                ++qh[A];
+                ++qh[B];
+                if (D::kind == SMC_WK_OR) {                   // OR = not (not a and not b)
+                    va = va == 2 ? 2 : 1 - va;
+                    vb = vb == 2 ? 2 : 1 - vb;
+                }
+                int v, r;
+                if (va == 0 && vb == 0) { v = 0; r = min(ra, rb); }
+                else if (va == 0) { v = 0; r = ra; }
+                else if (vb == 0) { v = 0; r = rb; }
+                else if (va == 1 && vb == 1) { v = 1; r = max(ra, rb); }
+                else { v = 2; r = SMC_WINF; }
+                if (D::kind == SMC_WK_OR && v != 2) v = 1 - v;
+                emit<I>(v, r);
+            }
+        }
+    }
+
+    template <int I> __device__ __forceinline__ void pump_node(bool fin, bool absorbed, int N) {
+        using D = SmcWN<I>;
+        if (err || dead<I>()) return;
+        if constexpr (D::kind == SMC_WK_F || D::kind == SMC_WK_G || D::kind == SMC_WK_U) temporal<I>(fin, absorbed, N);
+        else if constexpr (D::kind == SMC_WK_X) xnode<I>(fin, absorbed, N);
+        else if constexpr (D::kind == SMC_WK_NOT || D::kind == SMC_WK_AND || D::kind == SMC_WK_OR) boolean<I>();
+    }
+    template <int I> __device__ __forceinline__ void pump_from(bool fin, bool absorbed, int N) {
+        if constexpr (I < SMC_WIN_NODES) { pump_node<I>(fin, absorbed, N); pump_from<I + 1>(fin, absorbed, N); }
+    }
+    // oldest ring index still needed (tau_{j-1} / t_j of the next child position of each
+    // temporal node, tau_m / t_m of each X node's next position)
+    template <int I> __device__ __forceinline__ int ring_lo(int lo_) const {
+        if constexpr (I < SMC_WIN_NODES) {
+            using D = SmcWN<I>;
+            int l = lo_;
+            if constexpr (D::kind == SMC_WK_F || D::kind == SMC_WK_G || D::kind == SMC_WK_U) {
+                constexpr int B = D::kind == SMC_WK_U ? D::b : D::a;
+                if (!(stop[I] && lo[I] == hi[I]) && !dead<I>()) l = min(l, qh[B] - 1);
+            } else if constexpr (D::kind == SMC_WK_X) {
+                if (!stop[I] && !dead<I>()) l = min(l, lo[I]);
+            }
+            return ring_lo<I + 1>(l);
+        } else {
+            return lo_;
+        }
+    }
+    __device__ __forceinline__ void ring_put(double* a, int k, double v) {
+        if (k - ring_lo<0>(k) >= W) { err = true; return; }
+        a[k & msk] = v;                                   // every lane writes the same value
+    }
+    __device__ __forceinline__ void result() {
+        if (err) { res = 2; return; }
+        if (qt[SMC_WIN_ROOT] > 0) {
+            int v, r;
+            peek<SMC_WIN_ROOT>(0, v, r);
+            if (v != 2) { res = v; decided_at = r; }
+        }
+    }
+    // process the entered entry: leaves emit its position, every node consumes what it can
+    __device__ __forceinline__ void process_pending() {
+        if (!pend) return;
+        pend = false;
+        ring_put(tt(), last, pt);
+        ne = last + 1;
+        if (err) return;
+        leaves<0>(last, pt, pmask);
+    }
+
+    // ---------------------------------------------------------------- monitor interface
+    template <class XA> __device__ __forceinline__ void enter(smc_u32 k, double t, double tp, const XA& x) {
+        (void)tp;
+        if (res >= 0) return;
+        pend = true;
+        pmask = smc_lit_mask(x);
+        pt = t;
+        last = (int)k;
+    }
+    // the trace ends after entry N (prefix N, sojourn tau_N known unless absorbed)
+    __device__ __forceinline__ void finish(int N, bool absorbed) {
+        if (!err) pump_from<0>(true, absorbed, N);
+        if (err) { res = 2; return; }
+        int v = 2, r = N;
+        if (qt[SMC_WIN_ROOT] > 0) peek<SMC_WIN_ROOT>(0, v, r);
+        if (v == 2) { res = 0; decided_at = N; }          // unknown -> false at the root (R4)
+        else { res = v; decided_at = r; }
+    }
+    __device__ __forceinline__ void advance(smc_u32 k, double tn, double tj) {
+        if (res >= 0) return;
+        process_pending();
+        ring_put(tau(), (int)k, tj);
+        ntau = (int)k + 1;
+        if (!err) pump_from<0>(false, false, 0);
+        result();
+        if (res < 0 && tn > SMC_LIT_H) finish((int)k, false);   // the trace covers the horizon
+    }
+    __device__ __forceinline__ void absorb() {
+        if (res >= 0) return;
+        process_pending();
+        if (!err) pump_from<0>(false, false, 0);
+        result();
+        if (res < 0) finish(last, true);
+    }
+    // the event cap reached at entry k (entered, not processed): the prefix up to entry k - 1
+    // decides, else the replica is an error
+    __device__ __forceinline__ int at_cap(long long k) {
+        pend = false;
+        if (!err) pump_from<0>(true, false, (int)k - 1);
+        int v = 2, r = 0;
+        if (!err && qt[SMC_WIN_ROOT] > 0) peek<SMC_WIN_ROOT>(0, v, r);
+        if (v == 2) return 2;
+        decided_at = r;
+        return v;
+    }
+    __device__ __forceinline__ void timeout() {}
+    __device__ __forceinline__ int verdict() const { return res; }
+    __device__ __forceinline__ long long events(long long k) const { return decided_at >= 0 ? decided_at : k; }
+};

@@ -100,15 +100,11 @@ struct PropKernel {
     const void* tables = nullptr;
     bool timing_pending = false;
     int per_warp = 1;                      // trajectories per warp (variant 2)
-    // variant 3 (literal |=): per-thread trace buffers
-    double* lit_t = nullptr;
-    double* lit_tau = nullptr;
-    unsigned* lit_mask = nullptr;
-    unsigned char* lit_val = nullptr;
-    unsigned long long lit_cap = 0;        // entries per replica slot of the current launch
+    // window monitor (formulas outside the streaming templates, R27): per-slot rings
+    double* lit_t = nullptr;               // all slots' rings
+    unsigned long long lit_cap = 0;        // ring entries per replica slot of the current launch
     size_t lit_entries = 0, lit_per_entry = 0;
-    int lit_per_cta = 0;                   // replicas per CTA (0: not a literal kernel)
-    size_t lit_nodes = 0;                  // subformula nodes of the literal |=
+    int lit_per_cta = 0;                   // replica slots per CTA (0: no window monitor)
     smc_launch_info info{};
     uint64_t cap_global = 0;               // sum of capacity() over the ranks (one allreduce)
     uint64_t capacity() const {            // trajectories resident at once on this GPU
@@ -141,9 +137,6 @@ struct DeviceState {
     ~DeviceState() {
         for (auto& kv : kernels) {
             dfree(kv.second.lit_t);
-            dfree(kv.second.lit_tau);
-            dfree(kv.second.lit_mask);
-            dfree(kv.second.lit_val);
         }
         if (e0) cudaEventDestroy(e0);
         if (e1) cudaEventDestroy(e1);
@@ -190,40 +183,36 @@ DeviceState& device(Model& m) {
     return *m.dev;
 }
 
-// Trace buffers of the literal |= (reading R23), sized PER LAUNCH: the `grid` CTAs of this
-// launch hold `per_cta` replicas each, and every resident replica gets an equal share of the
-// budget (a quarter of the free device memory, at most 16 GiB per property) up to the event
-// cap (<= 2^24 entries).  A small batch (e.g. 2,000 replicas) therefore gets long traces --
-// full horizons of C3 / C4 -- while a machine-filling batch gets >= 4096 entries per replica
-// (fewer resident CTAs if needed).  The buffers grow when a launch needs more entries.
+// Rings of the window monitor (ssa_window.cuh, readings R23/R27), sized PER LAUNCH: every
+// replica slot of the `grid` CTAs (`per_cta` slots each) gets W ring entries of
+// `lit_per_entry` bytes, W the largest power of two up to SMC_WIN_W (default 4096) within the
+// budget (a third of the free device memory, at most 48 GiB); a launch that cannot give
+// every slot 1024 entries runs fewer resident CTAs.  The rings hold the formula's windows
+// (not the trace), so W bounds how many entries one window may span; a replica whose window
+// would overflow its ring ends as an error.
 void size_traces(Model& m, PropKernel& pk, int per_cta, int& grid) {
+    (void)m;
     size_t free_b = 0, total_b = 0;
     ck(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
     const size_t held = (size_t)pk.lit_entries * pk.lit_per_entry;   // ours, reusable
-    const size_t budget = std::min<size_t>((free_b + held) / 4, (size_t)16 << 30);
-    const size_t per_entry = 8 + 8 + 4 + pk.lit_nodes;
-    const size_t want_cap = (size_t)std::min<uint64_t>(m.event_cap + 2, 1ull << 24);
-    const size_t min_cap = std::min<size_t>(want_cap, 4096);
+    const size_t budget = std::min<size_t>((free_b + held) / 3, (size_t)48 << 30);
+    const size_t per_entry = pk.lit_per_entry;
+    size_t want = 4096;
+    if (const char* e = std::getenv("SMC_WIN_W")) want = std::max<size_t>(16, std::strtoull(e, nullptr, 10));
+    const size_t min_cap = std::min<size_t>(want, 1024);
     if (budget / ((size_t)grid * (size_t)per_cta * per_entry) < min_cap)
         grid = (int)std::max<size_t>(1, budget / (min_cap * per_entry * (size_t)per_cta));
     const size_t slots = (size_t)grid * (size_t)per_cta;
-    const size_t cap = std::min<size_t>(budget / (slots * per_entry), want_cap);
-    if (cap < 16) fail(SMC_E_CUDA, "literal |=: not enough device memory for trace buffers");
-    if (slots * cap > pk.lit_entries || per_entry != pk.lit_per_entry) {
+    size_t lim = std::min<size_t>(budget / (slots * per_entry), want);
+    size_t cap = 1;
+    while (cap * 2 <= lim) cap *= 2;
+    if (cap < 16) fail(SMC_E_CUDA, "window monitor: not enough device memory for the rings");
+    if (slots * cap > pk.lit_entries) {
         dfree(pk.lit_t);
-        dfree(pk.lit_tau);
-        dfree(pk.lit_mask);
-        dfree(pk.lit_val);
-        pk.lit_t = pk.lit_tau = nullptr;
-        pk.lit_mask = nullptr;
-        pk.lit_val = nullptr;
+        pk.lit_t = nullptr;
         pk.lit_entries = 0;
-        pk.lit_t = (double*)dalloc(slots * cap * 8);
-        pk.lit_tau = (double*)dalloc(slots * cap * 8);
-        pk.lit_mask = (unsigned*)dalloc(slots * cap * 4);
-        pk.lit_val = (unsigned char*)dalloc(slots * cap * pk.lit_nodes);
+        pk.lit_t = (double*)dalloc(slots * cap * per_entry);
         pk.lit_entries = slots * cap;
-        pk.lit_per_entry = per_entry;
     }
     pk.lit_cap = cap;
 }
@@ -286,8 +275,8 @@ PropKernel& prepare(Model& m, const Property& p) {
         ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, pk.block, 0), "occupancy");
         pk.grid_max = std::max(1, nb) * d.sm_count;
         pk.smem = 0;
-        pk.lit_per_cta = pk.block;          // buffers sized per launch (size_traces)
-        pk.lit_nodes = p.lnodes.size();
+        pk.lit_per_cta = pk.block;          // rings sized per launch (size_traces)
+        pk.lit_per_entry = window_bytes_per_entry(p);
     } else if (pk.variant == 4) {
         pk.block = tl->sw_blk;
         pk.smem = (int)(tl->bytes + (size_t)pk.block * (tl->sw_xd ? 8 : 4) * (size_t)(m.N + 1));
@@ -347,9 +336,9 @@ PropKernel& prepare(Model& m, const Property& p) {
         pk.smem = (int)(tl->bytes + (size_t)best_w * wb);
         pk.grid_max = best_nb * d.sm_count;
         pk.per_warp = 32 / tl->tw;
-        if (p.literal) {                   // one trace per tile, sized per launch (size_traces)
+        if (p.literal) {                   // one ring slot per tile, sized per launch (size_traces)
             pk.lit_per_cta = best_w * pk.per_warp;
-            pk.lit_nodes = p.lnodes.size();
+            pk.lit_per_entry = window_bytes_per_entry(p);
         }
     }
     pk.info.variant = pk.variant;
@@ -386,7 +375,7 @@ void launch_slice(Model& m, PropKernel& pk, uint64_t seed, uint64_t lo, uint64_t
         unsigned long long lit_cap;
     } P{seed, lo, count, spec ? d.spec_cursor() : (unsigned long long*)d.ctl,
         (long long*)(spec ? d.spec_scratch() : d.counters()), dev_verdict, dev_events, m.event_cap, pk.tables,
-        pk.lit_t, pk.lit_tau, pk.lit_mask, pk.lit_val, pk.lit_cap};
+        pk.lit_t, nullptr, nullptr, nullptr, pk.lit_cap};
     // thread and sweep variants, slice smaller than the resident capacity: one CTA per SM with just
     // enough warps for the slice (the compiled CTA size is an upper bound), so a small
     // batch spreads over every SM instead of filling a few
@@ -402,9 +391,6 @@ void launch_slice(Model& m, PropKernel& pk, uint64_t seed, uint64_t lo, uint64_t
     if (pk.lit_per_cta) {                  // literal |=: this launch's trace buffers
         size_traces(m, pk, pk.lit_per_cta, grid);
         P.lit_t = pk.lit_t;
-        P.lit_tau = pk.lit_tau;
-        P.lit_mask = pk.lit_mask;
-        P.lit_val = pk.lit_val;
         P.lit_cap = pk.lit_cap;
     }
     void* args[] = {&P};

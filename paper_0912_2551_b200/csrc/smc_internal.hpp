@@ -184,6 +184,8 @@ struct HillTables {
 };
 HillTables pack_hill_tables(const Model& m);
 std::string generate_source(const Model& m, const Property& p, int variant, const TileLayout* tl);
+// bytes per ring entry of one replica slot of the window monitor (ssa_window.cuh, R27)
+size_t window_bytes_per_entry(const Property& p);
 std::string embedded_source(const char* name);   // kernels/*.cuh embedded at build time
 
 // -------------------------------------------------------------------- jit ---

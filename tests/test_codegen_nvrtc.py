@@ -47,4 +47,4 @@ def test_literal_variant_compiles():
 
 def test_tile_recording_monitor_compiles():
     src, _ = _compile(workloads.c4(), 0, "F[0,0.3](S0 < S1 + 3 & G[0.01,0.04](S0 < S1 + 3))")
-    assert "smc_ssa_tile" in src and "recording monitor" in src
+    assert "smc_ssa_tile" in src and "struct SmcMon" in src and "SmcWN<" in src

@@ -516,7 +516,7 @@ NESTED = [("iso", "F[0,3](A <= 5 & G[0,0.5](B >= 4))"), ("iso", "G[0,1.5](!(A < 
 def test_nested_formulas_literal_variant_vs_oracle(smc, case):
     """NEXT-2: formulas outside the streaming templates (nested temporal operators, non-zero
     inner lower bounds, X inside F, unbounded with t_max) run through the literal variant
-    (buffered trace + |= on the device) and equal the oracle's literal mode replica for
+    (the window monitor on the device, R27) and equal the oracle's literal mode replica for
     replica, verdicts and event counts."""
     name, f = NESTED[case]
     cfg = dict(_iso_cfg() if name == "iso" else workloads.c2(), formula=f)
@@ -534,7 +534,7 @@ def test_nested_formulas_literal_variant_vs_oracle(smc, case):
 
 @pytest.mark.parametrize("case", range(len(NESTED)))
 def test_nested_formulas_tile_recording_monitor_vs_oracle(smc, case):
-    """NEXT-2 in the tile kernel (recording monitor, reading R23): the NESTED formulas with
+    """NEXT-2 in the tile kernel (window monitor, readings R23/R27): the NESTED formulas with
     the models forced to variant 2 equal the oracle's literal mode replica for replica."""
     name, f = NESTED[case]
     cfg = dict(_iso_cfg() if name == "iso" else workloads.c2(), formula=f)
