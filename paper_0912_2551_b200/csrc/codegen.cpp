@@ -301,7 +301,7 @@ size_t win_bytes(const Property& P) {
     const auto w = window_nodes(P);
     size_t nt = 0;
     for (auto& x : w) nt += (x.n.k == LNode::F || x.n.k == LNode::G || x.n.k == LNode::U) ? 1 : 0;
-    return 16 + 8 * w.size() + 32 * nt;
+    return 16 + 8 * w.size() + 40 * nt;
 }
 
 // smc_lit_mask(x): atom bit mask of a state; the node table of ssa_window.cuh
@@ -314,7 +314,9 @@ std::string window_code(const Property& P) {
     const auto w = window_nodes(P);
     o << "#define SMC_WIN_NODES " << w.size() << "\n#define SMC_WIN_ROOT " << w.size() - 1
       << "\n#define SMC_WIN_PER_ENTRY " << win_bytes(P) << "\ntemplate <int I> struct SmcWN;\n";
-    size_t ost = 16 + 8 * w.size();
+    size_t nt = 0;
+    for (auto& x : w) nt += (x.n.k == LNode::F || x.n.k == LNode::G || x.n.k == LNode::U) ? 1 : 0;
+    size_t oel = 16 + 8 * w.size(), ost = oel + 8 * nt;   // elapsed arrays, then 32-byte states
     for (size_t i = 0; i < w.size(); ++i) {
         const WinNode& x = w[i];
         const bool temporal = x.n.k == LNode::F || x.n.k == LNode::G || x.n.k == LNode::U;
@@ -327,8 +329,9 @@ std::string window_code(const Property& P) {
           << "    static constexpr bool lo_open = " << (x.n.I.lo_open ? "true" : "false")
           << ", hi_open = " << (x.n.I.hi_open ? "true" : "false") << ", hi_inf = " << (fin ? "false" : "true") << ";\n"
           << "    static constexpr int plim = " << x.plim << ";\n"
-          << "    static constexpr long long oq = " << 16 + 8 * i << ", ost = " << (temporal ? ost : 0) << ";\n};\n";
-        if (temporal) ost += 32;
+          << "    static constexpr long long oq = " << 16 + 8 * i << ", oel = " << (temporal ? oel : 0)
+          << ", ost = " << (temporal ? ost : 0) << ";\n};\n";
+        if (temporal) { oel += 8; ost += 32; }
     }
     return o.str();
 }

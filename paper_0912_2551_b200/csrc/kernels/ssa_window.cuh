@@ -45,15 +45,17 @@ enum { SMC_WK_ATOM = 0, SMC_WK_TRUE, SMC_WK_FALSE, SMC_WK_NOT, SMC_WK_AND, SMC_W
        SMC_WK_F, SMC_WK_G };
 #define SMC_WINF 0x7fffffff
 
-struct SmcWSt {            // pending position of a temporal node (32 B)
-    double el;             // elapsed(m, j) over the consumed child positions
+struct SmcWSt {            // pending position of a temporal node: all but the elapsed time (32 B)
     int tb;                // min r over true terms (SMC_WINF: none); once final: the result r
     int zm;                // max zero time over the false terms (-1: none)
     int p1;                // U: max r over the phi1 values (all 1 so far)
     int pz;                // U: min r over the phi1 zeros (SMC_WINF: none)
     int fl;                // bit 0 final, bits 1-2 value, bit 3 unknown term, bits 4-5 AND state
-    int pad;
+    int pad[3];
 };
+// The elapsed time of a pending position lives in its own array (8 B per position: the
+// step that only advances it -- every position before its window opens -- touches a quarter
+// of a sector); a final position's elapsed is set to -1 (elapsed times are >= 0).
 
 template <int I> struct SmcWN;
 
@@ -81,6 +83,7 @@ struct SmcMon {
     __device__ __forceinline__ double* tau() const { return (double*)(S + (long long)8 * W); }
     template <int I> __device__ __forceinline__ smc_u64* q() const { return (smc_u64*)(S + (long long)SmcWN<I>::oq * W); }
     template <int I> __device__ __forceinline__ SmcWSt* st() const { return (SmcWSt*)(S + (long long)SmcWN<I>::ost * W); }
+    template <int I> __device__ __forceinline__ double* elp() const { return (double*)(S + (long long)SmcWN<I>::oel * W); }
     __device__ __forceinline__ void sync() const { if (nl > 1) __syncwarp(gm); }
 
     __device__ __forceinline__ void bind(const SmcParams& Q, smc_u64 slot, unsigned mask, int lead) {
@@ -168,33 +171,43 @@ struct SmcMon {
         else if (s.fl & 8) tfinal(s, 2, SMC_WINF);
         else tfinal(s, 0, max(pv == 0 ? min(c, s.pz) : c, s.zm));
     }
-    // position m consumes child position j (the term j and the AND's operand j)
-    template <int I> __device__ __forceinline__ void tstep(SmcWSt& s, int m, int j, double tj, int v1, int r1, int v2,
-                                                           int r2) const {
+    // position m consumes child position j (the term j and the AND's operand j); `el` is
+    // elapsed(m, j - 1) on entry (0 for m == j); returns the new elapsed (< 0: final)
+    template <int I> __device__ __forceinline__ double tstep(SmcWSt* ST, int m, int j, double el, double tj, int v1,
+                                                             int r1, int v2, int r2, bool fresh) const {
         using D = SmcWN<I>;
-        if (m < j) {
-            s.el = __dadd_rn(s.el, tj);                   // elapsed(m, j), left to right
-            if (beyond<I>(s.el)) { tclose(s, j - 1); return; }
+        if (m < j) el = __dadd_rn(el, tj);                // elapsed(m, j), left to right
+        const bool clo = m < j && beyond<I>(el);
+        const bool term = !clo && contains<I>(el);
+        if (!clo && !term && D::kind != SMC_WK_U && !fresh) return el;   // before the window: elapsed only
+        SmcWSt s;
+        if (fresh) { s.tb = SMC_WINF; s.zm = -1; s.p1 = -1; s.pz = SMC_WINF; s.fl = 1 << 4; }
+        else s = ST[m & msk];
+        if (clo) {
+            tclose(s, j - 1);
+        } else {
+            int pv = (s.fl >> 4) & 3;
+            if (term) {
+                if (pv == 0 || v2 == 0) s.zm = max(s.zm, min(pv == 0 ? s.pz : SMC_WINF, v2 == 0 ? r2 : SMC_WINF));
+                else if (pv == 1 && v2 == 1) s.tb = min(s.tb, max(s.p1, r2));
+                else s.fl |= 8;                           // an unknown term (end of trace only)
+            }
+            if constexpr (D::kind == SMC_WK_U) {
+                if (v1 == 0) { s.pz = min(s.pz, r1); pv = 0; }
+                else if (v1 == 1) { if (pv == 1) s.p1 = max(s.p1, r1); }
+                else if (pv == 1) pv = 2;
+                s.fl = (s.fl & ~0x30) | (pv << 4);
+            }
+            if (s.tb != SMC_WINF && (s.tb <= j + 1 || pv == 0)) tfinal(s, 1, s.tb);
+            else if (s.tb == SMC_WINF && !(s.fl & 8) && pv == 0 && s.pz <= j) tfinal(s, 0, max(s.pz, s.zm));
         }
-        int pv = (s.fl >> 4) & 3;
-        if (contains<I>(s.el)) {
-            if (pv == 0 || v2 == 0) s.zm = max(s.zm, min(pv == 0 ? s.pz : SMC_WINF, v2 == 0 ? r2 : SMC_WINF));
-            else if (pv == 1 && v2 == 1) s.tb = min(s.tb, max(s.p1, r2));
-            else s.fl |= 8;                               // an unknown term (end of trace only)
-        }
-        if constexpr (D::kind == SMC_WK_U) {
-            if (v1 == 0) { s.pz = min(s.pz, r1); pv = 0; }
-            else if (v1 == 1) { if (pv == 1) s.p1 = max(s.p1, r1); }
-            else if (pv == 1) pv = 2;
-            s.fl = (s.fl & ~0x30) | (pv << 4);
-        }
-        if (s.tb != SMC_WINF && (s.tb <= j + 1 || pv == 0)) tfinal(s, 1, s.tb);
-        else if (s.tb == SMC_WINF && !(s.fl & 8) && pv == 0 && s.pz <= j) tfinal(s, 0, max(s.pz, s.zm));
+        ST[m & msk] = s;
+        return (s.fl & 1) ? -1.0 : el;
     }
     // the trace ended (or the child stream did) after child position jl: close or leave open
-    template <int I> __device__ __forceinline__ void tend(SmcWSt& s, int jl, bool fin, bool absorbed, int N) {
+    template <int I> __device__ __forceinline__ void tend(SmcWSt& s, double el, int jl, bool fin, bool absorbed, int N) {
         if (fin && absorbed && jl == N) { tclose(s, N); return; }     // no further entries (R7)
-        const double e2 = __dadd_rn(s.el, tau()[jl & msk]);
+        const double e2 = __dadd_rn(el, tau()[jl & msk]);
         if (beyond<I>(e2)) { tclose(s, jl); return; }
         if (!(fin && jl == N)) { err = true; return; }               // child ended inside the window
         const int pv = (s.fl >> 4) & 3;                              // the future term is unknown
@@ -205,9 +218,10 @@ struct SmcMon {
     template <int I> __device__ __forceinline__ void temit() {
         using D = SmcWN<I>;
         SmcWSt* ST = st<I>();
+        const double* EL = elp<I>();
         while (lo[I] < hi[I]) {
+            if (!(EL[lo[I] & msk] < 0.0)) break;
             const int f = ST[lo[I] & msk].fl;
-            if (!(f & 1)) break;
             int v = (f >> 1) & 3;
             if (D::kind == SMC_WK_G && v != 2) v = 1 - v;   // G = not F not
             emit<I>(v, ST[lo[I] & msk].tb);
@@ -235,15 +249,12 @@ struct SmcMon {
                 }
             }
             const double tj = j > 0 ? tau()[(j - 1) & msk] : 0.0;
+            double* EL = elp<I>();
             for (int m = lo[I] + lane; m < hi[I]; m += nl) {
-                SmcWSt s;
-                if (m == j) { s.el = 0.0; s.tb = SMC_WINF; s.zm = -1; s.p1 = -1; s.pz = SMC_WINF; s.fl = 1 << 4; s.pad = 0; }
-                else {
-                    s = ST[m & msk];
-                    if (s.fl & 1) continue;
-                }
-                tstep<I>(s, m, j, tj, v1, r1, v2, r2);
-                ST[m & msk] = s;
+                const bool fresh = m == j;
+                const double e0 = fresh ? 0.0 : EL[m & msk];
+                if (e0 < 0.0) continue;                       // final, waiting to be emitted
+                EL[m & msk] = tstep<I>(ST, m, j, e0, tj, v1, r1, v2, r2, fresh);
             }
             ++qh[B];
             if constexpr (D::kind == SMC_WK_U) ++qh[A];
@@ -255,11 +266,14 @@ struct SmcMon {
             stop[I] = true;
             if (lo[I] < hi[I]) {
                 const int jl = qh[B] - 1;
+                double* EL = elp<I>();
                 for (int m = lo[I] + lane; m < hi[I]; m += nl) {
+                    const double e0 = EL[m & msk];
+                    if (e0 < 0.0) continue;
                     SmcWSt s = ST[m & msk];
-                    if (s.fl & 1) continue;
-                    tend<I>(s, jl, fin, absorbed, N);
+                    tend<I>(s, e0, jl, fin, absorbed, N);
                     ST[m & msk] = s;
+                    EL[m & msk] = -1.0;
                 }
                 sync();
                 temit<I>();

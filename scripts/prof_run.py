@@ -3,6 +3,7 @@ n replicas of a workload.  Prints the events of the profiled launch so that
 scripts/ncu_summary.py can report instructions per event.
 
   python scripts/prof_run.py C4 20000        (ncu: -k regex:smc_ssa -s 1 -c 1)
+  python scripts/prof_run.py C3 100000 "G[0,290](F[1,10](P1 < 400))"   (another formula)
 """
 import json
 import os
@@ -20,6 +21,8 @@ import workloads  # noqa: E402
 def main():
     name, n = sys.argv[1], int(sys.argv[2])
     cfg = workloads.get(name)
+    if len(sys.argv) > 3:
+        cfg = dict(cfg, formula=sys.argv[3])
     torch.cuda.set_device(0)
     smc.use_torch()
     m = smc.Model.from_config(cfg)
