@@ -297,11 +297,13 @@ std::vector<WinNode> window_nodes(const Property& P) {
     return w;
 }
 
+// ring entry bytes: t, tau; a (v, r) queue per node; F / G: two (index, r) deques; U: elapsed +
+// 32-byte state per pending position
 size_t win_bytes(const Property& P) {
     const auto w = window_nodes(P);
-    size_t nt = 0;
-    for (auto& x : w) nt += (x.n.k == LNode::F || x.n.k == LNode::G || x.n.k == LNode::U) ? 1 : 0;
-    return 16 + 8 * w.size() + 40 * nt;
+    size_t b = 16 + 8 * w.size();
+    for (auto& x : w) b += (x.n.k == LNode::F || x.n.k == LNode::G) ? 16 : (x.n.k == LNode::U ? 40 : 0);
+    return b;
 }
 
 // smc_lit_mask(x): atom bit mask of a state; the node table of ssa_window.cuh
@@ -314,12 +316,13 @@ std::string window_code(const Property& P) {
     const auto w = window_nodes(P);
     o << "#define SMC_WIN_NODES " << w.size() << "\n#define SMC_WIN_ROOT " << w.size() - 1
       << "\n#define SMC_WIN_PER_ENTRY " << win_bytes(P) << "\ntemplate <int I> struct SmcWN;\n";
-    size_t nt = 0;
-    for (auto& x : w) nt += (x.n.k == LNode::F || x.n.k == LNode::G || x.n.k == LNode::U) ? 1 : 0;
-    size_t oel = 16 + 8 * w.size(), ost = oel + 8 * nt;   // elapsed arrays, then 32-byte states
+    size_t nu = 0, nfg = 0;
+    for (auto& x : w) { nu += x.n.k == LNode::U ? 1 : 0; nfg += (x.n.k == LNode::F || x.n.k == LNode::G) ? 1 : 0; }
+    // U: elapsed arrays, then 32-byte states; F / G: deques
+    size_t oel = 16 + 8 * w.size(), ost = oel + 8 * nu, odq = ost + 32 * nu;
     for (size_t i = 0; i < w.size(); ++i) {
         const WinNode& x = w[i];
-        const bool temporal = x.n.k == LNode::F || x.n.k == LNode::G || x.n.k == LNode::U;
+        const bool isu = x.n.k == LNode::U, isfg = x.n.k == LNode::F || x.n.k == LNode::G;
         const bool fin = x.n.I.finite();
         o << "template <> struct SmcWN<" << i << "> {   // " << (int)x.n.k << "\n"
           << "    static constexpr int kind = " << (int)x.n.k << ", a = " << x.a << ", b = " << x.b
@@ -329,9 +332,10 @@ std::string window_code(const Property& P) {
           << "    static constexpr bool lo_open = " << (x.n.I.lo_open ? "true" : "false")
           << ", hi_open = " << (x.n.I.hi_open ? "true" : "false") << ", hi_inf = " << (fin ? "false" : "true") << ";\n"
           << "    static constexpr int plim = " << x.plim << ";\n"
-          << "    static constexpr long long oq = " << 16 + 8 * i << ", oel = " << (temporal ? oel : 0)
-          << ", ost = " << (temporal ? ost : 0) << ";\n};\n";
-        if (temporal) { oel += 8; ost += 32; }
+          << "    static constexpr long long oq = " << 16 + 8 * i << ", oel = " << (isu ? oel : 0)
+          << ", ost = " << (isu ? ost : 0) << ", odq = " << (isfg ? odq : 0) << ";\n};\n";
+        if (isu) { oel += 8; ost += 32; }
+        if (isfg) odq += 16;
     }
     return o.str();
 }

@@ -70,6 +70,13 @@ struct SmcMon {
     int qh[SMC_WIN_NODES], qt[SMC_WIN_NODES];  // output queue: consumed by the parent / emitted
     int lo[SMC_WIN_NODES], hi[SMC_WIN_NODES];  // temporal: next position to emit / create; X: next
     bool stop[SMC_WIN_NODES];                  // no more positions will be created
+    // F / G nodes: the head position's window [ka, kb) over the child stream, the next child
+    // entry jc to consume, monotone deques (child indices) of the true entries (min r) and the
+    // false entries (max r) in [ka, jc), unknown entries in [ka, jc)
+    int ka[SMC_WIN_NODES], kb[SMC_WIN_NODES], jc[SMC_WIN_NODES];
+    int dth[SMC_WIN_NODES], dtt[SMC_WIN_NODES], dzh[SMC_WIN_NODES], dzt[SMC_WIN_NODES], nunk[SMC_WIN_NODES];
+    unsigned char hf[SMC_WIN_NODES];           // bit 0 head set, bit 1 ka found, bit 2 kb known, bit 3 elh valid
+    double elh[SMC_WIN_NODES];                 // elapsed(head, jc - 1), exact, while bit 3 is set
     int ne;                                    // entries processed (positions 0 .. ne-1)
     int ntau;                                  // sojourns known (tau_0 .. tau_{ntau-1})
     bool pend;                                 // an entered entry not yet processed
@@ -84,6 +91,9 @@ struct SmcMon {
     template <int I> __device__ __forceinline__ smc_u64* q() const { return (smc_u64*)(S + (long long)SmcWN<I>::oq * W); }
     template <int I> __device__ __forceinline__ SmcWSt* st() const { return (SmcWSt*)(S + (long long)SmcWN<I>::ost * W); }
     template <int I> __device__ __forceinline__ double* elp() const { return (double*)(S + (long long)SmcWN<I>::oel * W); }
+    // F / G deques of (child index, r)
+    template <int I> __device__ __forceinline__ int2* dqt() const { return (int2*)(S + (long long)SmcWN<I>::odq * W); }
+    template <int I> __device__ __forceinline__ int2* dqz() const { return (int2*)(S + (long long)SmcWN<I>::odq * W + 8ll * W); }
     __device__ __forceinline__ void sync() const { if (nl > 1) __syncwarp(gm); }
 
     __device__ __forceinline__ void bind(const SmcParams& Q, smc_u64 slot, unsigned mask, int lead) {
@@ -97,7 +107,13 @@ struct SmcMon {
     }
     __device__ __forceinline__ void init() {
 #pragma unroll
-        for (int i = 0; i < SMC_WIN_NODES; ++i) { qh[i] = qt[i] = lo[i] = hi[i] = 0; stop[i] = false; }
+        for (int i = 0; i < SMC_WIN_NODES; ++i) {
+            qh[i] = qt[i] = lo[i] = hi[i] = 0;
+            stop[i] = false;
+            ka[i] = kb[i] = jc[i] = dth[i] = dtt[i] = dzh[i] = dzt[i] = nunk[i] = 0;
+            hf[i] = 0;
+            elh[i] = 0.0;
+        }
         ne = ntau = 0;
         pend = false;
         last = 0;
@@ -134,7 +150,8 @@ struct SmcMon {
         using D = SmcWN<I>;
         if constexpr (D::kind == SMC_WK_ATOM || D::kind == SMC_WK_TRUE || D::kind == SMC_WK_FALSE) return stop[I];
         else if constexpr (D::kind == SMC_WK_X) return stop[I];
-        else if constexpr (D::kind == SMC_WK_F || D::kind == SMC_WK_G || D::kind == SMC_WK_U) return stop[I] && lo[I] == hi[I];
+        else if constexpr (D::kind == SMC_WK_F || D::kind == SMC_WK_G) return stop[I];
+        else if constexpr (D::kind == SMC_WK_U) return stop[I] && lo[I] == hi[I];
         else if constexpr (D::kind == SMC_WK_NOT) return ended<D::a>() && qh[D::a] == qt[D::a];
         else return (ended<D::a>() && qh[D::a] == qt[D::a]) || (ended<D::b>() && qh[D::b] == qt[D::b]);
     }
@@ -281,6 +298,168 @@ struct SmcMon {
         }
     }
 
+
+    // ---------------------------------------------------------------- F and G (head windows)
+    // F^I phi at m is the OR over the child entries k in the window [ka(m), kb(m)) (elapsed(m, k)
+    // in I; elapsed is monotone in k); G = not F not.  Positions are evaluated in order, one at
+    // a time (the head m = lo): the window's entries enter two monotone deques as the child
+    // stream delivers them -- the min r over the true entries and the max r over the false
+    // ones -- and leave them when the head advances (the windows of consecutive positions move
+    // forward), so a position costs O(1) amortized instead of O(window).  The window bounds
+    // compare elapsed(m, k) -- the left-to-right sum of the semantics -- with I: decided by the
+    // entry-time difference t_k - t_m when that is farther from the bound than the rounding of
+    // both sums can move it (|error| <= 4 (k + 2) u t_k, u = 2^-53), else by the exact sum.
+
+    __device__ __forceinline__ double t_at(int k) const {   // entry time t_k (k <= ne, tau_{k-1} known)
+        return k < ne ? tt()[k & msk] : __dadd_rn(tt()[(k - 1) & msk], tau()[(k - 1) & msk]);
+    }
+    __device__ __forceinline__ double el_exact(int m, int k) const {   // tau_m + ... + tau_{k-1}
+        double e = 0.0;
+        for (int i = m; i < k; ++i) e = (i == m) ? tau()[i & msk] : __dadd_rn(e, tau()[i & msk]);
+        return e;
+    }
+    // sign of elapsed(m, k) - B: -1, 0, +1
+    __device__ __forceinline__ int el_cmp(int m, int k, double B) const {
+        if (k == m) return 0.0 < B ? -1 : (0.0 > B ? 1 : 0);
+        const double tk = t_at(k);
+        const double d = __dsub_rn(tk, tt()[m & msk]);
+        const double dl = __dmul_rn(__dmul_rn((double)(k + 2), 4.4408920985006271e-16), __dmul_rn(tk, 1.0000010000000000));
+        if (__dsub_rn(d, dl) > B) return 1;
+        if (__dadd_rn(d, dl) < B) return -1;
+        const double e = el_exact(m, k);
+        return e < B ? -1 : (e > B ? 1 : 0);
+    }
+    // elapsed(m, k) against a bound: the head's exact running sum when k is the next entry of a
+    // head started from scratch (bit 3), else the entry-time difference with its error bound
+    template <int I> __device__ __forceinline__ int fg_cmp(int m, int k, double B) const {
+        if ((hf[I] & 8) && k == jc[I]) {
+            const double e = k == m ? 0.0 : __dadd_rn(elh[I], tau()[(k - 1) & msk]);
+            return e < B ? -1 : (e > B ? 1 : 0);
+        }
+        return el_cmp(m, k, B);
+    }
+    template <int I> __device__ __forceinline__ bool fg_lo_ok(int m, int k) const {   // elapsed(m,k) >= / > lo
+        using D = SmcWN<I>;
+        const int c = fg_cmp<I>(m, k, D::lo);
+        return D::lo_open ? c > 0 : c >= 0;
+    }
+    template <int I> __device__ __forceinline__ bool fg_beyond(int m, int k) const {
+        using D = SmcWN<I>;
+        if (D::hi_inf) return false;
+        const int c = fg_cmp<I>(m, k, D::hi);
+        return D::hi_open ? c >= 0 : c > 0;
+    }
+    template <int I> __device__ __forceinline__ void fg_val(int k, int& v, int& r) const {
+        using D = SmcWN<I>;
+        peek<D::a>(k, v, r);
+        if (D::kind == SMC_WK_G && v != 2) v = 1 - v;      // G = not F not
+    }
+    template <int I> __device__ __forceinline__ void fg_push(int k) {
+        int v, r;
+        fg_val<I>(k, v, r);
+        if (v == 1) {
+            int2* DT = dqt<I>();
+            while (dtt[I] > dth[I] && DT[(dtt[I] - 1) & msk].y >= r) --dtt[I];
+            DT[dtt[I] & msk] = make_int2(k, r);
+            ++dtt[I];
+        } else if (v == 0) {
+            int2* DZ = dqz<I>();
+            while (dzt[I] > dzh[I] && DZ[(dzt[I] - 1) & msk].y <= r) --dzt[I];
+            DZ[dzt[I] & msk] = make_int2(k, r);
+            ++dzt[I];
+        } else {
+            ++nunk[I];
+        }
+        if (dtt[I] - dth[I] > W || dzt[I] - dzh[I] > W) err = true;
+    }
+    // restart the head's window from scratch (rounding made a window bound move backwards)
+    template <int I> __device__ __forceinline__ void fg_reset(int m) {
+        ka[I] = kb[I] = 0;
+        jc[I] = m;
+        dth[I] = dtt[I] = dzh[I] = dzt[I] = nunk[I] = 0;
+        hf[I] = 1 | 8;                                        // the running sum starts at the head
+        elh[I] = 0.0;
+    }
+    template <int I> __device__ __forceinline__ void fgnode(bool fin, bool absorbed, int N) {
+        using D = SmcWN<I>;
+        constexpr int C = D::a;
+        const bool cend = ended<C>();
+        for (;;) {
+            if (stop[I]) return;
+            const int m = lo[I];
+            if (!(hf[I] & 1)) {                               // a new head position
+                if (m >= ne) return;                          // entry m not processed yet
+                if (!(m < D::plim && tt()[m & msk] <= D::tlim)) { stop[I] = true; return; }
+                fg_reset<I>(m);
+            }
+            // consume the child entries of the head's window
+            bool open_end = false;
+            for (;;) {
+                const int k = jc[I];
+                if (!(hf[I] & 4) && k > m) {                  // does the window end before entry k?
+                    if (fin && k == N + 1) {
+                        if (absorbed || fg_beyond<I>(m, k)) { kb[I] = k; hf[I] |= 4; }
+                        else { open_end = true; break; }
+                    } else if (k < ne || k - 1 < ntau) {
+                        if (fg_beyond<I>(m, k)) { kb[I] = k; hf[I] |= 4; }
+                    } else {
+                        break;                                // t_k not known yet
+                    }
+                }
+                if ((hf[I] & 4) && k >= kb[I]) break;        // window closed and consumed
+                if (k >= qt[C]) {
+                    if (cend || fin) {                        // the child stream ended inside the window
+                        if (!(fin && k == N + 1)) { err = true; return; }
+                    }
+                    break;
+                }
+                if (!(hf[I] & 2) && fg_lo_ok<I>(m, k)) { ka[I] = k; hf[I] |= 2; }
+                if (hf[I] & 2) fg_push<I>(k);
+                if (hf[I] & 8) elh[I] = k == m ? 0.0 : __dadd_rn(elh[I], tau()[(k - 1) & msk]);
+                ++jc[I];
+                if (m + 1 >= D::plim) qh[C] = jc[I];         // the last position: the deques hold what it needs
+            }
+            // is the head's (v, r) final?
+            const bool closed = (hf[I] & 4) && jc[I] >= kb[I];
+            const int tb = dtt[I] > dth[I] ? dqt<I>()[dth[I] & msk].y : SMC_WINF;
+            int v, r;
+            if (tb != SMC_WINF && (tb <= jc[I] || closed || open_end)) { v = 1; r = tb; }
+            else if (closed && nunk[I] == 0) {
+                const int zr = dzt[I] > dzh[I] ? dqz<I>()[dzh[I] & msk].y : -1;
+                v = 0;
+                r = max(kb[I] - 1, zr);
+            } else if (open_end || closed) { v = 2; r = SMC_WINF; }      // the end of the trace: unknown
+            else return;
+            emit<I>(D::kind == SMC_WK_G && v != 2 ? 1 - v : v, r);
+            if (err) return;
+            // advance the head to m + 1: drop the entries before its window
+            const int m1 = m + 1;
+            lo[I] = m1;
+            qh[C] = min(m1, qt[C]);                           // the child ring keeps [head, ...)
+            if (fin && m1 > N) { stop[I] = true; return; }
+            if (m1 >= ne) { hf[I] = 0; return; }              // entry m + 1 not processed yet
+            if (!(m1 < D::plim && tt()[m1 & msk] <= D::tlim)) { stop[I] = true; return; }
+            if (jc[I] < m1) { fg_reset<I>(m1); continue; }
+            // the new window's lower end: later or equal (else restart), entries before it leave
+            int a = (hf[I] & 2) ? max(ka[I], m1) : jc[I];
+            if (a > m1 && a - 1 < jc[I] && fg_lo_ok<I>(m1, a - 1)) { fg_reset<I>(m1); continue; }
+            while (a < jc[I] && !fg_lo_ok<I>(m1, a)) ++a;
+            if (jc[I] > m1 && fg_beyond<I>(m1, jc[I] - 1)) { fg_reset<I>(m1); continue; }
+            {
+                const int2* DT = dqt<I>();
+                const int2* DZ = dqz<I>();
+                while (dth[I] < dtt[I] && DT[dth[I] & msk].x < a) ++dth[I];
+                while (dzh[I] < dzt[I] && DZ[dzh[I] & msk].x < a) ++dzh[I];
+                if (nunk[I] > 0) {
+                    for (int k = (hf[I] & 2) ? ka[I] : a; k < a; ++k) { int vv, rr; fg_val<I>(k, vv, rr); if (vv == 2) --nunk[I]; }
+                }
+            }
+            if (a < jc[I]) { ka[I] = a; hf[I] |= 2; }
+            else hf[I] &= ~2;
+            hf[I] &= ~(4 | 8);                                // the window end is re-determined
+        }
+    }
+
     // ---------------------------------------------------------------- X, booleans
     template <int I> __device__ __forceinline__ void xnode(bool fin, bool absorbed, int N) {
         using D = SmcWN<I>;
@@ -345,7 +524,8 @@ struct SmcMon {
     template <int I> __device__ __forceinline__ void pump_node(bool fin, bool absorbed, int N) {
         using D = SmcWN<I>;
         if (err || dead<I>()) return;
-        if constexpr (D::kind == SMC_WK_F || D::kind == SMC_WK_G || D::kind == SMC_WK_U) temporal<I>(fin, absorbed, N);
+        if constexpr (D::kind == SMC_WK_F || D::kind == SMC_WK_G) fgnode<I>(fin, absorbed, N);
+        else if constexpr (D::kind == SMC_WK_U) temporal<I>(fin, absorbed, N);
         else if constexpr (D::kind == SMC_WK_X) xnode<I>(fin, absorbed, N);
         else if constexpr (D::kind == SMC_WK_NOT || D::kind == SMC_WK_AND || D::kind == SMC_WK_OR) boolean<I>();
     }
@@ -358,9 +538,12 @@ struct SmcMon {
         if constexpr (I < SMC_WIN_NODES) {
             using D = SmcWN<I>;
             int l = lo_;
-            if constexpr (D::kind == SMC_WK_F || D::kind == SMC_WK_G || D::kind == SMC_WK_U) {
-                constexpr int B = D::kind == SMC_WK_U ? D::b : D::a;
-                if (!(stop[I] && lo[I] == hi[I]) && !dead<I>()) l = min(l, qh[B] - 1);
+            if constexpr (D::kind == SMC_WK_F || D::kind == SMC_WK_G) {
+                // the head's t and taus (a later head re-reads them), or only tau_{jc-1} when
+                // the head is the node's last position (its running sum carries the rest)
+                if (!stop[I] && !dead<I>()) l = min(l, (lo[I] + 1 < D::plim) ? lo[I] : max(lo[I], jc[I] - 1));
+            } else if constexpr (D::kind == SMC_WK_U) {
+                if (!(stop[I] && lo[I] == hi[I]) && !dead<I>()) l = min(l, qh[D::b] - 1);
             } else if constexpr (D::kind == SMC_WK_X) {
                 if (!stop[I] && !dead<I>()) l = min(l, lo[I]);
             }

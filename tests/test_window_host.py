@@ -43,6 +43,8 @@ static inline double __fma_rn(double a, double b, double c) { return std::fma(a,
 using std::max;
 using std::min;
 struct SmcParams { double* lit_t; smc_u64 lit_cap; };
+struct int2 { int x, y; };
+static inline int2 make_int2(int a, int b) { return int2{a, b}; }
 """
 
 DRIVER = r"""
