@@ -20,11 +20,11 @@ struct SmcParams {
     int* events_out;           // optional per-replica event count
     smc_u64 event_cap;     // per-replica event cap
     const void* tables;    // packed model tables (tile variant)
-    double* lit_t;         // literal variant: per-thread trace buffers (entry times)
-    double* lit_tau;       //   sojourns (the last one is the overshoot draw)
-    unsigned* lit_mask;    //   atom bit masks
-    unsigned char* lit_val;    // subformula values, node-major per thread slice
-    smc_u64 lit_cap;       //   entries per thread slice
+    double* lit_t;         // window monitor (ssa_window.cuh): every replica slot's rings
+    double* lit_unused0;   //   (reserved)
+    unsigned* lit_unused1;
+    unsigned char* lit_unused2;
+    smc_u64 lit_cap;       //   ring entries per replica slot (a power of two)
 };
 
 // Philox4x32-10 (Salmon et al. 2011), counter (c0..c3), key (k0, k1).

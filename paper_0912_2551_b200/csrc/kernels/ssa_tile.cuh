@@ -22,9 +22,10 @@
 // * Propensity laws are evaluated in fp64 on integer-valued doubles; for
 //   reaction order <= 2 this is exactly (double)h with h the int64 combinatorial
 //   count (see smc_law_tab), order 3-4 takes the int64 path.
-// * Formulas outside the streaming templates use a generated recording monitor
-//   (buffered trace + literal |= at the horizon, reading R23) through the same
-//   SmcMon interface (bind / init / enter / advance / absorb / timeout / verdict).
+// * Formulas outside the streaming templates use the window monitor (ssa_window.cuh:
+//   the literal |= on the fly with memory bounded by the formula's windows, readings
+//   R23/R27; the tile's lanes share its rings) through the same SmcMon interface
+//   (bind / init / enter / advance / absorb / timeout / verdict / at_cap / events).
 // * The Philox + log draws of the next SMC_TW steps of every tile are computed
 //   together at the start of each burst of SMC_TW events, one draw per lane
 //   (state-independent, so batching them is exact).
@@ -32,7 +33,7 @@
 // Generated hooks (codegen.cpp): SMC_N, SMC_M, SMC_TW, SMC_GS, SMC_CH, SMC_NPAD,
 //   SMC_OFF_*, SMC_TAB_BYTES, SMC_TILE_BYTES, SMC_ANY_HILL, SMC_ANY_GENERAL, SMC_DEP16,
 //   SMC_ANY_EXPLICIT (+ smc_explicit), SMC_DEPSP, SMC_FATDEP, SMC_ROWLAYOUT, SMC_GSP,
-//   SMC_TMAX, SmcMon (+ SMC_LIT_H, SMC_LIT_NODES, smc_lit_* for the recording monitor).
+//   SMC_TMAX, SmcMon (+ SMC_LIT_H, the SmcWN node table, smc_lit_mask for the window monitor).
 
 struct SmcTabs {
     const int* x0;
@@ -462,7 +463,7 @@ extern "C" __global__ void __launch_bounds__(768, 1) smc_ssa_tile(SmcParams P) {
                 }
             }
             if (act && v >= 0) {
-                const long long ke = mon.events((long long)k);   // the recording monitor: the first
+                const long long ke = mon.events((long long)k);   // the window monitor: the first
                 if (tl == 0) {                                    // decision index
                     if (v == 1) ++c_true;
                     else if (v == 0) ++c_false;

@@ -225,7 +225,7 @@ PropKernel& prepare(Model& m, const Property& p) {
     PropKernel pk;
     pk.variant = m.variant();
     // buffered trace + literal |= (reading R23): thread-owned models run variant 3, tile
-    // models the tile kernel with the recording monitor
+    // models the tile kernel, both with the window monitor (R27)
     if (p.literal && pk.variant == 1) pk.variant = 3;
     if (p.literal && (pk.variant == 4 || pk.variant == 5)) pk.variant = 2;   // the recording monitor lives in the tile kernel
     const TileLayout* tl = nullptr;
