@@ -224,10 +224,10 @@ PropKernel& prepare(Model& m, const Property& p) {
     m.build_deps();
     PropKernel pk;
     pk.variant = m.variant();
-    // buffered trace + literal |= (reading R23): thread-owned models run variant 3, tile
+    // literal |= on the fly (reading R23): thread-owned models run variant 3, tile
     // models the tile kernel, both with the window monitor (R27)
     if (p.literal && pk.variant == 1) pk.variant = 3;
-    if (p.literal && (pk.variant == 4 || pk.variant == 5)) pk.variant = 2;   // the recording monitor lives in the tile kernel
+    if (p.literal && (pk.variant == 4 || pk.variant == 5)) pk.variant = 2;   // the window monitor lives in the tile kernel
     const TileLayout* tl = nullptr;
     const int v = pk.variant == 3 ? 1 : pk.variant;      // table set (variant 3 uses variant 1's)
     if (!d.tables_ready[v]) {
