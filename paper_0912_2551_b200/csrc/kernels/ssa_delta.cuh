@@ -124,6 +124,35 @@ __device__ __forceinline__ void smc_gadd(ulonglong2* w, smc_u64 cq, smc_i64 dh) 
     *w = v;
 }
 
+#ifndef SMC_DFAST
+#define SMC_DFAST 1
+#endif
+// The same update without branches on the law's kind (a divergent warp ran every kind's path):
+// h = x0 x1 with x1 = x0 - 1 for a homodimer (whose entry carries d1 = d0) and x1 = x[N] = 1
+// for a first-order law (d1 = 0), so dh = d0 x1 + d1 x0 - d0 d1 for every kind; and, while
+// |dh| < 2^32 (counts below ~2^28), Cq |dh| as two 32 x 32 -> 64-bit products added to the
+// 128-bit sum in two's complement.  Bit-identical to smc_ddh + smc_gadd (SMC_DCHECK).
+__device__ __forceinline__ void smc_gupd(ulonglong2* w, const SmcDLaw& L, int a, int b, const int* xs) {
+    const int x0 = xs[L.ops & 0xFFFFu];
+    const int xr = xs[L.ops >> 16];
+    const int x1 = (L.kind == 2u) ? x0 - 1 : xr;
+    const smc_i64 dh = (smc_i64)a * x1 + (smc_i64)b * x0 - (smc_i64)(a * b);
+    const smc_u64 u = (smc_u64)(dh < 0 ? -dh : dh);
+    if (u >> 32) { smc_gadd(w, L.cq, dh); return; }
+    const smc_u32 u32 = (smc_u32)u;
+    const smc_u64 p0 = (smc_u64)(smc_u32)L.cq * u32;
+    const smc_u64 p1 = (smc_u64)(smc_u32)(L.cq >> 32) * u32;
+    const smc_u64 lo = p0 + (p1 << 32);
+    const smc_u64 hi = (p1 >> 32) + (lo < p0 ? 1ull : 0ull);
+    const smc_u64 m = dh < 0 ? ~0ull : 0ull;                    // two's complement negation
+    const smc_u64 l2 = (lo ^ m) - m;
+    const smc_u64 h2 = (hi ^ m) + ((m & 1ull) & (lo == 0ull ? 1ull : 0ull));
+    ulonglong2 v = *w;
+    v.x += l2;
+    v.y += h2 + (v.x < l2 ? 1ull : 0ull);
+    *w = v;
+}
+
 extern "C" __global__ void __launch_bounds__(SMC_DBLOCK, 1) smc_ssa_delta(SmcParams P) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ __align__(8) unsigned long long bar;
@@ -383,7 +412,11 @@ extern "C" __global__ void __launch_bounds__(SMC_DBLOCK, 1) smc_ssa_delta(SmcPar
                     const int kk = (int)(e & 0xFFFFu), a = (int)((e >> 16) & 15u) - 8, b = (int)((e >> 20) & 15u) - 8;
 #endif
                     const SmcDLaw L = T.dlaw[kk];
+#if SMC_DFAST
+                    smc_gupd(gs + smc_gslot(kk / S), L, a, b, xs);
+#else
                     smc_gadd(gs + smc_gslot(kk / S), L.cq, smc_ddh(L, a, b, xs));
+#endif
                 }
                 at += (unsigned)cnt;
                 __syncwarp();
