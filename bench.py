@@ -121,7 +121,7 @@ def model_stats(cfg):
 
 # the committed ncu --set full summary the roofline's `traffic` comes from (named explicitly:
 # a stray capture in profiles/ must not change the bench line)
-TRAFFIC_FILE = os.path.join(ROOT, "profiles", "traffic_r01f8.json")
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "traffic_r02.json")
 
 
 def measured_profile(workload, kernel):
