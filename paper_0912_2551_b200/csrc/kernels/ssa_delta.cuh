@@ -64,6 +64,10 @@ struct SmcDTabs {
 #endif
 };
 
+#ifndef SMC_DFAST
+#define SMC_DFAST 1
+#endif
+
 // exact integer h_k in the table's form: x0 * x1 (kinds 0, 1, 3 with x[N] = 1), x0 (x0 - 1)
 // (kind 2; 0 for x0 <= 1).  Counts < 2^31, so the product fits int64 exactly.
 __device__ __forceinline__ smc_i64 smc_dh(const SmcDLaw& L, const int* xs) {
@@ -79,9 +83,16 @@ __device__ __forceinline__ double smc_dlaw(const SmcLaw& L, const int* xs) {
     // (the second operand is read only for x0 x1: kind 1 has x[N] = 1 -- fewer shared loads)
     const unsigned kind = (L.u0 >> 16) & 7u;
     const int v0 = xs[L.u0 & 0xFFFFu];
+#if SMC_DFAST
+    // branch-free: the second operand is x[N] = 1 for kinds 0 and 1, x0 - 1 for a homodimer
+    // (x0 (x0 - 1) = 0 at x0 = 0 either way)
+    const int xr = xs[L.u1 & 0xFFFFu];
+    const int xb = (kind == 2u) ? v0 - 1 : xr;
+#else
     int xb = 1;
     if (kind == 3u) xb = xs[L.u1 & 0xFFFFu];
     else if (kind == 2u) xb = max(v0 - 1, 0);
+#endif
     return __dmul_rn(L.c, __ll2double_rn((smc_i64)v0 * xb));
 }
 
@@ -124,9 +135,6 @@ __device__ __forceinline__ void smc_gadd(ulonglong2* w, smc_u64 cq, smc_i64 dh) 
     *w = v;
 }
 
-#ifndef SMC_DFAST
-#define SMC_DFAST 1
-#endif
 // The same update without branches on the law's kind (a divergent warp ran every kind's path):
 // h = x0 x1 with x1 = x0 - 1 for a homodimer (whose entry carries d1 = d0) and x1 = x[N] = 1
 // for a first-order law (d1 = 0), so dh = d0 x1 + d1 x0 - d0 d1 for every kind; and, while
