@@ -355,8 +355,23 @@ struct SmcMon {
         if (D::kind == SMC_WK_G && v != 2) v = 1 - v;      // G = not F not
     }
     template <int I> __device__ __forceinline__ void fg_push(int k) {
+        using D = SmcWN<I>;
         int v, r;
         fg_val<I>(k, v, r);
+        if (lo[I] + 1 >= D::plim) {                          // the node's last position: its window
+            if (v == 1) {                                     // never moves, only the extremes matter
+                int2* DT = dqt<I>();
+                if (dtt[I] == dth[I]) { DT[dth[I] & msk] = make_int2(k, r); dtt[I] = dth[I] + 1; }
+                else if (r < DT[dth[I] & msk].y) DT[dth[I] & msk] = make_int2(k, r);
+            } else if (v == 0) {
+                int2* DZ = dqz<I>();
+                if (dzt[I] == dzh[I]) { DZ[dzh[I] & msk] = make_int2(k, r); dzt[I] = dzh[I] + 1; }
+                else if (r > DZ[dzh[I] & msk].y) DZ[dzh[I] & msk] = make_int2(k, r);
+            } else {
+                ++nunk[I];
+            }
+            return;
+        }
         if (v == 1) {
             int2* DT = dqt<I>();
             while (dtt[I] > dth[I] && DT[(dtt[I] - 1) & msk].y >= r) --dtt[I];

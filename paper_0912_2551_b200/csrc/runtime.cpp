@@ -185,9 +185,9 @@ DeviceState& device(Model& m) {
 
 // Rings of the window monitor (ssa_window.cuh, readings R23/R27), sized PER LAUNCH: every
 // replica slot of the `grid` CTAs (`per_cta` slots each) gets W ring entries of
-// `lit_per_entry` bytes, W the largest power of two up to SMC_WIN_W (default 4096) within the
-// budget (a third of the free device memory, at most 48 GiB); a launch that cannot give
-// every slot 1024 entries runs fewer resident CTAs.  The rings hold the formula's windows
+// `lit_per_entry` bytes, W the largest power of two up to SMC_WIN_W (default 16384) within the
+// budget (half the free device memory, at most 64 GiB); a launch that cannot give every slot
+// 1024 entries runs fewer resident CTAs.  The rings hold the formula's windows
 // (not the trace), so W bounds how many entries one window may span; a replica whose window
 // would overflow its ring ends as an error.
 void size_traces(Model& m, PropKernel& pk, int per_cta, int& grid) {
@@ -195,9 +195,9 @@ void size_traces(Model& m, PropKernel& pk, int per_cta, int& grid) {
     size_t free_b = 0, total_b = 0;
     ck(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
     const size_t held = (size_t)pk.lit_entries * pk.lit_per_entry;   // ours, reusable
-    const size_t budget = std::min<size_t>((free_b + held) / 3, (size_t)48 << 30);
+    const size_t budget = std::min<size_t>((free_b + held) / 2, (size_t)64 << 30);
     const size_t per_entry = pk.lit_per_entry;
-    size_t want = 4096;
+    size_t want = 16384;
     if (const char* e = std::getenv("SMC_WIN_W")) want = std::max<size_t>(16, std::strtoull(e, nullptr, 10));
     const size_t min_cap = std::min<size_t>(want, 1024);
     if (budget / ((size_t)grid * (size_t)per_cta * per_entry) < min_cap)
