@@ -1289,6 +1289,7 @@ std::string generate_source(const Model& m, const Property& p, int variant, cons
           << "\n#define SMC_DBLOCK " << blk << "\n";
         if (const char* e = std::getenv("SMC_DCHECK")) o << "#define SMC_DCHECK " << std::atoi(e) << "\n";
         if (const char* e = std::getenv("SMC_DFAST")) o << "#define SMC_DFAST " << std::atoi(e) << "\n";
+        if (std::getenv("SMC_DTRACE")) o << "#define SMC_DTRACE 1\n";
         o << "#define SMC_DSCALE " << dlit(std::ldexp(1.0, tl->dl)) << "\n#define SMC_DINV " << dlit(std::ldexp(1.0, -tl->dl))
           << "\n#define SMC_DHI " << dlit(std::ldexp(1.0, 64 - tl->dl)) << "\n";
         o << "#define SMC_OFF_X0 " << tl->off_x0 << "\n#define SMC_OFF_LAW " << tl->off_law << "\n#define SMC_OFF_CQ "

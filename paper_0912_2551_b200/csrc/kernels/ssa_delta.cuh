@@ -217,7 +217,17 @@ extern "C" __global__ void __launch_bounds__(SMC_DBLOCK, 1) smc_ssa_delta(SmcPar
     smc_u32 c_true = 0, c_false = 0, c_err = 0;   // tile leader
     smc_i64 c_ev = 0;
 
+#ifdef SMC_DTRACE
+    long long guard = 0;
+#endif
     for (;;) {
+#ifdef SMC_DTRACE
+        if (++guard > 20000) {
+            if (tl == 0) printf("DTRACE guard: warp %d tile %d act %d exh %d rel %llu k %u x0 %d\n", warp, tile, (int)act,
+                                (int)exhausted, rel, k, xs[0]);
+            return;
+        }
+#endif
         // ---- refill: tiles without a trajectory claim fresh indices (one atomic per warp)
         for (;;) {
             const bool want = !act && !exhausted;
@@ -456,6 +466,11 @@ extern "C" __global__ void __launch_bounds__(SMC_DBLOCK, 1) smc_ssa_delta(SmcPar
                 }
                 if (bad) { printf("SMC_DCHECK traj %llu k %u j %d g %d jm %d\n", traj, k, j, g, jm); asm volatile("trap;"); }
             }
+#endif
+#ifdef SMC_DTRACE
+            if (act && tl == 0 && k < 12)
+                printf("DTRACE rel %llu k %u A %.17g tn %.17g j %d x0 %d v %d go %d ovf %d nr %d\n", rel, k, A, tn, j, xs[0], v,
+                       (int)go, (int)tile_ovf, nr);
 #endif
             if (go) {
                 if (tile_ovf) {

@@ -185,7 +185,7 @@ DeviceState& device(Model& m) {
 
 // Rings of the window monitor (ssa_window.cuh, readings R23/R27), sized PER LAUNCH: every
 // replica slot of the `grid` CTAs (`per_cta` slots each) gets W ring entries of
-// `lit_per_entry` bytes, W the largest power of two up to SMC_WIN_W (default 16384) within the
+// `lit_per_entry` bytes, W the largest power of two up to SMC_WIN_W (default 32768) within the
 // budget (half the free device memory, at most 64 GiB); a launch that cannot give every slot
 // 1024 entries runs fewer resident CTAs.  The rings hold the formula's windows
 // (not the trace), so W bounds how many entries one window may span; a replica whose window
@@ -197,7 +197,7 @@ void size_traces(Model& m, PropKernel& pk, int per_cta, int& grid) {
     const size_t held = (size_t)pk.lit_entries * pk.lit_per_entry;   // ours, reusable
     const size_t budget = std::min<size_t>((free_b + held) / 2, (size_t)64 << 30);
     const size_t per_entry = pk.lit_per_entry;
-    size_t want = 16384;
+    size_t want = 32768;
     if (const char* e = std::getenv("SMC_WIN_W")) want = std::max<size_t>(16, std::strtoull(e, nullptr, 10));
     const size_t min_cap = std::min<size_t>(want, 1024);
     if (budget / ((size_t)grid * (size_t)per_cta * per_entry) < min_cap)
