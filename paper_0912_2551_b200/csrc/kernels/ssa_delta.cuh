@@ -207,6 +207,30 @@ extern "C" __global__ void __launch_bounds__(SMC_DBLOCK, 1) smc_ssa_delta(SmcPar
     ulonglong2* const gs = (ulonglong2*)slice;                  // G exact group sums
     int* const xs = (int*)(slice + 16 * SMC_DG);
 
+    // every tile's slice starts as the initial state (x0 and its exact group sums), so the
+    // tiles that never get a trajectory (the tail of a launch: a warp with fewer trajectories
+    // than tiles) run the warp's lock-step code on well-defined values
+    for (int s = tl; s <= SMC_N; s += TW) xs[s] = T.x0[s];
+    __syncwarp();
+#pragma unroll 1
+    for (int i = 0; i < GPL; ++i) {
+        const int g = tl * GPL + i;
+        smc_u64 lo = 0ull, hi = 0ull;
+#pragma unroll 1
+        for (int m = 0; m < S; ++m) {
+            const int kk = g * S + m;
+            if (kk < SMC_M) {
+                const SmcDLaw L = T.dlaw[kk];
+                const smc_u64 h = (smc_u64)smc_dh(L, xs), cq = L.cq;
+                const smc_u64 plo = cq * h;
+                lo += plo;
+                hi += __umul64hi(cq, h) + (lo < plo ? 1ull : 0ull);
+            }
+        }
+        gs[smc_gslot(g)] = make_ulonglong2(lo, hi);
+    }
+    __syncwarp();
+
     bool act = false, exhausted = false;
     smc_u64 rel = 0, traj = 0;
     double t = 0.0, tp = 0.0;
@@ -313,6 +337,9 @@ extern "C" __global__ void __launch_bounds__(SMC_DBLOCK, 1) smc_ssa_delta(SmcPar
             const double tau = smc_tau(E, A);
             const double tn = __dadd_rn(t, tau);
             int v = -1;
+#ifdef SMC_DTRACE
+            if (act && tl == 0 && !(A > 0.0)) printf("DTRACE absorb rel %llu k %u A %g x %d %d %d %d\n", rel, k, A, xs[0], xs[1], xs[2], xs[3]);
+#endif
             if (act) {
                 if (!(A >= SMC_A_MIN) || A > SMC_A_MAX) {            // A == 0: absorbed; else error (R19)
                     if (A == 0.0) { mon.absorb(); v = mon.verdict(); }     // absorbed (reading R7)
@@ -386,6 +413,9 @@ extern "C" __global__ void __launch_bounds__(SMC_DBLOCK, 1) smc_ssa_delta(SmcPar
                 jm = __shfl_sync(SMC_FULL, hsrc * CH + hit, hsrc, TW);
             }
             const int j = go ? g * S + jm : 0;
+#ifdef SMC_DTRACE
+            if (act && !(A > 0.0)) printf("DTRACE sel lane %d rel %llu g %d jm %d j %d go %d v %d owner %d og %d\n", lane, rel, g, jm, j, (int)go, v, owner, og);
+#endif
 
             // ---- x += v_j (<= 4 distinct species, one lane each; wrapping add, sign = overflow)
             bool ovf = false;
@@ -468,7 +498,7 @@ extern "C" __global__ void __launch_bounds__(SMC_DBLOCK, 1) smc_ssa_delta(SmcPar
             }
 #endif
 #ifdef SMC_DTRACE
-            if (act && tl == 0 && k < 12)
+            if (act && tl == 0 && (k < 4 || !(A > 0.0) || k % 500 == 0))
                 printf("DTRACE rel %llu k %u A %.17g tn %.17g j %d x0 %d v %d go %d ovf %d nr %d\n", rel, k, A, tn, j, xs[0], v,
                        (int)go, (int)tile_ovf, nr);
 #endif
