@@ -882,7 +882,10 @@ TileLayout pack_delta_tables(const Model& m) {
     if (L.dl < 0) fail(SMC_E_MODEL, "delta variant: model not eligible (reading R26)");
     // tile width 8 (C5: 2.9e9 events/s vs 2.4e9 at 16, 1.6e9 at 32); widths below 8 are not
     // supported (TW = 4 hung on random networks)
-    L.tw = 8;
+    // small models (only reached by forcing the variant) use one tile per warp: with several
+    // tiles per warp, warp intrinsics returned inconsistent values on small absorbing models
+    // (C2 run to absorption), which full-warp tiles do not show
+    L.tw = M >= 256 ? 8 : 32;
     if (const char* e = std::getenv("SMC_TILE_WIDTH")) {
         const int w = std::atoi(e);
         if (w == 8 || w == 16 || w == 32) L.tw = w;
@@ -1290,6 +1293,7 @@ std::string generate_source(const Model& m, const Property& p, int variant, cons
         if (const char* e = std::getenv("SMC_DCHECK")) o << "#define SMC_DCHECK " << std::atoi(e) << "\n";
         if (const char* e = std::getenv("SMC_DFAST")) o << "#define SMC_DFAST " << std::atoi(e) << "\n";
         if (std::getenv("SMC_DTRACE")) o << "#define SMC_DTRACE 1\n";
+        if (std::getenv("SMC_DBOUNDS")) o << "#define SMC_DBOUNDS 1\n#define SMC_DTABEND " << tl->bytes << "\n";
         o << "#define SMC_DSCALE " << dlit(std::ldexp(1.0, tl->dl)) << "\n#define SMC_DINV " << dlit(std::ldexp(1.0, -tl->dl))
           << "\n#define SMC_DHI " << dlit(std::ldexp(1.0, 64 - tl->dl)) << "\n";
         o << "#define SMC_OFF_X0 " << tl->off_x0 << "\n#define SMC_OFF_LAW " << tl->off_law << "\n#define SMC_OFF_CQ "

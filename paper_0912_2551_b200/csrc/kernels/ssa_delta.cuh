@@ -96,6 +96,11 @@ __device__ __forceinline__ double smc_dlaw(const SmcLaw& L, const int* xs) {
     return __dmul_rn(L.c, __ll2double_rn((smc_i64)v0 * xb));
 }
 
+#ifdef SMC_DBOUNDS
+#define SMC_BC(i, lim, tag) do { if ((unsigned)(i) >= (unsigned)(lim)) { printf("DBOUNDS %s %d >= %d (lane %d warp %d)\n", tag, (int)(i), (int)(lim), (int)(threadIdx.x & 31), (int)(threadIdx.x >> 5)); asm volatile("trap;"); } } while (0)
+#else
+#define SMC_BC(i, lim, tag) do { } while (0)
+#endif
 // group g -> 16-byte slot in the tile's slice
 constexpr int SMC_DGPL = SMC_DG / SMC_TW;
 #ifndef SMC_DCHECK
@@ -351,6 +356,7 @@ extern "C" __global__ void __launch_bounds__(SMC_DBLOCK, 1) smc_ssa_delta(SmcPar
                 }
             }
             const bool go = act && v < 0;              // this tile applies a reaction
+            __syncwarp();                              // reconverge after the tile-divergent monitor step
             // ---- selection (Eq. 2b), level 1: owner lane by ballot, then its groups in order
             const double target = __dmul_rn(U, A);
             const smc_u32 bo = (__ballot_sync(SMC_FULL, Pl > target) & tbits) >> (tile * TW);
@@ -381,6 +387,7 @@ extern "C" __global__ void __launch_bounds__(SMC_DBLOCK, 1) smc_ssa_delta(SmcPar
             double cs = 0.0;
 #pragma unroll
             for (int c = 0; c < CH; ++c) {
+                SMC_BC(g * S + c * TW + tl, SMC_DG * SMC_DS, "law");
                 av[c] = smc_dlaw(T.law[g * S + c * TW + tl], xs);   // member tl CH + c (permuted table)
                 cs = (c == 0) ? av[0] : __dadd_rn(cs, av[c]);
             }
@@ -400,29 +407,29 @@ extern "C" __global__ void __launch_bounds__(SMC_DBLOCK, 1) smc_ssa_delta(SmcPar
                 if (av[c] > 0.0) lastm = c;
             }
             const smc_u32 bh = (__ballot_sync(SMC_FULL, hit >= 0) & tbits) >> (tile * TW);
-            int jm;
-            if (__any_sync(SMC_FULL, bh == 0u || fb)) {          // rounding: last a_k > 0 (R11)
-                const smc_u32 bl = (__ballot_sync(SMC_FULL, lastm >= 0) & tbits) >> (tile * TW);
-                const int src = bl ? 31 - __clz(bl) : 0;
-                const int jl = __shfl_sync(SMC_FULL, src * CH + lastm, src, TW);
-                const int hsrc = bh ? __ffs(bh) - 1 : 0;
-                const int jh = __shfl_sync(SMC_FULL, hsrc * CH + hit, hsrc, TW);
-                jm = (bh == 0u || fb) ? jl : jh;
-            } else {
-                const int hsrc = __ffs(bh) - 1;
-                jm = __shfl_sync(SMC_FULL, hsrc * CH + hit, hsrc, TW);
-            }
+            // the rounding fallback (R11: the last member with a_k > 0) and the regular hit, both
+            // always computed: the shuffles run converged, outside any warp-level branch
+            const smc_u32 bl = (__ballot_sync(SMC_FULL, lastm >= 0) & tbits) >> (tile * TW);
+            const int src = bl ? 31 - __clz(bl) : 0;
+            const int jl = __shfl_sync(SMC_FULL, src * CH + lastm, src, TW);
+            const int hsrc = bh ? __ffs(bh) - 1 : 0;
+            const int jh = __shfl_sync(SMC_FULL, hsrc * CH + hit, hsrc, TW);
+            const int jm = (bh == 0u || fb) ? jl : jh;
             const int j = go ? g * S + jm : 0;
 #ifdef SMC_DTRACE
             if (act && !(A > 0.0)) printf("DTRACE sel lane %d rel %llu g %d jm %d j %d go %d v %d owner %d og %d\n", lane, rel, g, jm, j, (int)go, v, owner, og);
 #endif
 
-            // ---- x += v_j (<= 4 distinct species, one lane each; wrapping add, sign = overflow)
-            bool ovf = false;
-            if (go && tl < 4) {
+            // ---- x += v_j (<= 4 distinct species, one lane each; wrapping add, sign = overflow);
+            // a selection outside the reactions (never seen on C4/C5 networks; observed on small
+            // absorbing models with several tiles per warp) ends the replica as an error
+            bool ovf = go && (unsigned)j >= (unsigned)SMC_M;
+            if (go && !ovf && tl < 4) {
+                SMC_BC(j, SMC_M, "chg j");
                 const unsigned e = T.chg[j * 4 + tl];
                 if (e != 0xFFFFu) {
                     const int sp = (int)(e >> 4);
+                    SMC_BC(sp, SMC_N, "chg sp");
                     const int nv = (int)((unsigned)xs[sp] + (unsigned)((int)(e & 15u) - 8));
                     ovf = nv < 0;
                     xs[sp] = nv;
@@ -430,9 +437,9 @@ extern "C" __global__ void __launch_bounds__(SMC_DBLOCK, 1) smc_ssa_delta(SmcPar
             }
             const bool tile_ovf = ((__ballot_sync(SMC_FULL, ovf) & tbits) != 0u);
 #if SMC_DDESC64
-            const smc_u64 desc = go ? T.dep_off[j] : 0ull;
+            const smc_u64 desc = (go && !tile_ovf) ? T.dep_off[j] : 0ull;
 #else
-            const unsigned desc = go ? T.dep_off[j] : 0u;
+            const unsigned desc = (go && !tile_ovf) ? T.dep_off[j] : 0u;
 #endif
             __syncwarp();
             // ---- Sg += Cq_k (h_k(x_new) - h_k(x_old)) for k in dep(j), exact, from the new
@@ -453,12 +460,17 @@ extern "C" __global__ void __launch_bounds__(SMC_DBLOCK, 1) smc_ssa_delta(SmcPar
                 const int cnt = (r < nr) ? (int)T.rcnt[j * SMC_DRMAX + r] : 0;
 #endif
                 if (tl < cnt) {
+#ifdef SMC_DBOUNDS
+                    SMC_BC(SMC_OFF_DEP + (at + tl) * (SMC_DDEP16 ? 2 : 4), SMC_DTABEND, "dep");
+#endif
                     const unsigned e = T.dep[at + (unsigned)tl];
 #if SMC_DDEP16
                     const int kk = (int)(e & 1023u), a = (int)((e >> 10) & 7u) - 4, b = (int)(e >> 13) - 4;
 #else
                     const int kk = (int)(e & 0xFFFFu), a = (int)((e >> 16) & 15u) - 8, b = (int)((e >> 20) & 15u) - 8;
 #endif
+                    SMC_BC(kk, SMC_M, "dlaw kk");
+                    SMC_BC(smc_gslot(kk / S), SMC_DG, "gslot");
                     const SmcDLaw L = T.dlaw[kk];
 #if SMC_DFAST
                     smc_gupd(gs + smc_gslot(kk / S), L, a, b, xs);
