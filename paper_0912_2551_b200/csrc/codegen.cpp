@@ -1243,7 +1243,9 @@ std::string generate_source(const Model& m, const Property& p, int variant, cons
         // the trace must cover what the semantics can look at: t_max for unbounded formulas,
         // else the formula's reach (as the oracle's literal mode)
         const double H = p.t_max > 0.0 ? p.t_max : p.horizon;
-        o << "#define SMC_BLOCK 128\n#define SMC_MINB 2\n#define SMC_PIPE2 0\n";
+        int minb = 2;                       // resident 128-thread CTAs the registers must allow
+        if (const char* e = std::getenv("SMC_LIT_MINB")) minb = std::max(1, std::atoi(e));
+        o << "#define SMC_BLOCK 128\n#define SMC_MINB " << minb << "\n#define SMC_PIPE2 0\n";
         o << "#define SMC_LIT_H " << dlit(H) << "\n#define SMC_LIT_NODES " << p.lnodes.size() << "\n";
     } else if (variant == 1) {
         // >= 4 resident CTAs of 128 threads: at most 128 registers per thread

@@ -11,7 +11,7 @@
 // Generated hooks (codegen.cpp): as variant 1, plus smc_lit_mask, the SmcWN node table
 // and SMC_LIT_H.
 
-extern "C" __global__ void __launch_bounds__(SMC_BLOCK, 2) smc_ssa_literal(SmcParams P) {
+extern "C" __global__ void __launch_bounds__(SMC_BLOCK, SMC_MINB) smc_ssa_literal(SmcParams P) {
     const smc_u64 gtid = (smc_u64)blockIdx.x * blockDim.x + threadIdx.x;
     const double* __restrict__ H = (const double*)P.tables;
     const unsigned me = 1u << (threadIdx.x & 31u);
