@@ -1263,6 +1263,10 @@ std::string generate_source(const Model& m, const Property& p, int variant, cons
         if (const char* e = std::getenv("SMC_UNROLL")) o << "#define SMC_UNROLL " << std::atoi(e) << "\n";
         if (const char* e = std::getenv("SMC_BURST")) o << "#define SMC_BURST " << std::max(1, std::atoi(e)) << "\n";
     } else if (variant == 4) {
+        if (p.literal) {
+            const double H = p.t_max > 0.0 ? p.t_max : p.horizon;
+            o << "#define SMC_LIT_H " << dlit(H) << "\n";
+        }
         // 128-thread CTAs; resident CTAs per SM bounded by the counts' shared memory
         // (tables + 128 columns of N+1 ints) and by registers (pass 1 keeps the counts and
         // the group prefixes in registers): 3 by default (<= 168 registers; C4: 3 -> 1.19e10,

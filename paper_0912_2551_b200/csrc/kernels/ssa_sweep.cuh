@@ -232,7 +232,8 @@ extern "C" __global__ void __launch_bounds__(SMC_BLOCK, SMC_MINB) smc_ssa_sweep(
     double e_cur = 0.0, u_cur = 0.0;      // draw of the current step k
     smc_u32 k = 0;
     smc_u64 rel = 0, traj = 0;
-    SmcMon mon;
+    SmcMon mon;                            // a template monitor, or the window monitor (R27)
+    mon.bind(P, (smc_u64)blockIdx.x * blockDim.x + threadIdx.x, 1u << lane, (int)lane);
     bool busy = false, exhausted = false;
     smc_u32 c_true = 0, c_false = 0, c_err = 0;
     smc_i64 c_ev = 0;
@@ -343,16 +344,17 @@ extern "C" __global__ void __launch_bounds__(SMC_BLOCK, SMC_MINB) smc_ssa_sweep(
                         u_cur = u_nx;
                         mon.enter(k, t, tp, X);
                         v = mon.verdict();
-                        if (v < 0 && k >= cap) v = 2;
+                        if (v < 0 && k >= cap) v = mon.at_cap((long long)k);
                     }
                 }
             }
             if (v >= 0) {
-                if (v == 1) ++c_true;
-                else if (v == 0) ++c_false;
+                const smc_u32 ke = (v == 0 || v == 1) ? (smc_u32)mon.events((long long)k) : k;   // window monitor:
+                if (v == 1) ++c_true;                                                    // the first decision
+                else if (v == 0) ++c_false;                                              // index
                 else ++c_err;
-                c_ev += k;
-                if (P.verdicts) { P.verdicts[rel] = (unsigned char)v; P.events_out[rel] = (int)k; }
+                c_ev += ke;
+                if (P.verdicts) { P.verdicts[rel] = (unsigned char)v; P.events_out[rel] = (int)ke; }
                 busy = false;
             }
         }

@@ -227,7 +227,9 @@ PropKernel& prepare(Model& m, const Property& p) {
     // literal |= on the fly (reading R23): thread-owned models run variant 3, tile
     // models the tile kernel, both with the window monitor (R27)
     if (p.literal && pk.variant == 1) pk.variant = 3;
-    if (p.literal && (pk.variant == 4 || pk.variant == 5)) pk.variant = 2;   // the window monitor lives in the tile kernel
+    // (the sweep is thread-owned and hosts the window monitor like variant 3; the delta kernel
+    // does not, its formulas run the tile kernel)
+    if (p.literal && pk.variant == 5) pk.variant = 2;
     const TileLayout* tl = nullptr;
     const int v = pk.variant == 3 ? 1 : pk.variant;      // table set (variant 3 uses variant 1's)
     if (!d.tables_ready[v]) {
@@ -279,6 +281,10 @@ PropKernel& prepare(Model& m, const Property& p) {
         pk.lit_per_entry = window_bytes_per_entry(p);
     } else if (pk.variant == 4) {
         pk.block = tl->sw_blk;
+        if (p.literal) {                   // one window-monitor slot per thread (size_traces)
+            pk.lit_per_cta = pk.block;
+            pk.lit_per_entry = window_bytes_per_entry(p);
+        }
         pk.smem = (int)(tl->bytes + (size_t)pk.block * (tl->sw_xd ? 8 : 4) * (size_t)(m.N + 1));
         cudaFuncAttributes fa;
         ck(cudaFuncGetAttributes(&fa, fn), "cudaFuncGetAttributes");
@@ -896,7 +902,7 @@ int smc_kernel_source(smc_model* h, const smc_property* ph, char* buf, size_t* l
         const int mv = m.variant();
         const int v = (ph->p->literal && mv == 1) ? 3 : mv;
         TileLayout tl;
-        const int vv = (ph->p->literal && (v == 4 || v == 5)) ? 2 : v;
+        const int vv = (ph->p->literal && v == 5) ? 2 : v;
         if (vv == 2 || vv == 4) tl = pack_tables(m, vv == 4);
         if (vv == 5) tl = pack_delta_tables(m);
         std::string s = generate_source(m, *ph->p, vv, (vv == 2 || vv == 4 || vv == 5) ? &tl : nullptr);

@@ -45,6 +45,13 @@ def test_literal_variant_compiles():
     assert "smc_ssa_literal" in src
 
 
-def test_tile_recording_monitor_compiles():
-    src, _ = _compile(workloads.c4(), 0, "F[0,0.3](S0 < S1 + 3 & G[0.01,0.04](S0 < S1 + 3))")
+def test_window_monitor_compiles_in_tile_and_sweep():
+    """The window monitor (R27) in the sweep kernel (C4's default for nested formulas) and in
+    the tile kernel (forced variant 2, and the delta kernel's models)."""
+    f = "F[0,0.3](S0 < S1 + 3 & G[0.01,0.04](S0 < S1 + 3))"
+    src, _ = _compile(workloads.c4(), 0, f)
+    assert "smc_ssa_sweep" in src and "struct SmcMon" in src and "SmcWN<" in src
+    src, _ = _compile(workloads.c4(), 2, f)
     assert "smc_ssa_tile" in src and "struct SmcMon" in src and "SmcWN<" in src
+    src, _ = _compile(workloads.c5(), 0, f)
+    assert "smc_ssa_tile" in src and "struct SmcMon" in src

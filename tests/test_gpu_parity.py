@@ -549,13 +549,13 @@ def test_nested_formulas_tile_recording_monitor_vs_oracle(smc, case):
 
 
 def test_nested_formula_on_c4_tile_vs_oracle(smc):
-    """A formula outside R16 on the 50 x 200 network (tile-only model)."""
+    """A formula outside R16 on the 50 x 200 network (the sweep kernel with the window monitor)."""
     f = "F[0.01,0.03](X[0,0.0001](S1 > S0 - 40))"
     cfg = dict(workloads.c4(), formula=f)
     m, p = _pair(smc, cfg)
     v, e = m.run_verdicts(p, 0, 40, 4)
     v, e = v.cpu().numpy(), e.cpu().numpy().astype(np.int64)
-    assert m.last_launch(p)["variant"] == 2
+    assert m.last_launch(p)["variant"] == 4                 # the sweep hosts the window monitor
     oc, ov, oe = O.run(O.OracleModel(cfg), O.OracleFormula(f, cfg["species"]), 4, 0, 40, mode="literal")
     assert int(((v != ov) | (e != oe)).sum()) == 0
 

@@ -12,7 +12,7 @@ from oracle import oracle as O
 
 pytestmark = pytest.mark.gpu
 
-CASES = [("C3", "G[0,290](F[1,10](P1 < 400))", 3), ("C4", "F[0,10](G[0.001,1](S0 > S1))", 2)]
+CASES = [("C3", "G[0,290](F[1,10](P1 < 400))", 3), ("C4", "F[0,10](G[0.001,1](S0 > S1))", 4)]
 
 
 @pytest.mark.parametrize("name,formula,variant", CASES)

@@ -1,6 +1,7 @@
 """The window monitor on the GPU (readings R23/R27): random networks x random nested
 formulas (the generator of test_window_host.py) through the thread-owned literal kernel and
-the tile kernel at two tile widths (the tile's lanes split the pending positions), replica
+the tile kernel at two tile widths (the tile's lanes split the pending positions) and the
+sweep kernel (one lane per slot), replica
 for replica against the oracle's literal mode: verdicts and exact first decision indices
 (P:229-237), no replica errors."""
 import os
@@ -19,7 +20,7 @@ def test_window_monitor_random_nested_gpu(smc, seed):
     cfg, f = _fuzz_case(seed)
     n = 500
     oc, ov, oe = O.run(O.OracleModel(cfg), O.OracleFormula(f, cfg["species"]), seed, 0, n, mode="literal")
-    for variant, width in ((0, None), (2, "8"), (2, "32")):
+    for variant, width in ((0, None), (2, "8"), (2, "32"), (4, None)):
         if width:
             os.environ["SMC_TILE_WIDTH"] = width
         try:
