@@ -298,12 +298,20 @@ std::vector<WinNode> window_nodes(const Property& P) {
 }
 
 // ring entry bytes: t, tau; a (v, r) queue per node; F / G: two (index, r) deques; U: elapsed +
-// 32-byte state per pending position
+// 32-byte state per pending position.  Nodes with a single position (plim == 1: the root and
+// root-level booleans) keep theirs in a small area of SMC_WIN_SE entries per slot instead.
+static size_t node_entry_bytes(const WinNode& x) {
+    return 8 + ((x.n.k == LNode::F || x.n.k == LNode::G) ? 16 : (x.n.k == LNode::U ? 40 : 0));
+}
 size_t win_bytes(const Property& P) {
-    const auto w = window_nodes(P);
-    size_t b = 16 + 8 * w.size();
-    for (auto& x : w) b += (x.n.k == LNode::F || x.n.k == LNode::G) ? 16 : (x.n.k == LNode::U ? 40 : 0);
+    size_t b = 16;
+    for (auto& x : window_nodes(P)) if (x.plim != 1) b += node_entry_bytes(x);
     return b;
+}
+size_t win_small(const Property& P) {
+    size_t b = 0;
+    for (auto& x : window_nodes(P)) if (x.plim == 1) b += node_entry_bytes(x);
+    return 16 * b;
 }
 
 // smc_lit_mask(x): atom bit mask of a state; the node table of ssa_window.cuh
@@ -315,27 +323,39 @@ std::string window_code(const Property& P) {
     o << "    return mk;\n}\n";
     const auto w = window_nodes(P);
     o << "#define SMC_WIN_NODES " << w.size() << "\n#define SMC_WIN_ROOT " << w.size() - 1
-      << "\n#define SMC_WIN_PER_ENTRY " << win_bytes(P) << "\ntemplate <int I> struct SmcWN;\n";
-    size_t nu = 0, nfg = 0;
-    for (auto& x : w) { nu += x.n.k == LNode::U ? 1 : 0; nfg += (x.n.k == LNode::F || x.n.k == LNode::G) ? 1 : 0; }
-    // U: elapsed arrays, then 32-byte states; F / G: deques
-    size_t oel = 16 + 8 * w.size(), ost = oel + 8 * nu, odq = ost + 32 * nu;
+      << "\n#define SMC_WIN_PER_ENTRY " << win_bytes(P) << "\n#define SMC_WIN_SMALL " << win_small(P)
+      << "\n#define SMC_WIN_SE 16\ntemplate <int I> struct SmcWN;\n";
+    // offsets in bytes-per-entry units: big nodes within the W-entry arrays (queues, then U's
+    // elapsed and states, then F / G deques), small nodes within the SMC_WIN_SE-entry area
+    size_t oq[2] = {16, 0}, oel[2] = {0, 0}, ost[2] = {0, 0}, odq[2] = {0, 0};
+    for (int sm = 0; sm < 2; ++sm) {
+        size_t o = oq[sm];
+        for (auto& x : w) if ((x.plim == 1) == (sm == 1)) o += 8;
+        oel[sm] = o;
+        for (auto& x : w) if ((x.plim == 1) == (sm == 1) && x.n.k == LNode::U) o += 8;
+        ost[sm] = o;
+        for (auto& x : w) if ((x.plim == 1) == (sm == 1) && x.n.k == LNode::U) o += 32;
+        odq[sm] = o;
+    }
     for (size_t i = 0; i < w.size(); ++i) {
         const WinNode& x = w[i];
         const bool isu = x.n.k == LNode::U, isfg = x.n.k == LNode::F || x.n.k == LNode::G;
         const bool fin = x.n.I.finite();
+        const int sm = x.plim == 1 ? 1 : 0;
         o << "template <> struct SmcWN<" << i << "> {   // " << (int)x.n.k << "\n"
           << "    static constexpr int kind = " << (int)x.n.k << ", a = " << x.a << ", b = " << x.b
           << ", atom = " << x.n.atom << ", par = " << x.par << ";\n"
           << "    static constexpr double lo = " << dlit(x.n.I.lo) << ", hi = " << dlit(fin ? x.n.I.hi : 0.0)
           << ", tlim = " << dlit(x.tlim) << ";\n"
           << "    static constexpr bool lo_open = " << (x.n.I.lo_open ? "true" : "false")
-          << ", hi_open = " << (x.n.I.hi_open ? "true" : "false") << ", hi_inf = " << (fin ? "false" : "true") << ";\n"
+          << ", hi_open = " << (x.n.I.hi_open ? "true" : "false") << ", hi_inf = " << (fin ? "false" : "true")
+          << ", small = " << (sm ? "true" : "false") << ";\n"
           << "    static constexpr int plim = " << x.plim << ";\n"
-          << "    static constexpr long long oq = " << 16 + 8 * i << ", oel = " << (isu ? oel : 0)
-          << ", ost = " << (isu ? ost : 0) << ", odq = " << (isfg ? odq : 0) << ";\n};\n";
-        if (isu) { oel += 8; ost += 32; }
-        if (isfg) odq += 16;
+          << "    static constexpr long long oq = " << oq[sm] << ", oel = " << (isu ? oel[sm] : 0)
+          << ", ost = " << (isu ? ost[sm] : 0) << ", odq = " << (isfg ? odq[sm] : 0) << ";\n};\n";
+        oq[sm] += 8;
+        if (isu) { oel[sm] += 8; ost[sm] += 32; }
+        if (isfg) odq[sm] += 16;
     }
     return o.str();
 }
@@ -1233,6 +1253,7 @@ TileLayout pack_tables(const Model& m, bool sweep) {
 }
 
 size_t window_bytes_per_entry(const Property& p) { return win_bytes(p); }
+size_t window_small_bytes(const Property& p) { return win_small(p); }
 
 std::string generate_source(const Model& m, const Property& p, int variant, const TileLayout* tl) {
     std::ostringstream o;

@@ -88,18 +88,25 @@ struct SmcMon {
 
     __device__ __forceinline__ double* tt() const { return (double*)S; }
     __device__ __forceinline__ double* tau() const { return (double*)(S + (long long)8 * W); }
-    template <int I> __device__ __forceinline__ smc_u64* q() const { return (smc_u64*)(S + (long long)SmcWN<I>::oq * W); }
-    template <int I> __device__ __forceinline__ SmcWSt* st() const { return (SmcWSt*)(S + (long long)SmcWN<I>::ost * W); }
-    template <int I> __device__ __forceinline__ double* elp() const { return (double*)(S + (long long)SmcWN<I>::oel * W); }
+    // array of node I at offset `off` (bytes-per-entry units): W entries, or SMC_WIN_SE entries
+    // in the small area for single-position nodes (their indices stay below 2)
+    template <int I> __device__ __forceinline__ char* arr(long long off) const {
+        if constexpr (SmcWN<I>::small) return S + (long long)W * SMC_WIN_PER_ENTRY + off * SMC_WIN_SE;
+        else return S + off * W;
+    }
+    template <int I> __device__ __forceinline__ long long len() const { return SmcWN<I>::small ? SMC_WIN_SE : W; }
+    template <int I> __device__ __forceinline__ smc_u64* q() const { return (smc_u64*)arr<I>(SmcWN<I>::oq); }
+    template <int I> __device__ __forceinline__ SmcWSt* st() const { return (SmcWSt*)arr<I>(SmcWN<I>::ost); }
+    template <int I> __device__ __forceinline__ double* elp() const { return (double*)arr<I>(SmcWN<I>::oel); }
     // F / G deques of (child index, r)
-    template <int I> __device__ __forceinline__ int2* dqt() const { return (int2*)(S + (long long)SmcWN<I>::odq * W); }
-    template <int I> __device__ __forceinline__ int2* dqz() const { return (int2*)(S + (long long)SmcWN<I>::odq * W + 8ll * W); }
+    template <int I> __device__ __forceinline__ int2* dqt() const { return (int2*)arr<I>(SmcWN<I>::odq); }
+    template <int I> __device__ __forceinline__ int2* dqz() const { return (int2*)(arr<I>(SmcWN<I>::odq) + 8 * len<I>()); }
     __device__ __forceinline__ void sync() const { if (nl > 1) __syncwarp(gm); }
 
     __device__ __forceinline__ void bind(const SmcParams& Q, smc_u64 slot, unsigned mask, int lead) {
         W = (int)Q.lit_cap;
         msk = W - 1;
-        S = (char*)Q.lit_t + slot * (smc_u64)W * (smc_u64)SMC_WIN_PER_ENTRY;
+        S = (char*)Q.lit_t + slot * ((smc_u64)W * (smc_u64)SMC_WIN_PER_ENTRY + (smc_u64)SMC_WIN_SMALL);
         gm = mask;
         leader = lead;
         nl = __popc(mask);

@@ -103,7 +103,7 @@ struct PropKernel {
     // window monitor (formulas outside the streaming templates, R27): per-slot rings
     double* lit_t = nullptr;               // all slots' rings
     unsigned long long lit_cap = 0;        // ring entries per replica slot of the current launch
-    size_t lit_entries = 0, lit_per_entry = 0;
+    size_t lit_bytes = 0, lit_per_entry = 0, lit_small = 0;
     int lit_per_cta = 0;                   // replica slots per CTA (0: no window monitor)
     smc_launch_info info{};
     uint64_t cap_global = 0;               // sum of capacity() over the ranks (one allreduce)
@@ -185,34 +185,37 @@ DeviceState& device(Model& m) {
 
 // Rings of the window monitor (ssa_window.cuh, readings R23/R27), sized PER LAUNCH: every
 // replica slot of the `grid` CTAs (`per_cta` slots each) gets W ring entries of
-// `lit_per_entry` bytes, W the largest power of two up to SMC_WIN_W (default 32768) within the
-// budget (half the free device memory, at most 64 GiB); a launch that cannot give every slot
-// 1024 entries runs fewer resident CTAs.  The rings hold the formula's windows
+// `lit_per_entry` bytes (+ a small area for the single-position nodes), W the largest power of
+// two up to SMC_WIN_W (default 32768) within the budget (60 % of the free device memory, at most
+// 100 GiB: the B200's HBM holds C4's one-time-unit windows for every resident lane); a launch
+// that cannot give every slot 1024 entries runs fewer resident CTAs.  The rings hold the formula's windows
 // (not the trace), so W bounds how many entries one window may span; a replica whose window
 // would overflow its ring ends as an error.
 void size_traces(Model& m, PropKernel& pk, int per_cta, int& grid) {
     (void)m;
     size_t free_b = 0, total_b = 0;
     ck(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
-    const size_t held = (size_t)pk.lit_entries * pk.lit_per_entry;   // ours, reusable
-    const size_t budget = std::min<size_t>((free_b + held) / 2, (size_t)64 << 30);
-    const size_t per_entry = pk.lit_per_entry;
+    const size_t held = pk.lit_bytes;                                  // ours, reusable
+    const size_t budget = std::min<size_t>((size_t)((double)(free_b + held) * 0.6), (size_t)100 << 30);
+    const size_t per_entry = pk.lit_per_entry, small = pk.lit_small;
     size_t want = 32768;
     if (const char* e = std::getenv("SMC_WIN_W")) want = std::max<size_t>(16, std::strtoull(e, nullptr, 10));
     const size_t min_cap = std::min<size_t>(want, 1024);
-    if (budget / ((size_t)grid * (size_t)per_cta * per_entry) < min_cap)
-        grid = (int)std::max<size_t>(1, budget / (min_cap * per_entry * (size_t)per_cta));
+    if (budget / ((size_t)grid * (size_t)per_cta) < min_cap * per_entry + small)
+        grid = (int)std::max<size_t>(1, budget / ((min_cap * per_entry + small) * (size_t)per_cta));
     const size_t slots = (size_t)grid * (size_t)per_cta;
-    size_t lim = std::min<size_t>(budget / (slots * per_entry), want);
+    const size_t per_slot = budget / slots;
+    size_t lim = per_slot > small ? std::min<size_t>((per_slot - small) / per_entry, want) : 0;
     size_t cap = 1;
     while (cap * 2 <= lim) cap *= 2;
     if (cap < 16) fail(SMC_E_CUDA, "window monitor: not enough device memory for the rings");
-    if (slots * cap > pk.lit_entries) {
+    const size_t need = slots * (cap * per_entry + small);
+    if (need > pk.lit_bytes) {
         dfree(pk.lit_t);
         pk.lit_t = nullptr;
-        pk.lit_entries = 0;
-        pk.lit_t = (double*)dalloc(slots * cap * per_entry);
-        pk.lit_entries = slots * cap;
+        pk.lit_bytes = 0;
+        pk.lit_t = (double*)dalloc(need);
+        pk.lit_bytes = need;
     }
     pk.lit_cap = cap;
 }
@@ -279,11 +282,13 @@ PropKernel& prepare(Model& m, const Property& p) {
         pk.smem = 0;
         pk.lit_per_cta = pk.block;          // rings sized per launch (size_traces)
         pk.lit_per_entry = window_bytes_per_entry(p);
+        pk.lit_small = window_small_bytes(p);
     } else if (pk.variant == 4) {
         pk.block = tl->sw_blk;
         if (p.literal) {                   // one window-monitor slot per thread (size_traces)
             pk.lit_per_cta = pk.block;
             pk.lit_per_entry = window_bytes_per_entry(p);
+            pk.lit_small = window_small_bytes(p);
         }
         pk.smem = (int)(tl->bytes + (size_t)pk.block * (tl->sw_xd ? 8 : 4) * (size_t)(m.N + 1));
         cudaFuncAttributes fa;
@@ -345,6 +350,7 @@ PropKernel& prepare(Model& m, const Property& p) {
         if (p.literal) {                   // one ring slot per tile, sized per launch (size_traces)
             pk.lit_per_cta = best_w * pk.per_warp;
             pk.lit_per_entry = window_bytes_per_entry(p);
+            pk.lit_small = window_small_bytes(p);
         }
     }
     pk.info.variant = pk.variant;

@@ -186,6 +186,8 @@ HillTables pack_hill_tables(const Model& m);
 std::string generate_source(const Model& m, const Property& p, int variant, const TileLayout* tl);
 // bytes per ring entry of one replica slot of the window monitor (ssa_window.cuh, R27)
 size_t window_bytes_per_entry(const Property& p);
+// bytes per replica slot of the single-position nodes' small area
+size_t window_small_bytes(const Property& p);
 std::string embedded_source(const char* name);   // kernels/*.cuh embedded at build time
 
 // -------------------------------------------------------------------- jit ---

@@ -52,7 +52,7 @@ static std::vector<char> g_buf;
 extern "C" int win_check(const double* t, const double* tau, const long long* x, int N, long long ne, int absorbed,
                          long long W, long long cap, long long* events) {
     SmcParams P;
-    g_buf.assign((size_t)W * SMC_WIN_PER_ENTRY, 0);
+    g_buf.assign((size_t)W * SMC_WIN_PER_ENTRY + SMC_WIN_SMALL, 0);
     P.lit_t = (double*)g_buf.data();
     P.lit_cap = (smc_u64)W;
     SmcMon mon;
