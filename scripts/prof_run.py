@@ -21,7 +21,7 @@ import workloads  # noqa: E402
 def main():
     name, n = sys.argv[1], int(sys.argv[2])
     cfg = workloads.get(name)
-    if len(sys.argv) > 3:
+    if len(sys.argv) > 3 and sys.argv[3]:
         cfg = dict(cfg, formula=sys.argv[3])
     torch.cuda.set_device(0)
     smc.use_torch()
