@@ -15,7 +15,7 @@ timeout 900 python bench.py --workload C4 --formula "F[0,10](G[0.001,1](S0 > S1)
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches_default.csv \
     python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/${TAG}_ncu_launches.log 2>&1; echo "launches rc=$?"
 prof() {  # W N [formula]
-  mkdir -p gpurun_out/cubin_${TAG}_$1$3tag
+  mkdir -p gpurun_out/cubin_${TAG}_$1$4
   timeout 600 python scripts/prof_run.py $1 $2 "$3" > gpurun_out/${TAG}_plain_$1$4.log 2>&1 && \
   SMC_DUMP_CUBIN=gpurun_out/cubin_${TAG}_$1$4 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:smc_ssa -s 1 -c 1 \
       -o gpurun_out/${TAG}_prof_$1$4 python scripts/prof_run.py $1 $2 "$3" > gpurun_out/${TAG}_ncu_$1$4.log 2>&1
