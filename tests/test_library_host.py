@@ -136,10 +136,11 @@ def test_variant_selection_and_errors():
     for bad in (3, 6, -1, 1):            # 3 is the literal variant (chosen by the formula), 1 needs N, M <= 32
         with pytest.raises(smc.SmcError):
             m.set_variant(bad)
-    # a literal (nested) formula on a sweep model runs the tile kernel's recording monitor
+    # a literal (nested) formula on a sweep model runs the sweep kernel with the window monitor (R27)
     m.set_variant(4)
     lp = smc.Property(m, "F[0,1](G[0.5,1](S0 > S1))")
-    assert "smc_ssa_tile" in m.kernel_source(lp)
+    src = m.kernel_source(lp)
+    assert "smc_ssa_sweep" in src and "SmcWN<" in src
     # the counts of 128 trajectories must fit in shared memory
     big = dict(cfg, species=["S%d" % i for i in range(500)], x0=[1] * 500)
     mb = smc.Model.from_config(big)
