@@ -66,3 +66,34 @@ def test_two_ranks_on_device_equal_one(smc):
     for r in range(world):
         for name, *_ in CASES:
             assert out[r][name] == ref[name], (r, name, out[r][name], ref[name])
+
+
+def _nccl_rank_main(rank, world, port, out):
+    import torch
+    import torch.distributed as dist
+
+    import paper_0912_2551_b200 as smc
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", 0))
+    smc.use_torch()
+    smc.set_allreduce_torch(device=True)            # the hook bench.py installs at N > 1
+    res = {}
+    for name, n, conf, eps in CASES:
+        res[name] = _work(smc, workloads.get(name), n, conf, eps)
+    out[rank] = res
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_nccl_hook_one_rank_equals_no_hook(smc):
+    """The device-pointer allreduce through NCCL itself (one rank: the only NCCL group one GPU
+    can hold): every round's int64[4] counts go through ncclAllReduce on the device pointer
+    and the results equal the hook-less run bit for bit."""
+    ref = {name: _work(smc, workloads.get(name), n, conf, eps) for name, n, conf, eps in CASES}
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.start_processes(_nccl_rank_main, args=(1, _free_port(), out), nprocs=1, join=True, start_method="spawn")
+    for name, *_ in CASES:
+        assert out[0][name] == ref[name], (name, out[0][name], ref[name])
