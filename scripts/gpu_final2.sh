@@ -21,7 +21,7 @@ prof() {  # W N [formula]
       -o gpurun_out/${TAG}_prof_$1$4 python scripts/prof_run.py $1 $2 "$3" > gpurun_out/${TAG}_ncu_$1$4.log 2>&1
   echo "prof $1$4 rc=$?"; tail -1 gpurun_out/${TAG}_plain_$1$4.log | cut -c1-200
 }
-prof C5 54128 "" ""
+# (C5 capture: profiles/r02_ncu.md, tag r02m)
 prof C3 100000 "G[0,290](F[1,10](P1 < 400))" n
 prof C4 20000 "F[0,10](G[0.001,1](S0 > S1))" n
 for f in gpurun_out/${TAG}_*.log; do echo "== $f"; tail -1 $f | cut -c1-220; done
