@@ -84,15 +84,20 @@ def main(state_path, budget_s, chunk):
             else:
                 lo, hi = smc.smc_wilson_interval(st["n_true"], st["n_tot"], conf)
                 st.update(done=True, p_hat=p_hat, lower=lo, upper=hi)
+        if not st["done"] and st["n_tot"] > 0:                         # progress record (not part of Fig. 2)
+            lo, hi = smc.smc_wilson_interval(st["n_true"], st["n_tot"], conf)
+            st["interim"] = dict(p_hat=st["n_true"] / st["n_tot"], lower=lo, upper=hi, half_width=(hi - lo) / 2,
+                                 target_n_tot=st["n_tot"] + st["round_end"] - st["cursor"])
         json.dump(dict(st, device_seconds=st["device_seconds"] + dev_s), open(state_path, "w"), indent=1)
     clocks.window = (t0, time.time())
     clk = clocks.stop()
     st["device_seconds"] += dev_s
     st["calls"].append(dict(device_seconds=dev_s, wall_seconds=time.time() - t0, clocks=clk,
                             gpu=torch.cuda.get_device_name(0), variant=m.last_launch(p)["variant"]))
+    st["events_per_s"] = st["events"] / st["device_seconds"]
+    st["trajectories_per_s"] = st["n_tot"] / st["device_seconds"]
     if st["done"]:
-        st["events_per_s"] = st["events"] / st["device_seconds"]
-        st["trajectories_per_s"] = st["n_tot"] / st["device_seconds"]
+        st.pop("interim", None)
     json.dump(st, open(state_path, "w"), indent=1)
     print(json.dumps(st))
 

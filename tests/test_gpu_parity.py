@@ -94,8 +94,7 @@ def test_c2_wilson_estimate(smc):
 def test_c3_replicas(smc, variant):
     cfg = workloads.c3()
     a, ae, *_ = _compare(smc, cfg, cfg["seed"], 0, 400, variant)
-    assert a >= 0.995 and ae >= 0.995          # 400 replicas: one flip allowed at most
-    assert a == 1.0 or a * 400 >= 399
+    assert a == 1.0 and ae == 1.0              # 400 replicas: 0 mismatches (verdict and event count)
 
 
 def test_c3r_stress(smc):
