@@ -178,10 +178,15 @@ def use_torch(allocator=True, stream=True):
     launches onto torch's current CUDA stream."""
     import torch
     if allocator:
+        big = {}                    # blocks of >= 1 GiB (the window monitor's rings)
+
         def alloc(size, user):
             try:
-                return torch.cuda.caching_allocator_alloc(int(size), device=torch.cuda.current_device(),
-                                                          stream=torch.cuda.current_stream())
+                ptr = torch.cuda.caching_allocator_alloc(int(size), device=torch.cuda.current_device(),
+                                                         stream=torch.cuda.current_stream())
+                if int(size) >= (1 << 30):
+                    big[int(ptr)] = int(size)
+                return ptr
             except Exception:
                 import traceback
                 traceback.print_exc()
@@ -190,6 +195,10 @@ def use_torch(allocator=True, stream=True):
         def free(ptr, user):
             if ptr and torch is not None and getattr(torch, "cuda", None) is not None:   # not at interpreter exit
                 torch.cuda.caching_allocator_delete(int(ptr))
+                # the library sizes the rings from cudaMemGetInfo, which does not see blocks
+                # cached by torch: hand a freed ring back to the driver
+                if big.pop(int(ptr), None):
+                    torch.cuda.empty_cache()
         a, f = ALLOC_FN(alloc), FREE_FN(free)
         _keep.extend([a, f])
         check(lib().smc_set_allocator(a, f, None))

@@ -188,7 +188,8 @@ DeviceState& device(Model& m) {
 // `lit_per_entry` bytes (+ a small area for the single-position nodes), W the largest power of
 // two up to SMC_WIN_W (default 32768) within the budget (60 % of the free device memory, at most
 // 100 GiB: the B200's HBM holds C4's one-time-unit windows for every resident lane); a launch
-// that cannot give every slot 1024 entries runs fewer resident CTAs.  The rings hold the formula's windows
+// that cannot give every slot the full W runs down to half as many resident CTAs first, and one
+// that cannot give every slot 1024 entries fewer still.  The rings hold the formula's windows
 // (not the trace), so W bounds how many entries one window may span; a replica whose window
 // would overflow its ring ends as an error.
 void size_traces(Model& m, PropKernel& pk, int per_cta, int& grid) {
@@ -201,6 +202,13 @@ void size_traces(Model& m, PropKernel& pk, int per_cta, int& grid) {
     size_t want = 32768;
     if (const char* e = std::getenv("SMC_WIN_W")) want = std::max<size_t>(16, std::strtoull(e, nullptr, 10));
     const size_t min_cap = std::min<size_t>(want, 1024);
+    // capacity before residency: a window that overflows its ring ends the replica as an
+    // error, fewer resident CTAs only cost time -- when the budget cannot give every slot
+    // the full W, up to half of the CTAs are given up before W is halved
+    {
+        const size_t g_fit = budget / ((want * per_entry + small) * (size_t)per_cta);
+        if (g_fit < (size_t)grid) grid = (int)std::max<size_t>(g_fit, std::max<size_t>(1, (size_t)grid / 2));
+    }
     if (budget / ((size_t)grid * (size_t)per_cta) < min_cap * per_entry + small)
         grid = (int)std::max<size_t>(1, budget / ((min_cap * per_entry + small) * (size_t)per_cta));
     const size_t slots = (size_t)grid * (size_t)per_cta;
