@@ -1,7 +1,9 @@
 """Nested formulas outside the streaming templates (non-zero inner lower bounds; readings
-R23/R27) at the FULL horizons of C3 and C4 -- traces of 17k-29k entries, several times the
-window monitor's ring (<= 4,096 entries per replica slot: memory bounded by the formula's
-windows, not the trace) -- in MACHINE-FILLING launches of 10^5 replicas: no replica ends in
+R23/R27) at the FULL horizons of C3 and C4 -- traces of 17k-29k entries, the window
+monitor's rings (<= 32,768 entries per replica slot) holding one inner window, not the trace
+(C4's G[0.001,1] windows reach ~17.6k entries) -- in MACHINE-FILLING launches of 10^5
+replicas, run one after the other in one process (the second sizes its rings from the memory
+the first gave back): no replica ends in
 error, and the first 2,000 replicas' verdicts AND event counts equal the oracle's literal
 mode exactly (the exact first decision index of P:291-294, R24)."""
 import numpy as np
