@@ -231,6 +231,15 @@ int64_t smc_wilson_sample_size(double p, double half_width, double confidence);
 /* Rank r's slice [lo, hi) of the round range [base, base + n) over `world` ranks:
  * lo = base + floor(r n / world), hi = base + floor((r+1) n / world). */
 int smc_shard_range(uint64_t base, uint64_t n, int32_t rank, int32_t world, uint64_t* lo, uint64_t* hi);
+/* Ring plan of the window monitor (formulas outside the streaming templates, P:229-237;
+ * DESIGN reading R27) for one launch; host arithmetic only, no device access.  `grid` CTAs
+ * of `per_cta` replica slots each share `budget_bytes`; a slot needs W * per_entry + small
+ * bytes for rings of W entries.  W is the largest power of two <= want that fits, after
+ * giving up CTAs in this order: down to max(1, grid/2) CTAs to reach W = want, then as many
+ * as needed to reach W = min(want, 1024).  *grid_out <= grid CTAs, *cap_out = W.
+ * SMC_E_ARG on a zero size or count; SMC_E_CUDA ("not enough device memory") if W < 16. */
+int smc_window_ring_plan(uint64_t budget_bytes, uint64_t per_entry, uint64_t small, int32_t per_cta, int32_t grid,
+                         uint64_t want, int32_t* grid_out, uint64_t* cap_out);
 
 /* ------------------------------------------------------------------------ */
 /* Integration hooks (PyTorch owns device memory, streams, process groups)    */

@@ -10,7 +10,7 @@ kernel calls) every call raises.
 """
 from ._native import (  # noqa: F401
     SmcError, lib, smc_last_error,
-    smc_normal_quantile, smc_wilson_interval, smc_wilson_sample_size, smc_shard_range,
+    smc_normal_quantile, smc_wilson_interval, smc_wilson_sample_size, smc_shard_range, smc_window_ring_plan,
     smc_philox_blocks, smc_draw_blocks, smc_set_shard, smc_set_stream,
 )
 from .api import (  # noqa: F401

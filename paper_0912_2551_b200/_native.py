@@ -54,6 +54,8 @@ SIGNATURES = [
     ("smc_wilson_interval", c_i32, [c_i64, c_i64, c_dbl, ctypes.POINTER(c_dbl), ctypes.POINTER(c_dbl)]),
     ("smc_wilson_sample_size", c_i64, [c_dbl, c_dbl, c_dbl]),
     ("smc_shard_range", c_i32, [c_u64, c_u64, c_i32, c_i32, ctypes.POINTER(c_u64), ctypes.POINTER(c_u64)]),
+    ("smc_window_ring_plan", c_i32, [c_u64, c_u64, c_u64, c_i32, c_i32, c_u64, ctypes.POINTER(c_i32),
+                                     ctypes.POINTER(c_u64)]),
     ("smc_set_allocator", c_i32, [ALLOC_FN, FREE_FN, c_vp]),
     ("smc_set_stream", c_i32, [c_vp]),
     ("smc_set_shard", c_i32, [c_i32, c_i32]),
@@ -127,6 +129,13 @@ def smc_shard_range(base, n, rank, world):
     lo, hi = c_u64(), c_u64()
     check(lib().smc_shard_range(base, n, rank, world, ctypes.byref(lo), ctypes.byref(hi)))
     return lo.value, hi.value
+
+
+def smc_window_ring_plan(budget_bytes, per_entry, small, per_cta, grid, want=32768):
+    g, cap = c_i32(), c_u64()
+    check(lib().smc_window_ring_plan(budget_bytes, per_entry, small, per_cta, grid, want, ctypes.byref(g),
+                                     ctypes.byref(cap)))
+    return g.value, cap.value
 
 
 def smc_philox_blocks(seed, trajectory, step0, n):

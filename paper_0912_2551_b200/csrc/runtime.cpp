@@ -198,26 +198,14 @@ void size_traces(Model& m, PropKernel& pk, int per_cta, int& grid) {
     ck(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
     const size_t held = pk.lit_bytes;                                  // ours, reusable
     const size_t budget = std::min<size_t>((size_t)((double)(free_b + held) * 0.6), (size_t)100 << 30);
-    const size_t per_entry = pk.lit_per_entry, small = pk.lit_small;
     size_t want = 32768;
     if (const char* e = std::getenv("SMC_WIN_W")) want = std::max<size_t>(16, std::strtoull(e, nullptr, 10));
-    const size_t min_cap = std::min<size_t>(want, 1024);
-    // capacity before residency: a window that overflows its ring ends the replica as an
-    // error, fewer resident CTAs only cost time -- when the budget cannot give every slot
-    // the full W, up to half of the CTAs are given up before W is halved
-    {
-        const size_t g_fit = budget / ((want * per_entry + small) * (size_t)per_cta);
-        if (g_fit < (size_t)grid) grid = (int)std::max<size_t>(g_fit, std::max<size_t>(1, (size_t)grid / 2));
-    }
-    if (budget / ((size_t)grid * (size_t)per_cta) < min_cap * per_entry + small)
-        grid = (int)std::max<size_t>(1, budget / ((min_cap * per_entry + small) * (size_t)per_cta));
-    const size_t slots = (size_t)grid * (size_t)per_cta;
-    const size_t per_slot = budget / slots;
-    size_t lim = per_slot > small ? std::min<size_t>((per_slot - small) / per_entry, want) : 0;
-    size_t cap = 1;
-    while (cap * 2 <= lim) cap *= 2;
-    if (cap < 16) fail(SMC_E_CUDA, "window monitor: not enough device memory for the rings");
-    const size_t need = slots * (cap * per_entry + small);
+    int32_t g = grid;
+    uint64_t cap = 0;
+    if (smc_window_ring_plan(budget, pk.lit_per_entry, pk.lit_small, per_cta, grid, want, &g, &cap) != SMC_OK)
+        fail(SMC_E_CUDA, "window monitor: not enough device memory for the rings");
+    grid = g;
+    const size_t need = (size_t)grid * (size_t)per_cta * ((size_t)cap * pk.lit_per_entry + pk.lit_small);
     if (need > pk.lit_bytes) {
         dfree(pk.lit_t);
         pk.lit_t = nullptr;
@@ -928,3 +916,31 @@ int smc_kernel_source(smc_model* h, const smc_property* ph, char* buf, size_t* l
 }
 
 }  // extern "C"
+
+// The window monitor's ring plan (smc.h; DESIGN R27).  Capacity before residency: a window
+// that overflows its ring ends the replica as an error, fewer resident CTAs only cost time.
+extern "C" int smc_window_ring_plan(uint64_t budget, uint64_t per_entry, uint64_t small, int32_t per_cta, int32_t grid,
+                                    uint64_t want, int32_t* grid_out, uint64_t* cap_out) {
+    if (per_entry == 0 || per_cta < 1 || grid < 1 || want < 1 || !grid_out || !cap_out) {
+        set_error("smc_window_ring_plan: sizes and counts must be positive");
+        return SMC_E_ARG;
+    }
+    uint64_t g = (uint64_t)grid;
+    const uint64_t pc = (uint64_t)per_cta;
+    const uint64_t g_fit = budget / ((want * per_entry + small) * pc);          // CTAs that get the full W
+    if (g_fit < g) g = std::max<uint64_t>(g_fit, std::max<uint64_t>(1, g / 2));
+    const uint64_t min_cap = std::min<uint64_t>(want, 1024);
+    if (budget / (g * pc) < min_cap * per_entry + small)
+        g = std::max<uint64_t>(1, budget / ((min_cap * per_entry + small) * pc));
+    const uint64_t per_slot = budget / (g * pc);
+    const uint64_t lim = per_slot > small ? std::min<uint64_t>((per_slot - small) / per_entry, want) : 0;
+    uint64_t cap = 1;
+    while (cap * 2 <= lim) cap *= 2;
+    *grid_out = (int32_t)g;
+    *cap_out = cap;
+    if (lim < 16) {
+        set_error("window monitor: not enough device memory for the rings");
+        return SMC_E_CUDA;
+    }
+    return SMC_OK;
+}

@@ -25,7 +25,7 @@ def header_symbols():
 def test_exports_every_declared_symbol():
     L = smc.lib()
     syms = header_symbols()
-    assert len(syms) == 29
+    assert len(syms) == 30
     for s in syms:
         assert hasattr(L, s), s
     assert sorted(n for n, _, _ in _native.SIGNATURES) == syms
@@ -237,3 +237,37 @@ def test_property_of_another_model_and_event_cap_bounds():
     with pytest.raises(smc.SmcError):
         m1.set_event_cap(2 ** 31)
     m1.set_event_cap(2 ** 31 - 1)
+
+
+def test_window_ring_plan():
+    """Ring plan of the window monitor (DESIGN R27; smc.h): capacity before residency."""
+    GiB = 1 << 30
+    pe, small, pc, grid = 48, 1024, 384, 148                 # C4's nested bench formula on the sweep kernel
+    full = grid * pc * (32768 * pe + small)
+    assert smc.smc_window_ring_plan(100 * GiB, pe, small, pc, grid) == (grid, 32768)       # fits: nothing given up
+    assert full <= 100 * GiB
+    g, cap = smc.smc_window_ring_plan(47 * GiB, pe, small, pc, grid)                       # the final pass's failure
+    assert cap == 32768 and grid // 2 <= g < grid and g * pc * (cap * pe + small) <= 47 * GiB
+    g, cap = smc.smc_window_ring_plan(20 * GiB, pe, small, pc, grid)                       # half the CTAs, then W halves
+    assert g == grid // 2 and cap == 8192 and g * pc * (cap * pe + small) <= 20 * GiB
+    g, cap = smc.smc_window_ring_plan(1 * GiB, pe, small, pc, grid)                        # W >= 1024 before residency
+    assert cap == 1024 and 1 <= g < grid // 2 and g * pc * (cap * pe + small) <= 1 * GiB
+    assert smc.smc_window_ring_plan(1 << 40, pe, small, pc, grid, 4096) == (grid, 4096)    # SMC_WIN_W
+    assert smc.smc_window_ring_plan(100 * GiB, pe, small, 128, 8) == (8, 32768)            # small launches untouched
+    g = np.random.default_rng(7)
+    for _ in range(2000):                                    # invariants: within budget, power of two, never more CTAs
+        b = int(g.integers(1 << 20, 1 << 38))
+        pe_, sm_ = int(g.integers(8, 200)), int(g.integers(0, 4096))
+        pc_, gr_ = int(g.integers(1, 1025)), int(g.integers(1, 600))
+        want = int(2 ** g.integers(4, 16))
+        try:
+            go, cap = smc.smc_window_ring_plan(b, pe_, sm_, pc_, gr_, want)
+        except smc.SmcError:
+            assert b // pc_ < 16 * pe_ + sm_ + pe_               # only when one CTA cannot hold 16 entries per slot
+            continue
+        assert 1 <= go <= gr_ and 16 <= cap <= want and cap & (cap - 1) == 0
+        assert go * pc_ * (cap * pe_ + sm_) <= b
+        if go < gr_:                                         # CTAs were given up only for capacity
+            assert (go + 1) * pc_ * (min(want, 1024) * pe_ + sm_) > b or go >= max(1, gr_ // 2)
+    with pytest.raises(smc.SmcError):
+        smc.smc_window_ring_plan(1 << 30, 0, 0, 128, 8)
